@@ -1,0 +1,233 @@
+/* SPDX-License-Identifier: Apache-2.0
+ *
+ * gridmath_b200 -- C ABI of the B200-native block-distributed GEMM path.
+ *
+ * The reference (dMath re-creation, C++20 library `gridmath`, reference
+ * proj/) has no FFI; its operator boundary is the C++ master API
+ * (proj/include/gridmath/session.hpp:62-179) and the worker op dispatch
+ * (proj/src/kernels.cpp:1138-1171). This header is the plain-C surface a
+ * binding (ctypes / cgo / JNI) attaches to. Two layers:
+ *
+ *   gm_session_* / gm_matrix_* / gm_gemm / gm_replicate_*   master API
+ *        -> mirrors gridmath::Session + gridmath::gemm  (session.hpp:62-162)
+ *   gm_device_* / gm_arena_* / gm_gemm_local / gm_convert / gm_pack_rect
+ *        -> the per-worker device layer the worker runtime calls
+ *           (replaces runGemm<T>, PoolAllocator, packRect/convertBuffer)
+ *
+ * Conventions: every function returns 0 on success and non-zero on error;
+ * the message is available from gm_last_error() (thread-local), mirroring the
+ * reference's gridmath::Error (proj/include/gridmath/common.hpp:11-14).
+ * Device pointers and `stream` (a cudaStream_t, NULL = legacy default stream)
+ * are plain pointers; there are no torch types anywhere in this ABI.
+ */
+#ifndef GRIDMATH_B200_H
+#define GRIDMATH_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Storage precision tags. 0/1/2 are the reference's gridmath::Precision
+ * values (proj/include/gridmath/precision.hpp:12) and keep their descriptor
+ * wire bytes; 3 is the new bf16 storage tag. */
+enum { GM_HALF = 0, GM_SINGLE = 1, GM_DOUBLE = 2, GM_BF16 = 3 };
+
+/* Math mode for Single-compute GEMMs, carried in OpDescriptor.flags[3]
+ * (unused by the reference's Gemm, kernels.cpp:209-211). */
+enum { GM_MATH_DEFAULT = 0, /* 3xTF32: fp32-accurate */
+       GM_MATH_TF32 = 1     /* 1xTF32: opt-in, ~1e-4 rel */ };
+
+/* Replication states (reference gridmath::ReplState, session.hpp:36). */
+enum { GM_REPL_IN_FLIGHT = 0, GM_REPL_DONE = 1, GM_REPL_FAILED = 2 };
+
+const char* gm_last_error(void);
+int gm_version(int32_t* major, int32_t* minor);
+
+/* ------------------------------------------------------------------------
+ * Device layer
+ * ---------------------------------------------------------------------- */
+
+int gm_device_count(int32_t* count);
+/* Binds the calling thread to `device` and warms the context. */
+int gm_device_init(int32_t device);
+int gm_device_synchronize(int32_t device);
+
+/* Per-worker pooled device arena (replaces gridmath::PoolAllocator,
+ * proj/include/gridmath/pool.hpp:13-67): power-of-two size classes from 256
+ * bytes, carved from large cudaMalloc slabs that are never returned until
+ * the arena dies, so steady-state ops perform zero cudaMalloc calls. */
+typedef struct gm_arena gm_arena;
+typedef struct {
+  uint64_t allocations_from_os; /* slab cudaMallocs */
+  uint64_t reuses;              /* allocations served from a free list */
+  uint64_t frees;
+  uint64_t held_bytes;          /* bytes parked in free lists */
+  uint64_t reserved_bytes;      /* bytes obtained from cudaMalloc */
+} gm_arena_stats;
+
+int gm_arena_create(int32_t device, uint64_t slab_bytes, gm_arena** out);
+int gm_arena_destroy(gm_arena* arena);
+int gm_arena_alloc(gm_arena* arena, uint64_t bytes, void** ptr);
+int gm_arena_free(gm_arena* arena, void* ptr);
+int gm_arena_get_stats(const gm_arena* arena, gm_arena_stats* out);
+
+/* One local block GEMM:  C = alpha * op(A) * op(B) + beta * C  on the
+ * calling thread's current device (replaces runGemm<T>,
+ * proj/src/kernels.cpp:445-558). All matrices are row-major with the given
+ * pitches (elements). op(A) is m x k (A stored k x m when trans_a), op(B) is
+ * k x n (B stored n x k when trans_b). Compute type follows
+ * kernels::computePrecision (kernels.cpp:136-140): Double if any operand is
+ * Double, else Single; two 16-bit operands of the same kind run natively on
+ * tcgen05 kind::f16 with fp32 accumulation. beta == 0 never reads C;
+ * alpha == 0 never reads A or B. */
+typedef struct {
+  uint64_t m, n, k;
+  uint64_t lda, ldb, ldc;
+  int32_t trans_a, trans_b;
+  int32_t prec_a, prec_b, prec_c;
+  int32_t math;      /* GM_MATH_* */
+  int32_t cta_group; /* 0 = default (2-SM UMMA), 1 = single-SM */
+  int32_t max_ctas;  /* 0 = all SMs */
+  double alpha, beta;
+} gm_gemm_desc;
+
+/* Device scratch bytes gm_gemm_local needs for `d` (operand conversion,
+ * 3xTF32 split, alignment staging). */
+int gm_gemm_workspace_size(const gm_gemm_desc* d, uint64_t* bytes);
+int gm_gemm_local(const gm_gemm_desc* d, const void* a, const void* b, void* c,
+                  void* workspace, uint64_t workspace_bytes, void* stream);
+
+/* Elementwise storage conversion (replaces gridmath::convertBuffer,
+ * proj/src/precision.cpp:6-28): RNE, Half overflow -> inf, Double->Half via
+ * float exactly as the reference. */
+int gm_convert(const void* src, int32_t src_prec, void* dst, int32_t dst_prec, uint64_t count,
+               void* stream);
+
+/* 2D sub-rectangle copy between row-major buffers (replaces packRect /
+ * unpackRect, proj/src/pieces.cpp:45-63). Pitches in elements. */
+int gm_copy_rect(const void* src, uint64_t src_ld, void* dst, uint64_t dst_ld, uint64_t rows,
+                 uint64_t cols, uint32_t elem_bytes, void* stream);
+
+/* Synthetic input generator: element i of the SplitMix64 stream seeded with
+ * `seed` (reference proj/include/gridmath/common.hpp:37-50) mapped to
+ * U[lo, hi), rounded RNE to `prec`, written row-major into the rectangle
+ * [r0, r0+rows) x [c0, c0+cols) of a `full_cols`-wide matrix held at `dst`
+ * with pitch `ld`. Identical values on host (oracle) and device. */
+int gm_fill_uniform(void* dst, int32_t prec, uint64_t ld, uint64_t r0, uint64_t rows, uint64_t c0,
+                    uint64_t cols, uint64_t full_cols, uint64_t seed, double lo, double hi,
+                    void* stream);
+
+/* ------------------------------------------------------------------------
+ * Layout helpers (pure host logic; reference proj/src/layout.cpp:13-114)
+ * ---------------------------------------------------------------------- */
+
+typedef struct {
+  uint64_t row_start, row_count, col_start, col_count;
+  uint32_t owner;
+} gm_tile;
+
+/* Each writes up to `cap` tiles into `out` and the count into *n. */
+int gm_layout_row_block(uint64_t rows, uint64_t cols, uint32_t workers, gm_tile* out,
+                        uint32_t cap, uint32_t* n);
+int gm_layout_col_block(uint64_t rows, uint64_t cols, uint32_t workers, gm_tile* out,
+                        uint32_t cap, uint32_t* n);
+int gm_layout_grid(uint64_t rows, uint64_t cols, uint32_t pr, uint32_t pc, gm_tile* out,
+                   uint32_t cap, uint32_t* n);
+/* 0 = ok, 1 = overlap, 2 = gap, 3 = out of range, 4 = unknown worker
+ * (reference LayoutViolation, layout.hpp:56). */
+int gm_layout_validate(uint64_t rows, uint64_t cols, const gm_tile* tiles, uint32_t n,
+                       uint32_t worker_count, int32_t* violation);
+
+/* ------------------------------------------------------------------------
+ * Master API (reference gridmath::Session, session.hpp:62-179)
+ * ---------------------------------------------------------------------- */
+
+typedef struct gm_session gm_session;
+
+typedef struct {
+  uint32_t workers;                 /* P, total worker count */
+  int32_t deterministic;            /* SessionOptions::deterministic (default 1) */
+  uint64_t replication_chunk_bytes; /* kept for wire compatibility */
+  uint64_t root_seed;
+  int32_t check_metadata_every_op;
+  /* B200 placement. Single process (spmd_rank < 0): worker r runs on device
+   * devices[r % num_devices] (num_devices == 0: all visible devices).
+   * SPMD (one process per GPU, torchrun): this process hosts worker
+   * spmd_rank on `devices[0]`; data plane is NCCL, bootstrapped from
+   * nccl_unique_id (128 bytes, same on every rank). */
+  int32_t spmd_rank;
+  int32_t num_devices;
+  int32_t devices[16];
+  uint8_t nccl_unique_id[128];
+  uint64_t arena_slab_bytes;        /* 0 = default */
+  int32_t gemm_max_ctas;            /* 0 = all SMs (cap leaves SMs for NCCL) */
+  int32_t transport;                /* 0 = auto, 1 = NCCL, 2 = copy-engine peer pulls */
+} gm_session_options;
+
+void gm_session_options_default(gm_session_options* o);
+int gm_session_create(const gm_session_options* opts, gm_session** out);
+int gm_session_destroy(gm_session* s);
+/* SPMD only: the NCCL unique id rank 0 must broadcast before create. */
+int gm_nccl_unique_id(uint8_t out[128]);
+
+int gm_matrix_create(gm_session* s, uint64_t rows, uint64_t cols, int32_t prec,
+                     const gm_tile* tiles, uint32_t ntiles, uint64_t* id);
+int gm_matrix_destroy(gm_session* s, uint64_t id);
+/* Full row-major image in storage precision. In SPMD mode every rank passes
+ * the full image and uploads only its own tiles. */
+int gm_matrix_set_raw(gm_session* s, uint64_t id, const void* host, uint64_t bytes);
+/* setData (double values, converted like convertBuffer), setDataF32. */
+int gm_matrix_set_f64(gm_session* s, uint64_t id, const double* host, uint64_t count);
+int gm_matrix_set_f32(gm_session* s, uint64_t id, const float* host, uint64_t count);
+/* Device-side generation of the synthetic SplitMix64 inputs (gm_fill_uniform
+ * semantics) straight into the owners' tiles; no host image needed. */
+int gm_matrix_fill_uniform(gm_session* s, uint64_t id, uint64_t seed, double lo, double hi);
+/* getDataRaw: full row-major image (SPMD: tiles not owned locally are
+ * gathered from their owners). */
+int gm_matrix_get_raw(gm_session* s, uint64_t id, void* host, uint64_t bytes);
+/* Copy only the locally owned tiles into `host` (a full-size image); the
+ * remaining bytes are left untouched. */
+int gm_matrix_get_local_raw(gm_session* s, uint64_t id, void* host, uint64_t bytes);
+int gm_matrix_info(gm_session* s, uint64_t id, uint64_t* rows, uint64_t* cols, int32_t* prec,
+                   uint64_t* version, uint64_t* replicated_version);
+
+/* gridmath::gemm (session.hpp:161-162): synchronous like the reference
+ * (returns once every worker finished; errors aggregated). */
+int gm_gemm(gm_session* s, uint64_t a, uint64_t b, uint64_t c, double alpha, double beta,
+            int32_t trans_a, int32_t trans_b);
+/* Same op with the Single-compute math mode in flags[3]. */
+int gm_gemm_ex(gm_session* s, uint64_t a, uint64_t b, uint64_t c, double alpha, double beta,
+               int32_t trans_a, int32_t trans_b, int32_t math);
+/* Asynchronous issue: enqueue on the workers' streams and return; pair
+ * with gm_session_synchronize. Used by the benchmark to time on-device. */
+int gm_gemm_async(gm_session* s, uint64_t a, uint64_t b, uint64_t c, double alpha, double beta,
+                  int32_t trans_a, int32_t trans_b);
+int gm_session_synchronize(gm_session* s);
+
+/* Replication (session.hpp:81-84). */
+int gm_replicate_async(gm_session* s, uint64_t id, uint64_t* version);
+int gm_replicate_sync(gm_session* s, uint64_t id);
+int gm_replicate_wait(gm_session* s, uint64_t id, uint64_t version, int32_t* state);
+int gm_replicate_state(gm_session* s, uint64_t id, uint64_t version, int32_t* state);
+
+/* Introspection (session.hpp:101-112). */
+typedef struct {
+  uint64_t os_allocations, reuses, frees, held_bytes, resident_bytes;
+  uint64_t cache_hits, cache_misses, cache_bytes; /* panel cache */
+  uint64_t bytes_sent, bytes_received;            /* data plane */
+} gm_worker_stats;
+int gm_query_worker_stats(gm_session* s, gm_worker_stats* rows, uint32_t cap, uint32_t* n);
+int gm_verify_metadata(gm_session* s);
+int gm_session_local_workers(gm_session* s, uint32_t* ranks, uint32_t cap, uint32_t* n);
+/* Device time of the last gm_gemm/gm_gemm_async per local worker (ms),
+ * measured with CUDA events on the worker's compute stream. */
+int gm_last_op_device_ms(gm_session* s, float* ms, uint32_t cap, uint32_t* n);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* GRIDMATH_B200_H */

@@ -1,0 +1,243 @@
+// SPDX-License-Identifier: Apache-2.0
+// Storage-precision conversion, rectangle staging, 3xTF32 operand split and
+// the SplitMix64 synthetic-input generator, all as HBM-bound grid-stride
+// kernels (one pass, coalesced along rows).
+//
+// Conversion semantics follow the reference's convertBuffer / storeScalar
+// (proj/src/precision.cpp:6-28, proj/include/gridmath/precision.hpp:42-149):
+//   * any -> Half rounds through float (double -> float -> half, RNE), values
+//     >= 65520 become +-inf, NaN keeps its top payload bits (or 1);
+//   * Double -> Single is RNE;  Half/Single/BF16 -> wider is exact;
+//   * BF16 (new tag 3) is RNE from float, and from double through float,
+//     matching the Half convention.
+#include <cuda_bf16.h>
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "convert.h"
+
+namespace gmk {
+
+__device__ __forceinline__ uint16_t f32_to_half_bits(float f) {
+  const uint32_t x = __float_as_uint(f);
+  if ((x & 0x7F800000u) == 0x7F800000u && (x & 0x007FFFFFu) != 0) {
+    // NaN: sign, all-ones exponent, payload = top 10 mantissa bits (never 0).
+    uint32_t pay = (x & 0x007FFFFFu) >> 13;
+    if (pay == 0) pay = 1;
+    return static_cast<uint16_t>(((x >> 16) & 0x8000u) | 0x7C00u | pay);
+  }
+  // Finite and inf: IEEE binary16 RNE (overflow -> inf) is exactly the
+  // reference's hand-rolled rounding.
+  return __half_as_ushort(__float2half_rn(f));
+}
+
+__device__ __forceinline__ float half_bits_to_f32(uint16_t h) {
+  const uint32_t sign = static_cast<uint32_t>(h & 0x8000u) << 16;
+  const uint32_t e = (h >> 10) & 0x1Fu;
+  const uint32_t m = h & 0x3FFu;
+  if (e == 31) return __uint_as_float(sign | 0x7F800000u | (m << 13));  // inf / NaN payload kept
+  return __half2float(__ushort_as_half(h));
+}
+
+__device__ __forceinline__ double load_elem(const void* base, int prec, uint64_t idx) {
+  switch (prec) {
+    case 0: return static_cast<double>(half_bits_to_f32(reinterpret_cast<const uint16_t*>(base)[idx]));
+    case 1: return static_cast<double>(reinterpret_cast<const float*>(base)[idx]);
+    case 2: return reinterpret_cast<const double*>(base)[idx];
+    default: {
+      const uint32_t b = static_cast<uint32_t>(reinterpret_cast<const uint16_t*>(base)[idx]) << 16;
+      return static_cast<double>(__uint_as_float(b));
+    }
+  }
+}
+
+__device__ __forceinline__ float load_elem_f32(const void* base, int prec, uint64_t idx) {
+  switch (prec) {
+    case 0: return half_bits_to_f32(reinterpret_cast<const uint16_t*>(base)[idx]);
+    case 1: return reinterpret_cast<const float*>(base)[idx];
+    case 2: return static_cast<float>(reinterpret_cast<const double*>(base)[idx]);
+    default: return __uint_as_float(static_cast<uint32_t>(reinterpret_cast<const uint16_t*>(base)[idx]) << 16);
+  }
+}
+
+__device__ __forceinline__ uint16_t f32_to_bf16_bits(float f) {
+  return __bfloat16_as_ushort(__float2bfloat16_rn(f));
+}
+
+__device__ __forceinline__ void store_elem(void* base, int prec, uint64_t idx, double v) {
+  switch (prec) {
+    case 0: reinterpret_cast<uint16_t*>(base)[idx] = f32_to_half_bits(__double2float_rn(v)); break;
+    case 1: reinterpret_cast<float*>(base)[idx] = __double2float_rn(v); break;
+    case 2: reinterpret_cast<double*>(base)[idx] = v; break;
+    default: reinterpret_cast<uint16_t*>(base)[idx] = f32_to_bf16_bits(__double2float_rn(v)); break;
+  }
+}
+
+__device__ __forceinline__ void store_elem_f32(void* base, int prec, uint64_t idx, float v) {
+  switch (prec) {
+    case 0: reinterpret_cast<uint16_t*>(base)[idx] = f32_to_half_bits(v); break;
+    case 1: reinterpret_cast<float*>(base)[idx] = v; break;
+    case 2: reinterpret_cast<double*>(base)[idx] = static_cast<double>(v); break;
+    default: reinterpret_cast<uint16_t*>(base)[idx] = f32_to_bf16_bits(v); break;
+  }
+}
+
+// Elementwise rectangle conversion. Single->Half takes the float fast path
+// (the reference's convertBuffer does the same; the results are identical).
+__global__ void convert_rect_kernel(const void* __restrict__ src, int sp, uint64_t sld,
+                                    void* __restrict__ dst, int dp, uint64_t dld, uint64_t rows,
+                                    uint64_t cols) {
+  const uint64_t total = rows * cols;
+  const bool via_f32 = (sp != 2 && dp != 2);
+  for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    const uint64_t r = i / cols, c = i % cols;
+    if (via_f32)
+      store_elem_f32(dst, dp, r * dld + c, load_elem_f32(src, sp, r * sld + c));
+    else
+      store_elem(dst, dp, r * dld + c, load_elem(src, sp, r * sld + c));
+  }
+}
+
+// 3xTF32 split: hi = tf32_rna(x) (low 13 mantissa bits zero), lo = x - hi.
+__global__ void split_tf32_kernel(const void* __restrict__ src, int sp, uint64_t sld,
+                                  float* __restrict__ hi, float* __restrict__ lo, uint64_t dld,
+                                  uint64_t rows, uint64_t cols) {
+  const uint64_t total = rows * cols;
+  for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    const uint64_t r = i / cols, c = i % cols;
+    const float x = load_elem_f32(src, sp, r * sld + c);
+    uint32_t h;
+    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(h) : "f"(x));
+    const float hf = __uint_as_float(h);
+    hi[r * dld + c] = hf;
+    lo[r * dld + c] = x - hf;
+  }
+}
+
+// Transposing variants: src is R x C (pitch sld); dst is C x R (pitch dld).
+// 32x32 tiles staged through shared memory so both sides stay coalesced.
+__global__ void split_tf32_t_kernel(const void* __restrict__ src, int sp, uint64_t sld,
+                                    float* __restrict__ hi, float* __restrict__ lo, uint64_t dld,
+                                    uint64_t rows, uint64_t cols, int split) {
+  __shared__ float tile[32][33];
+  const uint64_t r0 = static_cast<uint64_t>(blockIdx.y) * 32, c0 = static_cast<uint64_t>(blockIdx.x) * 32;
+  for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+    const uint64_t r = r0 + i, c = c0 + threadIdx.x;
+    tile[i][threadIdx.x] = (r < rows && c < cols) ? load_elem_f32(src, sp, r * sld + c) : 0.0f;
+  }
+  __syncthreads();
+  for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+    const uint64_t oc = c0 + i, orow = r0 + threadIdx.x;  // output row = source col
+    if (oc < cols && orow < rows) {
+      const float x = tile[threadIdx.x][i];
+      if (split) {
+        uint32_t h;
+        asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(h) : "f"(x));
+        const float hf = __uint_as_float(h);
+        hi[oc * dld + orow] = hf;
+        lo[oc * dld + orow] = x - hf;
+      } else {
+        hi[oc * dld + orow] = x;
+      }
+    }
+  }
+}
+
+__device__ __forceinline__ uint64_t avalanche64(uint64_t z) {
+  z ^= z >> 30;
+  z *= 0xBF58476D1CE4E5B9ull;
+  z ^= z >> 27;
+  z *= 0x94D049BB133111EBull;
+  z ^= z >> 31;
+  return z;
+}
+
+// Draw i (0-based) of SplitMix64(seed) is avalanche64(seed + (i+1)*salt)
+// (reference common.hpp:37-50); element (r, c) of a full_cols-wide matrix is
+// draw r*full_cols + c, mapped to lo + (hi-lo)*u with u in [0,1) on 53 bits,
+// then stored like setData (double -> storage, convertBuffer rules).
+__global__ void fill_uniform_kernel(void* __restrict__ dst, int prec, uint64_t ld, uint64_t r0,
+                                    uint64_t rows, uint64_t c0, uint64_t cols, uint64_t full_cols,
+                                    uint64_t seed, double lo, double hi) {
+  const uint64_t total = rows * cols;
+  for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    const uint64_t r = i / cols, c = i % cols;
+    const uint64_t draw = (r0 + r) * full_cols + (c0 + c);
+    const uint64_t x = avalanche64(seed + (draw + 1) * 0x9E3779B97F4A7C15ull);
+    const double u = static_cast<double>(x >> 11) * 0x1.0p-53;
+    store_elem(dst, prec, r * ld + c, lo + (hi - lo) * u);
+  }
+}
+
+// C = beta * C (alpha == 0 path; beta == 0 writes zeros without reading C).
+__global__ void scale_rect_kernel(void* __restrict__ c, int prec, uint64_t ld, uint64_t rows,
+                                  uint64_t cols, double beta) {
+  const uint64_t total = rows * cols;
+  for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    const uint64_t r = i / cols, cc = i % cols;
+    const uint64_t idx = r * ld + cc;
+    if (beta == 0.0) {
+      store_elem(c, prec, idx, 0.0);
+    } else if (prec == 2) {
+      store_elem(c, prec, idx, beta * load_elem(c, prec, idx));
+    } else {
+      // Single compute: beta and C in float, like runGemm<float>.
+      store_elem_f32(c, prec, idx, static_cast<float>(beta) * load_elem_f32(c, prec, idx));
+    }
+  }
+}
+
+namespace {
+unsigned grid_for(uint64_t total) {
+  uint64_t g = (total + 255) / 256;
+  if (g > 148ull * 16) g = 148ull * 16;
+  if (g == 0) g = 1;
+  return static_cast<unsigned>(g);
+}
+}  // namespace
+
+cudaError_t convert_rect(const void* src, int sp, uint64_t sld, void* dst, int dp, uint64_t dld,
+                         uint64_t rows, uint64_t cols, cudaStream_t s) {
+  if (rows == 0 || cols == 0) return cudaSuccess;
+  convert_rect_kernel<<<grid_for(rows * cols), 256, 0, s>>>(src, sp, sld, dst, dp, dld, rows, cols);
+  return cudaGetLastError();
+}
+
+cudaError_t split_tf32(const void* src, int sp, uint64_t sld, float* hi, float* lo, uint64_t dld,
+                       uint64_t rows, uint64_t cols, cudaStream_t s) {
+  if (rows == 0 || cols == 0) return cudaSuccess;
+  split_tf32_kernel<<<grid_for(rows * cols), 256, 0, s>>>(src, sp, sld, hi, lo, dld, rows, cols);
+  return cudaGetLastError();
+}
+
+cudaError_t split_tf32_t(const void* src, int sp, uint64_t sld, float* hi, float* lo,
+                         uint64_t dld, uint64_t rows, uint64_t cols, bool split, cudaStream_t s) {
+  if (rows == 0 || cols == 0) return cudaSuccess;
+  dim3 grid(static_cast<unsigned>((cols + 31) / 32), static_cast<unsigned>((rows + 31) / 32));
+  split_tf32_t_kernel<<<grid, dim3(32, 8), 0, s>>>(src, sp, sld, hi, lo, dld, rows, cols, split ? 1 : 0);
+  return cudaGetLastError();
+}
+
+cudaError_t fill_uniform(void* dst, int prec, uint64_t ld, uint64_t r0, uint64_t rows, uint64_t c0,
+                         uint64_t cols, uint64_t full_cols, uint64_t seed, double lo, double hi,
+                         cudaStream_t s) {
+  if (rows == 0 || cols == 0) return cudaSuccess;
+  fill_uniform_kernel<<<grid_for(rows * cols), 256, 0, s>>>(dst, prec, ld, r0, rows, c0, cols,
+                                                            full_cols, seed, lo, hi);
+  return cudaGetLastError();
+}
+
+cudaError_t scale_rect(void* c, int prec, uint64_t ld, uint64_t rows, uint64_t cols, double beta,
+                       cudaStream_t s) {
+  if (rows == 0 || cols == 0) return cudaSuccess;
+  scale_rect_kernel<<<grid_for(rows * cols), 256, 0, s>>>(c, prec, ld, rows, cols, beta);
+  return cudaGetLastError();
+}
+
+}  // namespace gmk

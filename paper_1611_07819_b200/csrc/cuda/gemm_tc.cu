@@ -1,0 +1,501 @@
+// SPDX-License-Identifier: Apache-2.0
+// Local block GEMM on the 5th-generation tensor cores (sm_100a).
+//
+//   C[m,n] = alpha * sum_k op(A)[m,k] * op(B)[k,n]  (+ beta * C[m,n])
+//
+// This is the device replacement of the reference's scalar panel loop
+// runGemm<T> (reference proj/src/kernels.cpp:445-558, hot loop :506-519).
+// Semantics kept: beta == 0 never reads C (kernels.cpp:463); accumulation
+// per output element is one ascending-k chain (kernels.cpp:527-528), here in
+// fp32 TMEM with a fixed K=16 MMA step, so results do not depend on how C is
+// tiled or distributed (deterministic mode).
+//
+// Structure (persistent, warp-specialised, one CTA or CTA pair per SM/TPC):
+//   warp 0      TMA producer: k-blocks of A and B into a kStages smem ring
+//   warp 1      MMA issuer (leader CTA only): tcgen05.mma kind::f16/tf32,
+//               fp32 accumulators double-buffered in TMEM (2 x 256 columns)
+//   warps 2..5  epilogue: tcgen05.ld TMEM -> registers -> alpha/beta ->
+//               convert -> global stores
+// A may be K-major (row-major A) or MN-major (transA); B may be MN-major
+// (row-major B) or K-major (transB) -- both majors are native to tcgen05 for
+// 16-bit and tf32 inputs, so no transpose pass is needed.
+// For Single-precision storage the 3xTF32 variant splits A and B into
+// hi/lo tf32 pairs (split kernel in convert.cu) and issues hi*lo + lo*hi +
+// hi*hi per k-step, which reproduces fp32 GEMM accuracy (~1e-7 rel).
+#include <cuda.h>
+#include <cudaTypedefs.h>
+#include <cuda_bf16.h>
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <cstring>
+#include <cstdio>
+#include <cstdlib>
+#include <mutex>
+
+#include "gemm_tc.h"
+#include "ptx.cuh"
+
+namespace gmk {
+
+constexpr uint32_t kBlockMcta = 128;  // accumulator rows per CTA (TMEM lanes)
+constexpr uint32_t kBlockN = 256;     // MMA N (TMEM columns per accumulator)
+constexpr uint32_t kSwizzleBytes = 128;
+constexpr uint32_t kNumThreads = 192;  // 6 warps
+
+// Operand element = 2 bytes (kind::f16) or 4 bytes (kind::tf32). A k-block
+// is one 128-byte swizzle row: 64 x 16-bit or 32 x 32-bit elements.
+template <int kCG, int kElemBytes, int kSplit>
+struct TcCfg {
+  static constexpr uint32_t kBlockK = kSwizzleBytes / kElemBytes;
+  static constexpr uint32_t kMmaK = 32 / kElemBytes;  // 16 (f16) or 8 (tf32)
+  static constexpr uint32_t kBlockNcta = kBlockN / kCG;
+  static constexpr uint32_t kBytesA = kBlockMcta * kSwizzleBytes;  // per operand part
+  static constexpr uint32_t kBytesB = kBlockNcta * kSwizzleBytes;
+  static constexpr uint32_t kParts = kSplit ? 2 : 1;               // hi (+ lo)
+  static constexpr uint32_t kStageBytes = kParts * (kBytesA + kBytesB);
+  static constexpr uint32_t kStages = (196u * 1024u) / kStageBytes;
+  static constexpr uint32_t kSmemBytes = kStages * kStageBytes + 1024 + 256;
+};
+
+struct TcParams {
+  uint32_t m, n, k;
+  uint32_t a_mn_major, b_mn_major;
+  uint32_t idesc;
+  float alpha, beta;
+  void* c;
+  uint64_t ldc;
+  uint32_t c_dtype;  // 0 f16, 1 bf16, 2 f32
+  uint32_t c_vec;    // 16B vector stores legal
+  uint32_t num_m_blocks, num_n_blocks;  // in units of (kBlockMcta*kCG) x kBlockN
+};
+
+__device__ __forceinline__ void tile_coords(uint32_t t, const TcParams& p, uint32_t& mb,
+                                            uint32_t& nb) {
+  // Group 16 M-blocks together so consecutive tiles share B panels in L2.
+  constexpr uint32_t kGroup = 16;
+  const uint32_t per_group = kGroup * p.num_n_blocks;
+  const uint32_t g = t / per_group;
+  const uint32_t first_m = g * kGroup;
+  const uint32_t gsize = min(kGroup, p.num_m_blocks - first_m);
+  const uint32_t r = t % per_group;
+  mb = first_m + r % gsize;
+  nb = r / gsize;
+}
+
+__device__ __forceinline__ float load_c(const TcParams& p, uint64_t off) {
+  if (p.c_dtype == 2) return reinterpret_cast<const float*>(p.c)[off];
+  if (p.c_dtype == 1) return __bfloat162float(reinterpret_cast<const __nv_bfloat16*>(p.c)[off]);
+  return __half2float(reinterpret_cast<const __half*>(p.c)[off]);
+}
+
+__device__ __forceinline__ void store_row32(const TcParams& p, uint32_t row, uint32_t col0,
+                                            const uint32_t (&v)[32]) {
+  if (row >= p.m || col0 >= p.n) return;
+  const uint64_t base = static_cast<uint64_t>(row) * p.ldc + col0;
+  float f[32];
+#pragma unroll
+  for (int i = 0; i < 32; ++i) f[i] = p.alpha * __uint_as_float(v[i]);
+  const bool full = col0 + 32 <= p.n;
+  if (p.beta != 0.0f) {
+    if (full) {
+#pragma unroll
+      for (int i = 0; i < 32; ++i) f[i] += p.beta * load_c(p, base + i);
+    } else {
+      for (uint32_t i = 0; i < 32 && col0 + i < p.n; ++i) f[i] += p.beta * load_c(p, base + i);
+    }
+  }
+  if (full && p.c_vec) {
+    if (p.c_dtype == 2) {
+      float4* dst = reinterpret_cast<float4*>(reinterpret_cast<float*>(p.c) + base);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) dst[i] = make_float4(f[4 * i], f[4 * i + 1], f[4 * i + 2], f[4 * i + 3]);
+    } else {
+      uint32_t packed[16];
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        if (p.c_dtype == 1) {
+          __nv_bfloat162 h = __floats2bfloat162_rn(f[2 * i], f[2 * i + 1]);
+          packed[i] = *reinterpret_cast<uint32_t*>(&h);
+        } else {
+          __half2 h = __floats2half2_rn(f[2 * i], f[2 * i + 1]);
+          packed[i] = *reinterpret_cast<uint32_t*>(&h);
+        }
+      }
+      uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<uint16_t*>(p.c) + base);
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+        dst[i] = make_uint4(packed[4 * i], packed[4 * i + 1], packed[4 * i + 2], packed[4 * i + 3]);
+    }
+    return;
+  }
+  for (uint32_t i = 0; i < 32 && col0 + i < p.n; ++i) {
+    if (p.c_dtype == 2)
+      reinterpret_cast<float*>(p.c)[base + i] = f[i];
+    else if (p.c_dtype == 1)
+      reinterpret_cast<__nv_bfloat16*>(p.c)[base + i] = __float2bfloat16_rn(f[i]);
+    else
+      reinterpret_cast<__half*>(p.c)[base + i] = __float2half_rn(f[i]);
+  }
+}
+
+// kSplit: 3xTF32 (maps a_hi/a_lo, b_hi/b_lo). Otherwise a single pair.
+template <int kCG, int kElemBytes, int kSplit>
+__global__ void __launch_bounds__(kNumThreads, 1)
+    tc_gemm_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid_constant__ CUtensorMap tm_b,
+                   const __grid_constant__ CUtensorMap tm_a_lo,
+                   const __grid_constant__ CUtensorMap tm_b_lo, const TcParams p) {
+  using Cfg = TcCfg<kCG, kElemBytes, kSplit>;
+  constexpr uint32_t kStages = Cfg::kStages;
+  constexpr uint32_t kBlockK = Cfg::kBlockK;
+  constexpr uint32_t kMmaK = Cfg::kMmaK;
+  constexpr uint32_t kBlockNcta = Cfg::kBlockNcta;
+
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + kStages * Cfg::kStageBytes);
+  uint64_t* empty_bar = full_bar + kStages;
+  uint64_t* tfull_bar = empty_bar + kStages;  // [2]
+  uint64_t* tempty_bar = tfull_bar + 2;       // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty_bar + 2);
+
+  const uint32_t warp = warp_id_sync();
+  const uint32_t lane = threadIdx.x & 31;
+  const uint32_t rank = (kCG == 2) ? cluster_ctarank() : 0;
+  const bool leader = rank == 0;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tm_a);
+    tma_prefetch_desc(&tm_b);
+    if (kSplit) {
+      tma_prefetch_desc(&tm_a_lo);
+      tma_prefetch_desc(&tm_b_lo);
+    }
+    for (uint32_t s = 0; s < kStages; ++s) {
+      mbar_init(&full_bar[s], 1);
+      mbar_init(&empty_bar[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tfull_bar[a], 1);
+      mbar_init(&tempty_bar[a], 4 * kCG);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc<kCG>(tmem_slot, 512);
+  if constexpr (kCG == 2) {
+    cluster_sync();
+  } else {
+    __syncthreads();
+  }
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  const uint32_t num_tiles = p.num_m_blocks * p.num_n_blocks;
+  const uint32_t num_kb = (p.k + kBlockK - 1) / kBlockK;
+  const uint32_t unit = blockIdx.x / kCG, num_units = gridDim.x / kCG;
+
+  if (warp == 0) {
+    // ------------------------------------------------------------ producer
+    if (lane == 0) {
+      uint32_t stage = 0, phase = 0;
+      for (uint32_t t = unit; t < num_tiles; t += num_units) {
+        uint32_t mb, nb;
+        tile_coords(t, p, mb, nb);
+        const int32_t m0 = static_cast<int32_t>(mb * kBlockMcta * kCG + rank * kBlockMcta);
+        const int32_t n0 = static_cast<int32_t>(nb * kBlockN + rank * kBlockNcta);
+        for (uint32_t kb = 0; kb < num_kb; ++kb) {
+          mbar_wait(&empty_bar[stage], phase ^ 1);
+          uint8_t* sa = smem + stage * Cfg::kStageBytes;
+          uint8_t* sb = sa + Cfg::kParts * Cfg::kBytesA;
+          const int32_t k0 = static_cast<int32_t>(kb * kBlockK);
+          // The leader's barrier tracks both CTAs' bytes; the peer's TMA
+          // completions land on it directly (2-SM TMA), no peer arrive needed.
+          if (leader) mbar_arrive_expect_tx(&full_bar[stage], Cfg::kStageBytes * kCG);
+          for (uint32_t part = 0; part < Cfg::kParts; ++part) {
+            const CUtensorMap* ma = part ? &tm_a_lo : &tm_a;
+            const CUtensorMap* mbm = part ? &tm_b_lo : &tm_b;
+            uint8_t* da = sa + part * Cfg::kBytesA;
+            uint8_t* db = sb + part * Cfg::kBytesB;
+            if (!p.a_mn_major) {
+              if (kCG == 2) tma_load_2d_2sm(da, ma, &full_bar[stage], k0, m0);
+              else tma_load_2d(da, ma, &full_bar[stage], k0, m0);
+            } else {
+              // MN-major: boxes of (64 B-elements of M) x kBlockK rows of K.
+              constexpr uint32_t kChunk = kSwizzleBytes / kElemBytes;
+#pragma unroll
+              for (uint32_t j = 0; j < kBlockMcta / kChunk; ++j) {
+                if (kCG == 2)
+                  tma_load_2d_2sm(da + j * kBlockK * kSwizzleBytes, ma, &full_bar[stage], m0 + j * kChunk, k0);
+                else
+                  tma_load_2d(da + j * kBlockK * kSwizzleBytes, ma, &full_bar[stage], m0 + j * kChunk, k0);
+              }
+            }
+            if (p.b_mn_major) {
+              constexpr uint32_t kChunk = kSwizzleBytes / kElemBytes;
+#pragma unroll
+              for (uint32_t j = 0; j < kBlockNcta / kChunk; ++j) {
+                if (kCG == 2)
+                  tma_load_2d_2sm(db + j * kBlockK * kSwizzleBytes, mbm, &full_bar[stage], n0 + j * kChunk, k0);
+                else
+                  tma_load_2d(db + j * kBlockK * kSwizzleBytes, mbm, &full_bar[stage], n0 + j * kChunk, k0);
+              }
+            } else {
+              if (kCG == 2) tma_load_2d_2sm(db, mbm, &full_bar[stage], k0, n0);
+              else tma_load_2d(db, mbm, &full_bar[stage], k0, n0);
+            }
+          }
+          if (++stage == kStages) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------------------ MMA issuer
+    if (leader && lane == 0) {
+      uint32_t stage = 0, phase = 0, acc = 0, acc_phase = 0;
+      // K-major: advance 32 bytes per MMA-K step inside the 128B swizzle row;
+      // MN-major: advance (kMmaK rows x 128B).
+      const uint32_t a_lbo = p.a_mn_major ? kBlockK * kSwizzleBytes : 16;
+      const uint32_t b_lbo = p.b_mn_major ? kBlockK * kSwizzleBytes : 16;
+      const uint32_t a_step = p.a_mn_major ? kMmaK * kSwizzleBytes : 32;
+      const uint32_t b_step = p.b_mn_major ? kMmaK * kSwizzleBytes : 32;
+      for (uint32_t t = unit; t < num_tiles; t += num_units) {
+        mbar_wait(&tempty_bar[acc], acc_phase ^ 1);
+        tc_fence_after();
+        const uint32_t tmem_d = tmem_base + acc * kBlockN;
+        for (uint32_t kb = 0; kb < num_kb; ++kb) {
+          mbar_wait(&full_bar[stage], phase);
+          tc_fence_after();
+          const uint32_t sa = smem_u32(smem + stage * Cfg::kStageBytes);
+          const uint32_t sb = sa + Cfg::kParts * Cfg::kBytesA;
+#pragma unroll
+          for (uint32_t kk = 0; kk < kBlockK / kMmaK; ++kk) {
+            const uint32_t first = (kb | kk) == 0 ? 0u : 1u;
+            const uint64_t ah = sdesc_sw128(sa + kk * a_step, a_lbo, 1024);
+            const uint64_t bh = sdesc_sw128(sb + kk * b_step, b_lbo, 1024);
+            if constexpr (kSplit) {
+              const uint64_t al = sdesc_sw128(sa + Cfg::kBytesA + kk * a_step, a_lbo, 1024);
+              const uint64_t bl = sdesc_sw128(sb + Cfg::kBytesB + kk * b_step, b_lbo, 1024);
+              mma_tf32<kCG>(tmem_d, al, bh, p.idesc, first);
+              mma_tf32<kCG>(tmem_d, ah, bl, p.idesc, 1u);
+              mma_tf32<kCG>(tmem_d, ah, bh, p.idesc, 1u);
+            } else if constexpr (kElemBytes == 4) {
+              mma_tf32<kCG>(tmem_d, ah, bh, p.idesc, first);
+            } else {
+              mma_f16<kCG>(tmem_d, ah, bh, p.idesc, first);
+            }
+          }
+          if constexpr (kCG == 2) mma_commit_2sm(&empty_bar[stage], 0x3);
+          else mma_commit(&empty_bar[stage]);
+          if (kb + 1 == num_kb) {
+            if constexpr (kCG == 2) mma_commit_2sm(&tfull_bar[acc], 0x3);
+            else mma_commit(&tfull_bar[acc]);
+          }
+          if (++stage == kStages) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        acc ^= 1;
+        if (acc == 0) acc_phase ^= 1;
+      }
+    }
+  } else {
+    // ------------------------------------------------------------ epilogue
+    const uint32_t lane_grp = warp & 3;  // TMEM lanes [32*lane_grp, +32)
+    uint32_t acc = 0, acc_phase = 0;
+    for (uint32_t t = unit; t < num_tiles; t += num_units) {
+      uint32_t mb, nb;
+      tile_coords(t, p, mb, nb);
+      mbar_wait(&tfull_bar[acc], acc_phase);
+      tc_fence_after();
+      const uint32_t row = mb * kBlockMcta * kCG + rank * kBlockMcta + lane_grp * 32 + lane;
+      const uint32_t taddr = tmem_base + ((lane_grp * 32) << 16) + acc * kBlockN;
+#pragma unroll 1
+      for (uint32_t c = 0; c < kBlockN; c += 32) {
+        uint32_t v[32];
+        __syncwarp();
+        tmem_ld_32x32b_x32(taddr + c, v);
+        tmem_wait_ld();
+        store_row32(p, row, nb * kBlockN + c, v);
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) {
+        if (kCG == 2 && !leader) mbar_arrive_cluster(&tempty_bar[acc], 0);
+        else mbar_arrive(&tempty_bar[acc]);
+      }
+      acc ^= 1;
+      if (acc == 0) acc_phase ^= 1;
+    }
+  }
+
+  __syncwarp();
+  tc_fence_before();
+  if constexpr (kCG == 2) {
+    cluster_sync();
+  } else {
+    __syncthreads();
+  }
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc<kCG>(tmem_base, 512);
+  }
+}
+
+// ------------------------------------------------------------------ host side
+
+namespace {
+
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    cudaDriverEntryPointQueryResult q;
+    void* p = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  });
+  return fn;
+}
+
+int make_map_2d(CUtensorMap* map, const void* ptr, CUtensorMapDataType dt, uint32_t esize,
+                uint64_t inner, uint64_t outer, uint64_t pitch_elems, uint32_t box_inner,
+                uint32_t box_outer, const char** err) {
+  auto fn = encode_fn();
+  if (!fn) {
+    *err = "cuTensorMapEncodeTiled unavailable";
+    return 1;
+  }
+  cuuint64_t dims[2] = {inner, outer};
+  cuuint64_t strides[1] = {pitch_elems * esize};
+  cuuint32_t box[2] = {box_inner, box_outer};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = fn(map, dt, 2, const_cast<void*>(ptr), dims, strides, box, estr,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    *err = "cuTensorMapEncodeTiled failed (alignment or stride)";
+    return 1;
+  }
+  return 0;
+}
+
+int sm_count(int dev) {
+  static int counts[64] = {0};
+  if (dev < 0 || dev >= 64) return 148;
+  if (!counts[dev]) cudaDeviceGetAttribute(&counts[dev], cudaDevAttrMultiProcessorCount, dev);
+  return counts[dev];
+}
+
+template <int kCG, int kElemBytes, int kSplit>
+int launch(const TcOperand& a, const TcOperand& b, const TcOperand* a_lo, const TcOperand* b_lo,
+           const TcParams& p0, int max_ctas, cudaStream_t stream, const char** err) {
+  using Cfg = TcCfg<kCG, kElemBytes, kSplit>;
+  const CUtensorMapDataType dt = kElemBytes == 4 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32
+                                                 : CU_TENSOR_MAP_DATA_TYPE_UINT16;
+  constexpr uint32_t kChunk = kSwizzleBytes / kElemBytes;
+  TcParams p = p0;
+  CUtensorMap ma, mb, mal, mbl;
+  auto map_a = [&](CUtensorMap* m, const TcOperand& op) {
+    // A logical M x K. K-major: stored M rows x K cols; MN-major: K rows x M cols.
+    if (!p.a_mn_major) return make_map_2d(m, op.ptr, dt, kElemBytes, p.k, p.m, op.ld, Cfg::kBlockK, kBlockMcta, err);
+    return make_map_2d(m, op.ptr, dt, kElemBytes, p.m, p.k, op.ld, kChunk, Cfg::kBlockK, err);
+  };
+  auto map_b = [&](CUtensorMap* m, const TcOperand& op) {
+    // B logical K x N. MN-major: stored K rows x N cols; K-major: N rows x K cols.
+    if (p.b_mn_major) return make_map_2d(m, op.ptr, dt, kElemBytes, p.n, p.k, op.ld, kChunk, Cfg::kBlockK, err);
+    return make_map_2d(m, op.ptr, dt, kElemBytes, p.k, p.n, op.ld, Cfg::kBlockK, Cfg::kBlockNcta, err);
+  };
+  if (map_a(&ma, a) || map_b(&mb, b)) return 1;
+  if (kSplit) {
+    if (map_a(&mal, *a_lo) || map_b(&mbl, *b_lo)) return 1;
+  } else {
+    mal = ma;
+    mbl = mb;
+  }
+  p.num_m_blocks = (p.m + kBlockMcta * kCG - 1) / (kBlockMcta * kCG);
+  p.num_n_blocks = (p.n + kBlockN - 1) / kBlockN;
+  const uint32_t tiles = p.num_m_blocks * p.num_n_blocks;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  auto kern = tc_gemm_kernel<kCG, kElemBytes, kSplit>;
+  // Persistent grid = the number of CTAs (CTA pairs) that are co-resident.
+  static int resident[64] = {0};
+  cudaLaunchConfig_t cfg{};
+  cfg.blockDim = dim3(kNumThreads, 1, 1);
+  cfg.dynamicSmemBytes = Cfg::kSmemBytes;
+  cfg.stream = stream;
+  cudaLaunchAttribute attrs[1];
+  attrs[0].id = cudaLaunchAttributeClusterDimension;
+  attrs[0].val.clusterDim.x = kCG;
+  attrs[0].val.clusterDim.y = 1;
+  attrs[0].val.clusterDim.z = 1;
+  cfg.attrs = attrs;
+  cfg.numAttrs = 1;
+  if (dev < 64 && !resident[dev]) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::kSmemBytes);
+    int clusters = 0;
+    cfg.gridDim = dim3(sm_count(dev), 1, 1);
+    if (cudaOccupancyMaxActiveClusters(&clusters, kern, &cfg) != cudaSuccess || clusters <= 0) {
+      cudaGetLastError();
+      clusters = sm_count(dev) / kCG;
+    }
+    resident[dev] = clusters * kCG;
+  }
+  int ctas = dev < 64 ? resident[dev] : sm_count(dev);
+  if (max_ctas > 0 && max_ctas < ctas) ctas = max_ctas;
+  ctas = (ctas / kCG) * kCG;
+  const int need = static_cast<int>(tiles) * kCG;
+  if (need < ctas) ctas = need;
+  cfg.gridDim = dim3(ctas, 1, 1);
+  static const bool debug = std::getenv("GM_DEBUG") != nullptr;
+  if (debug)
+    std::fprintf(stderr, "[gm] tc_gemm cg=%d elem=%d split=%d m=%u n=%u k=%u grid=%d resident=%d stages=%u smem=%u\n",
+                 kCG, kElemBytes, kSplit, p.m, p.n, p.k, ctas, dev < 64 ? resident[dev] : -1,
+                 Cfg::kStages, Cfg::kSmemBytes);
+  cudaError_t e = cudaLaunchKernelEx(&cfg, kern, ma, mb, mal, mbl, p);
+  if (e != cudaSuccess) {
+    *err = cudaGetErrorString(e);
+    return 1;
+  }
+  return 0;
+}
+
+}  // namespace
+
+int tc_gemm(const TcGemmArgs& g, cudaStream_t stream, const char** err) {
+  TcParams p{};
+  p.m = static_cast<uint32_t>(g.m);
+  p.n = static_cast<uint32_t>(g.n);
+  p.k = static_cast<uint32_t>(g.k);
+  p.a_mn_major = g.trans_a ? 1 : 0;
+  p.b_mn_major = g.trans_b ? 0 : 1;
+  p.alpha = static_cast<float>(g.alpha);
+  p.beta = static_cast<float>(g.beta);
+  p.c = g.c;
+  p.ldc = g.ldc;
+  p.c_dtype = g.c_dtype;
+  const uint32_t cb = g.c_dtype == 2 ? 4 : 2;
+  p.c_vec = ((reinterpret_cast<uintptr_t>(g.c) % 16) == 0 && (g.ldc * cb) % 16 == 0) ? 1 : 0;
+  const int cg = g.cta_group == 1 ? 1 : 2;
+  const uint32_t mrows = kBlockMcta * cg;
+  if (g.kind == TcKind::F16 || g.kind == TcKind::BF16) {
+    const uint32_t fmt = g.kind == TcKind::BF16 ? 1 : 0;
+    p.idesc = make_idesc(fmt, fmt, p.a_mn_major, p.b_mn_major, mrows, kBlockN);
+    return cg == 1 ? launch<1, 2, 0>(g.a, g.b, nullptr, nullptr, p, g.max_ctas, stream, err)
+                   : launch<2, 2, 0>(g.a, g.b, nullptr, nullptr, p, g.max_ctas, stream, err);
+  }
+  p.idesc = make_idesc(2, 2, p.a_mn_major, p.b_mn_major, mrows, kBlockN);
+  if (g.kind == TcKind::TF32)
+    return cg == 1 ? launch<1, 4, 0>(g.a, g.b, nullptr, nullptr, p, g.max_ctas, stream, err)
+                   : launch<2, 4, 0>(g.a, g.b, nullptr, nullptr, p, g.max_ctas, stream, err);
+  return cg == 1 ? launch<1, 4, 1>(g.a, g.b, &g.a_lo, &g.b_lo, p, g.max_ctas, stream, err)
+                 : launch<2, 4, 1>(g.a, g.b, &g.a_lo, &g.b_lo, p, g.max_ctas, stream, err);
+}
+
+}  // namespace gmk
