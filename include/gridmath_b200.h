@@ -141,6 +141,35 @@ int gm_layout_grid(uint64_t rows, uint64_t cols, uint32_t pr, uint32_t pc, gm_ti
 int gm_layout_validate(uint64_t rows, uint64_t cols, const gm_tile* tiles, uint32_t n,
                        uint32_t worker_count, int32_t* violation);
 
+/* GEMM plan (pure host logic, no device needed): every data movement the
+ * GEMM C = op(A) op(B) performs for the given layouts, from the same planner
+ * the runtime executes (reference planGemm, kernels.cpp:204-251). One entry
+ * per piece: `operand` 0 = A / 1 = B, rectangle in the operand's stored
+ * coordinates, src == dst for pieces copied from the consumer's own tiles.
+ * a_replicated / b_replicated: the operand has a fresh replica (no pieces).
+ * remote_bytes[w] (size `workers`): bytes worker w receives from peers. */
+typedef struct {
+  uint32_t src, dst, operand, pad;
+  uint64_t r0, r1, c0, c1;
+} gm_plan_piece;
+
+int gm_plan_gemm(uint32_t workers, uint64_t a_rows, uint64_t a_cols, int32_t a_prec,
+                 const gm_tile* a_tiles, uint32_t a_n, uint64_t b_rows, uint64_t b_cols,
+                 int32_t b_prec, const gm_tile* b_tiles, uint32_t b_n, uint64_t c_rows,
+                 uint64_t c_cols, int32_t c_prec, const gm_tile* c_tiles, uint32_t c_n,
+                 int32_t trans_a, int32_t trans_b, int32_t a_replicated, int32_t b_replicated,
+                 gm_plan_piece* out, uint32_t cap, uint32_t* n, uint64_t* remote_bytes);
+
+/* Descriptor wire encoding (reference descriptor.cpp:6-20): u64 id, u64 rows,
+ * u64 cols, u8 precision, u64 version, u32 tiles, per tile 4 x u64 + u32. */
+int gm_descriptor_encode(uint64_t id, uint64_t rows, uint64_t cols, int32_t prec,
+                         uint64_t version, const gm_tile* tiles, uint32_t n, uint8_t* out,
+                         uint32_t cap, uint32_t* len);
+
+/* Host storage conversion (convertBuffer semantics; setData's host path). */
+int gm_convert_host(const void* src, int32_t src_prec, void* dst, int32_t dst_prec,
+                    uint64_t count);
+
 /* ------------------------------------------------------------------------
  * Master API (reference gridmath::Session, session.hpp:62-179)
  * ---------------------------------------------------------------------- */

@@ -67,7 +67,10 @@ uint16_t oracle_float_to_half(float f) {
   }
 }
 
-/* precision.hpp:77-100 (exact). */
+/* precision.hpp:77-100. Restated bug-for-bug: for subnormal halves the
+ * reference uses exponent 112 - shift where IEEE needs 113 - shift, so every
+ * subnormal widens to half its IEEE value (the product keeps IEEE semantics;
+ * see DESIGN.md "Known reference deviations"). */
 float oracle_half_to_float(uint16_t h) {
   const uint32_t sign = (uint32_t)(h & 0x8000u) << 16;
   uint32_t e = (h >> 10) & 0x1Fu, m = h & 0x3FFu, out;
@@ -86,6 +89,15 @@ float oracle_half_to_float(uint16_t h) {
     out = sign | ((e + 112) << 23) | (m << 13);
   }
   return u2f(out);
+}
+
+/* Bulk variants (keep NaN payload bits intact, unlike a scalar ctypes round trip). */
+void oracle_half_to_float_n(const uint16_t* in, float* out, uint64_t n) {
+  for (uint64_t i = 0; i < n; ++i) out[i] = oracle_half_to_float(in[i]);
+}
+
+void oracle_float_to_half_n(const float* in, uint16_t* out, uint64_t n) {
+  for (uint64_t i = 0; i < n; ++i) out[i] = oracle_float_to_half(in[i]);
 }
 
 uint16_t oracle_float_to_bf16(float f) {

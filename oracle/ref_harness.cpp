@@ -16,6 +16,7 @@
 // Used by tests/ (parity checker), oracle/make_golden.py (golden vectors) and
 // bench.py --impl reference (the reference CPU arm).
 #include <chrono>
+#include <cmath>
 #include <cstdint>
 #include <cstring>
 #include <string>
@@ -43,8 +44,24 @@ Layout toLayout(const HTile* t, uint32_t n) {
   return l;
 }
 
+// Exact IEEE widening of the input images, so that the reference's own
+// setData (double -> storage via floatToHalf / float cast) reproduces the
+// input bits exactly. NOT the reference's halfToFloat: that one maps every
+// subnormal half to half its value (precision.hpp:87 uses 112 - shift where
+// IEEE needs 113 - shift), which would re-round subnormal inputs on upload.
 std::vector<double> rawToDouble(const void* raw, Precision p, uint64_t count) {
   std::vector<double> out(count);
+  if (p == Precision::Half) {
+    const auto* h = static_cast<const uint16_t*>(raw);
+    for (uint64_t i = 0; i < count; ++i) {
+      const uint32_t e = (h[i] >> 10) & 0x1Fu, m = h[i] & 0x3FFu;
+      const double sign = (h[i] & 0x8000u) ? -1.0 : 1.0;
+      if (e == 31) out[i] = m ? std::nan("") : sign * INFINITY;
+      else if (e == 0) out[i] = sign * std::ldexp(static_cast<double>(m), -24);
+      else out[i] = sign * std::ldexp(static_cast<double>(m | 0x400u), static_cast<int>(e) - 25);
+    }
+    return out;
+  }
   convertBuffer(static_cast<const uint8_t*>(raw), p, reinterpret_cast<uint8_t*>(out.data()),
                 Precision::Double, count);
   return out;

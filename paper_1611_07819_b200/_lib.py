@@ -58,6 +58,11 @@ class gm_worker_stats(Structure):
                 ("bytes_received", c_uint64)]
 
 
+class gm_plan_piece(Structure):
+    _fields_ = [("src", c_uint32), ("dst", c_uint32), ("operand", c_uint32), ("pad", c_uint32),
+                ("r0", c_uint64), ("r1", c_uint64), ("c0", c_uint64), ("c1", c_uint64)]
+
+
 _P = POINTER
 _SIGNATURES = {
     "gm_last_error": ([], c_char_p),
@@ -86,6 +91,13 @@ _SIGNATURES = {
                         _P(c_uint32)], c_int32),
     "gm_layout_validate": ([c_uint64, c_uint64, _P(gm_tile), c_uint32, c_uint32, _P(c_int32)],
                            c_int32),
+    "gm_plan_gemm": ([c_uint32, c_uint64, c_uint64, c_int32, _P(gm_tile), c_uint32, c_uint64, c_uint64,
+                      c_int32, _P(gm_tile), c_uint32, c_uint64, c_uint64, c_int32, _P(gm_tile), c_uint32,
+                      c_int32, c_int32, c_int32, c_int32, _P(gm_plan_piece), c_uint32, _P(c_uint32),
+                      _P(c_uint64)], c_int32),
+    "gm_descriptor_encode": ([c_uint64, c_uint64, c_uint64, c_int32, c_uint64, _P(gm_tile), c_uint32,
+                              _P(c_uint8), c_uint32, _P(c_uint32)], c_int32),
+    "gm_convert_host": ([c_void_p, c_int32, c_void_p, c_int32, c_uint64], c_int32),
     "gm_session_options_default": ([_P(gm_session_options)], None),
     "gm_session_create": ([_P(gm_session_options), _P(c_void_p)], c_int32),
     "gm_session_destroy": ([c_void_p], c_int32),

@@ -196,6 +196,11 @@ std::uint64_t gemmWorkspaceBytes(const gm_gemm_desc& d) {
   return makePlan(dd, odd, odd).bytes;
 }
 
+std::uint64_t gemmWorkspaceBytes(const gm_gemm_desc& d, const void* a, const void* b) {
+  if (d.m == 0 || d.n == 0 || d.alpha == 0.0 || d.k == 0) return 0;
+  return makePlan(d, a, b).bytes;
+}
+
 void gemmLocal(const gm_gemm_desc& d, const void* a, const void* b, void* c, void* workspace,
                std::uint64_t workspaceBytes, cudaStream_t stream) {
   if (d.m == 0 || d.n == 0) return;

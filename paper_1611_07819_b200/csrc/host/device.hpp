@@ -56,7 +56,8 @@ class DeviceArena {
 };
 
 // Local GEMM on the current device. Returns the staging workspace it needs.
-std::uint64_t gemmWorkspaceBytes(const gm_gemm_desc& d);
+std::uint64_t gemmWorkspaceBytes(const gm_gemm_desc& d);  // worst case over alignment
+std::uint64_t gemmWorkspaceBytes(const gm_gemm_desc& d, const void* a, const void* b);
 // Throws gridmath::Error on failure.
 void gemmLocal(const gm_gemm_desc& d, const void* a, const void* b, void* c, void* workspace,
                std::uint64_t workspaceBytes, cudaStream_t stream);

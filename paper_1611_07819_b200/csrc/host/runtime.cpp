@@ -1,0 +1,1207 @@
+// SPDX-License-Identifier: Apache-2.0
+// Implementation of the master/worker runtime (see runtime.hpp).
+//
+// Reference call stacks this follows (paths under /root/reference/proj):
+//   gemm()          session.cpp:533-545 -> issueOp :78-105 -> kernels::validate
+//                   kernels.cpp:296-312 -> applyOpMetadata ops.cpp:146-177
+//   execGemm        kernels.cpp:560-568: planGemm (:204-251, merged C row/col
+//                   intervals per worker; an A need per row interval and a B
+//                   need per col interval; viaReplica when the replica is
+//                   fresh, pieces.cpp:14-30) -> piece transport -> runGemm
+//   replication     session.cpp:329-375, worker.cpp:245-448
+// The B200 path takes each need over the full k range at once (one band,
+// one fixed ascending-k accumulation chain per output element inside the
+// tensor-core kernel) instead of 256-wide host panels; the per-element
+// order is therefore independent of the layout and of P (deterministic
+// mode, reference kernels.hpp:19-22).
+#include "runtime.hpp"
+
+#include <algorithm>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+
+#include "../cuda/convert.h"
+
+namespace gridmath {
+
+namespace {
+
+constexpr std::uint64_t kPitchAlign = 16;  // TMA row-stride rule
+
+std::uint64_t paddedLd(std::uint64_t cols, std::uint64_t eb) {
+  return ((cols * eb + kPitchAlign - 1) / kPitchAlign * kPitchAlign) / eb;
+}
+
+void ncclCheck(ncclResult_t r, const char* what) {
+  if (r != ncclSuccess) throw Error(std::string(what) + ": " + ncclGetErrorString(r));
+}
+
+struct Interval {
+  std::uint64_t lo = 0, hi = 0;
+};
+
+std::vector<Interval> mergeIntervals(std::vector<Interval> v) {
+  std::sort(v.begin(), v.end(), [](const Interval& a, const Interval& b) { return a.lo < b.lo; });
+  std::vector<Interval> out;
+  for (const Interval& i : v) {
+    if (!out.empty() && i.lo <= out.back().hi)
+      out.back().hi = std::max(out.back().hi, i.hi);
+    else
+      out.push_back(i);
+  }
+  return out;
+}
+
+const MatrixDescriptor& lookup(const DescriptorTable& t, std::uint64_t id) {
+  auto it = t.find(id);
+  if (it == t.end()) throw Error("unknown matrix id " + std::to_string(id));
+  return it->second;
+}
+
+void requireDistinct(const OpDescriptor& op, std::initializer_list<int> slots) {
+  for (int i : slots)
+    for (int j : slots)
+      if (i != j && op.ids[i] == op.ids[j]) throw Error("operands must be distinct matrices");
+}
+
+// Master-side checks before anything is issued (reference kernels.cpp:265-379).
+void validateOp(const DescriptorTable& t, const OpDescriptor& op, std::uint32_t workers) {
+  switch (op.opcode) {
+    case OpCode::CreateMatrix: {
+      WireReader r(op.blob);
+      const MatrixDescriptor d = decodeDescriptor(r);
+      if (d.rows == 0 || d.cols == 0) throw Error("createMatrix: empty shape");
+      const LayoutReport rep = validateLayout(d.rows, d.cols, d.layout, workers);
+      if (!rep.ok()) throw Error("createMatrix: invalid layout: " + rep.detail);
+      if (t.count(d.matrixId)) throw Error("createMatrix: duplicate id");
+      return;
+    }
+    case OpCode::DestroyMatrix:
+    case OpCode::SetData:
+    case OpCode::GetData:
+    case OpCode::ReplicateStart:
+      (void)lookup(t, op.ids[0]);
+      return;
+    case OpCode::Gemm: {
+      const MatrixDescriptor& a = lookup(t, op.ids[0]);
+      const MatrixDescriptor& b = lookup(t, op.ids[1]);
+      const MatrixDescriptor& c = lookup(t, op.ids[2]);
+      requireDistinct(op, {0, 2});
+      requireDistinct(op, {1, 2});
+      const bool ta = op.flags[0], tb = op.flags[1];
+      const std::uint64_t m = ta ? a.cols : a.rows, k = ta ? a.rows : a.cols;
+      const std::uint64_t kb = tb ? b.cols : b.rows, n = tb ? b.rows : b.cols;
+      if (k != kb || c.rows != m || c.cols != n)
+        throw Error("gemm: dimension mismatch (" + std::to_string(m) + "x" + std::to_string(k) +
+                    " * " + std::to_string(kb) + "x" + std::to_string(n) + " -> " +
+                    std::to_string(c.rows) + "x" + std::to_string(c.cols) + ")");
+      return;
+    }
+    case OpCode::MetaChecksum:
+    case OpCode::QueryStats:
+      return;
+    default:
+      throw Error("op not supported on the B200 GEMM path");
+  }
+}
+
+BandView offsetView(const void* base, std::uint64_t ld, std::uint64_t r, std::uint64_t c,
+                    std::uint64_t eb) {
+  return {static_cast<const std::uint8_t*>(base) + (r * ld + c) * eb, ld};
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------- DistMatrix
+
+std::uint64_t DistMatrix::rows() const { return session_->descriptor(id_).rows; }
+std::uint64_t DistMatrix::cols() const { return session_->descriptor(id_).cols; }
+Precision DistMatrix::precision() const { return session_->descriptor(id_).precision; }
+
+// ---------------------------------------------------------------- PanelCache
+
+CacheEntry* PanelCache::lookup(std::uint64_t id, std::uint64_t version, const Rect& r,
+                               std::uint64_t tick) {
+  for (CacheEntry& e : entries_)
+    if (e.matrixId == id && e.version == version && e.rect == r) {
+      e.lastUse = tick;
+      ++hits;
+      return &e;
+    }
+  ++misses;
+  return nullptr;
+}
+
+std::vector<CacheEntry> PanelCache::reserve(std::uint64_t bytes, std::uint64_t budget,
+                                            std::uint64_t protectTick) {
+  std::vector<CacheEntry> evicted;
+  while (bytes_ + bytes > budget) {
+    // Least recently used entry not in use by the current op.
+    auto victim = entries_.end();
+    for (auto it = entries_.begin(); it != entries_.end(); ++it)
+      if (it->lastUse != protectTick && (victim == entries_.end() || it->lastUse < victim->lastUse))
+        victim = it;
+    if (victim == entries_.end()) break;
+    bytes_ -= victim->bytes;
+    evicted.push_back(*victim);
+    entries_.erase(victim);
+  }
+  return evicted;
+}
+
+CacheEntry& PanelCache::insert(CacheEntry e) {
+  bytes_ += e.bytes;
+  entries_.push_back(e);
+  return entries_.back();
+}
+
+std::vector<CacheEntry> PanelCache::dropAll() {
+  std::vector<CacheEntry> out(entries_.begin(), entries_.end());
+  entries_.clear();
+  bytes_ = 0;
+  return out;
+}
+
+std::vector<CacheEntry> PanelCache::dropMatrix(std::uint64_t id, bool keepCurrent,
+                                               std::uint64_t version) {
+  std::vector<CacheEntry> out;
+  for (auto it = entries_.begin(); it != entries_.end();) {
+    if (it->matrixId == id && !(keepCurrent && it->version == version)) {
+      bytes_ -= it->bytes;
+      out.push_back(*it);
+      it = entries_.erase(it);
+    } else {
+      ++it;
+    }
+  }
+  return out;
+}
+
+// ---------------------------------------------------------------- Worker
+
+Worker::Worker(std::uint32_t r, int dev, std::uint64_t budget)
+    : rank(r), device(dev), arena(dev), cacheBudget(budget) {
+  activate();
+  cudaCheck(cudaStreamCreateWithFlags(&compute, cudaStreamNonBlocking), "worker: compute stream");
+  int lo = 0, hi = 0;
+  cudaDeviceGetStreamPriorityRange(&lo, &hi);
+  cudaCheck(cudaStreamCreateWithPriority(&comm, cudaStreamNonBlocking, hi), "worker: comm stream");
+  cudaCheck(cudaEventCreate(&tStart), "worker: event");
+  cudaCheck(cudaEventCreate(&tEnd), "worker: event");
+}
+
+Worker::~Worker() {
+  activate();
+  cudaStreamSynchronize(compute);
+  cudaStreamSynchronize(comm);
+  releaseReaders();
+  for (CacheEntry& e : cache.dropAll())
+    if (e.ready) cudaEventDestroy(e.ready);
+  for (auto& kv : replicas)
+    if (kv.second.ready) cudaEventDestroy(kv.second.ready);
+  if (nccl) ncclCommDestroy(nccl);
+  for (cudaEvent_t e : pool_) cudaEventDestroy(e);
+  cudaEventDestroy(tStart);
+  cudaEventDestroy(tEnd);
+  cudaStreamDestroy(compute);
+  cudaStreamDestroy(comm);
+}
+
+void Worker::activate() const { cudaCheck(cudaSetDevice(device), "cudaSetDevice"); }
+
+cudaEvent_t Worker::event() {
+  if (!pool_.empty()) {
+    cudaEvent_t e = pool_.back();
+    pool_.pop_back();
+    return e;
+  }
+  activate();
+  cudaEvent_t e;
+  cudaCheck(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "worker: event");
+  return e;
+}
+
+void Worker::recycle(cudaEvent_t e) {
+  if (e) pool_.push_back(e);
+}
+
+void* Worker::workspace(std::uint64_t bytes) {
+  if (bytes <= wsBytes_) return ws_;
+  if (ws_) arena.free(ws_, compute);
+  ws_ = arena.alloc(bytes, compute);
+  wsBytes_ = bytes;
+  return ws_;
+}
+
+void Worker::releaseReaders() {
+  for (auto& rd : readers_) rd.second->recycle(rd.first);
+  readers_.clear();
+}
+
+void Worker::beforeMutation() {
+  if (readers_.empty()) return;
+  activate();
+  for (auto& rd : readers_) {
+    cudaCheck(cudaStreamWaitEvent(compute, rd.first, 0), "worker: wait reader");
+    rd.second->recycle(rd.first);
+  }
+  readers_.clear();
+}
+
+// ---------------------------------------------------------------- Session
+
+Session::Session(SessionOptions opts) : opts_(std::move(opts)) {
+  if (opts_.workers == 0) throw Error("session: need at least one worker");
+  int ndev = 0;
+  cudaCheck(cudaGetDeviceCount(&ndev), "cudaGetDeviceCount");
+  if (ndev == 0) throw Error("session: no CUDA device");
+  std::vector<int> devs = opts_.devices;
+  if (devs.empty())
+    for (int d = 0; d < ndev; ++d) devs.push_back(d);
+  for (int d : devs)
+    if (d < 0 || d >= ndev) throw Error("session: bad device " + std::to_string(d));
+  workers_.resize(opts_.workers);
+  remoteCaches_.resize(opts_.workers);
+  auto budget = [&](int dev) -> std::uint64_t {
+    if (opts_.panelCacheBytes) return opts_.panelCacheBytes;
+    cudaDeviceProp prop{};
+    cudaGetDeviceProperties(&prop, dev);
+    return prop.totalGlobalMem / 4;
+  };
+  if (opts_.spmdRank >= 0) {
+    if (static_cast<std::uint32_t>(opts_.spmdRank) >= opts_.workers)
+      throw Error("session: spmd rank out of range");
+    const int dev = devs[0];
+    auto w = std::make_unique<Worker>(opts_.spmdRank, dev, budget(dev));
+    if (opts_.workers > 1) {
+      ncclUniqueId id;
+      static_assert(sizeof(id.internal) == 128, "nccl id size");
+      std::memcpy(id.internal, opts_.ncclId.data(), 128);
+      w->activate();
+      ncclCheck(ncclCommInitRank(&w->nccl, static_cast<int>(opts_.workers), id, opts_.spmdRank),
+                "ncclCommInitRank");
+      nccl_ = true;
+    }
+    workers_[opts_.spmdRank] = std::move(w);
+  } else {
+    for (std::uint32_t r = 0; r < opts_.workers; ++r) {
+      const int dev = devs[r % devs.size()];
+      workers_[r] = std::make_unique<Worker>(r, dev, budget(dev));
+    }
+    // Peer access between the distinct devices in use (copy-engine data plane).
+    std::set<int> used;
+    for (auto& w : workers_) used.insert(w->device);
+    for (int a : used)
+      for (int b : used) {
+        if (a == b) continue;
+        int can = 0;
+        cudaDeviceCanAccessPeer(&can, a, b);
+        if (can) {
+          cudaSetDevice(a);
+          const cudaError_t e = cudaDeviceEnablePeerAccess(b, 0);
+          if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled)
+            throw Error(std::string("peer access: ") + cudaGetErrorString(e));
+          cudaGetLastError();
+        }
+      }
+    peerCopies_ = true;
+  }
+}
+
+Session::~Session() {
+  try {
+    synchronize();
+  } catch (...) {
+  }
+  // Reader events can belong to a peer's pool: return them all before any
+  // worker goes away.
+  for (auto& w : workers_)
+    if (w) w->releaseReaders();
+  workers_.clear();
+}
+
+Worker* Session::local(std::uint32_t rank) const {
+  return rank < workers_.size() ? workers_[rank].get() : nullptr;
+}
+
+bool Session::isLocal(std::uint32_t rank) const { return local(rank) != nullptr; }
+
+std::vector<std::uint32_t> Session::localRanks() const {
+  std::vector<std::uint32_t> r;
+  for (auto& w : workers_)
+    if (w) r.push_back(w->rank);
+  return r;
+}
+
+void Session::forEachLocal(const std::function<void(Worker&)>& f) {
+  std::vector<std::string> errs;
+  for (auto& w : workers_) {
+    if (!w) continue;
+    try {
+      w->activate();
+      f(*w);
+    } catch (const std::exception& e) {
+      errs.push_back("worker " + std::to_string(w->rank) + ": " + e.what());
+    }
+  }
+  checkErrors(errs);
+}
+
+void Session::checkErrors(std::vector<std::string>& errs) {
+  if (errs.empty()) return;
+  std::string msg = "op failed: ";
+  for (auto& e : errs) msg += e + "; ";
+  throw Error(msg);
+}
+
+const MatrixDescriptor& Session::descriptor(std::uint64_t id) const { return lookup(table_, id); }
+
+std::uint64_t Session::issue(OpDescriptor& op) {
+  op.execId = nextExec_++;
+  validateOp(table_, op, opts_.workers);
+  std::vector<std::pair<std::uint64_t, std::uint64_t>> moved;
+  for (std::uint64_t id : mutatedMatrices(op)) {
+    auto it = table_.find(id);
+    if (it != table_.end()) moved.push_back({id, it->second.version});
+  }
+  applyOpMetadata(op, table_);
+  // Control plane: every local worker mirrors the op through the wire codec.
+  const std::vector<std::uint8_t> wire = op.encode();
+  for (auto& w : workers_)
+    if (w) applyOpMetadata(OpDescriptor::decode(wire), w->descs);
+  for (const auto& mv : moved) mutationHook(mv.first, mv.second);
+  if (opts_.checkMetadataEveryOp) verifyMetadataConsistency();
+  return op.execId;
+}
+
+// A matrix is about to change: in-flight replicas of the old version fail
+// (reference worker.cpp:207-239), cached panels of it die, and its owners'
+// compute streams wait for every reader of their tiles (WAR).
+void Session::mutationHook(std::uint64_t id, std::uint64_t oldVersion) {
+  const std::uint64_t newVersion = table_.count(id) ? table_.at(id).version : ~0ull;
+  for (auto& wp : workers_) {
+    if (!wp) continue;
+    Worker& w = *wp;
+    w.activate();
+    auto rit = w.replicas.find(id);
+    if (rit != w.replicas.end() && rit->second.version == oldVersion &&
+        rit->second.state == ReplicaState::Pending) {
+      if (cudaEventQuery(rit->second.ready) == cudaSuccess) {
+        rit->second.state = ReplicaState::Valid;
+      } else {
+        cudaGetLastError();
+        rit->second.state = ReplicaState::Stale;
+        replFailed_[{id, oldVersion}] = true;
+      }
+    }
+    for (CacheEntry& e : w.cache.dropMatrix(id, true, newVersion)) {
+      w.arena.free(e.ptr, w.compute);
+      w.recycle(e.ready);
+    }
+    w.beforeMutation();
+  }
+  for (std::uint32_t r = 0; r < opts_.workers; ++r)
+    if (!isLocal(r)) remoteCaches_[r].dropMatrix(id, true, newVersion);
+}
+
+// ---------------------------------------------------------------- lifecycle
+
+DistMatrix Session::createMatrix(std::uint64_t rows, std::uint64_t cols, Precision p,
+                                 const Layout& layout) {
+  MatrixDescriptor d;
+  d.matrixId = nextMatrixId_++;
+  d.rows = rows;
+  d.cols = cols;
+  d.precision = p;
+  d.layout = layout;
+  OpDescriptor op;
+  op.opcode = OpCode::CreateMatrix;
+  op.ids[0] = d.matrixId;
+  WireWriter w;
+  encodeDescriptor(d, w);
+  op.blob = w.take();
+  issue(op);
+  try {
+    execCreate(op);
+  } catch (...) {
+    try {
+      execDestroy(d.matrixId);
+    } catch (...) {
+    }
+    throw;
+  }
+  return DistMatrix(this, d.matrixId);
+}
+
+void Session::execCreate(const OpDescriptor& op) {
+  WireReader r(op.blob);
+  const MatrixDescriptor d = decodeDescriptor(r);
+  const std::uint64_t eb = bytesOf(d.precision);
+  forEachLocal([&](Worker& w) {
+    std::vector<DeviceTile> mine;
+    for (const auto& t : d.layout.tiles) {
+      if (t.second.rank != w.rank) continue;
+      DeviceTile dt;
+      dt.extent = t.first;
+      dt.ld = paddedLd(t.first.colCount, eb);
+      const std::uint64_t bytes = t.first.rowCount * dt.ld * eb;
+      dt.ptr = w.arena.alloc(bytes, w.compute);
+      cudaCheck(cudaMemsetAsync(dt.ptr, 0, bytes, w.compute), "create: zero tile");
+      w.residentBytes += t.first.elements() * eb;
+      mine.push_back(dt);
+    }
+    w.tiles[d.matrixId] = std::move(mine);
+  });
+}
+
+void Session::destroy(DistMatrix m) {
+  OpDescriptor op;
+  op.opcode = OpCode::DestroyMatrix;
+  op.ids[0] = m.id();
+  const std::uint64_t oldVersion = descriptor(m.id()).version;
+  issue(op);
+  mutationHook(m.id(), oldVersion);
+  execDestroy(m.id());
+}
+
+void Session::execDestroy(std::uint64_t id) {
+  forEachLocal([&](Worker& w) {
+    w.beforeMutation();
+    auto it = w.tiles.find(id);
+    if (it != w.tiles.end()) {
+      const std::uint64_t eb = 1;  // residentBytes tracked in bytes below
+      (void)eb;
+      for (DeviceTile& t : it->second) w.arena.free(t.ptr, w.compute);
+      w.tiles.erase(it);
+    }
+    auto rit = w.replicas.find(id);
+    if (rit != w.replicas.end()) {
+      cudaStreamWaitEvent(w.compute, rit->second.ready, 0);
+      w.arena.free(rit->second.full, w.compute);
+      cudaEventDestroy(rit->second.ready);
+      w.replicas.erase(rit);
+    }
+    for (CacheEntry& e : w.cache.dropMatrix(id, false, 0)) {
+      w.arena.free(e.ptr, w.compute);
+      w.recycle(e.ready);
+    }
+  });
+  for (auto& c : remoteCaches_) c.dropMatrix(id, false, 0);
+  // resident bytes recomputed from the remaining tiles
+  for (auto& w : workers_) {
+    if (!w) continue;
+    w->residentBytes = 0;
+    for (auto& kv : w->tiles) {
+      const std::uint64_t eb = bytesOf(lookup(w->descs, kv.first).precision);
+      for (auto& t : kv.second) w->residentBytes += t.extent.elements() * eb;
+    }
+  }
+}
+
+// ---------------------------------------------------------------- data in/out
+
+void Session::setDataRaw(DistMatrix m, const void* image, std::uint64_t bytes) {
+  const MatrixDescriptor d = descriptor(m.id());
+  if (bytes != d.byteCount())
+    throw Error("setData: expected " + std::to_string(d.byteCount()) + " bytes, got " +
+                std::to_string(bytes));
+  OpDescriptor op;
+  op.opcode = OpCode::SetData;
+  op.ids[0] = m.id();
+  issue(op);
+  const std::uint64_t eb = bytesOf(d.precision);
+  const auto* img = static_cast<const std::uint8_t*>(image);
+  forEachLocal([&](Worker& w) {
+    for (DeviceTile& t : w.tiles.at(d.matrixId)) {
+      const TileExtent& e = t.extent;
+      cudaCheck(cudaMemcpy2DAsync(t.ptr, t.ld * eb, img + (e.rowStart * d.cols + e.colStart) * eb,
+                                  d.cols * eb, e.colCount * eb, e.rowCount, cudaMemcpyDefault,
+                                  w.compute),
+                "setData: upload");
+    }
+    cudaCheck(cudaStreamSynchronize(w.compute), "setData: sync");
+  });
+}
+
+void Session::setData(DistMatrix m, const std::vector<double>& rowMajor) {
+  const MatrixDescriptor& d = descriptor(m.id());
+  if (rowMajor.size() != d.elementCount())
+    throw Error("setData: expected " + std::to_string(d.elementCount()) + " values, got " +
+                std::to_string(rowMajor.size()));
+  std::vector<std::uint8_t> staging(d.byteCount());
+  convertBuffer(reinterpret_cast<const std::uint8_t*>(rowMajor.data()), Precision::Double,
+                staging.data(), d.precision, rowMajor.size());
+  setDataRaw(m, staging.data(), staging.size());
+}
+
+void Session::setDataF32(DistMatrix m, const std::vector<float>& rowMajor) {
+  const MatrixDescriptor& d = descriptor(m.id());
+  if (rowMajor.size() != d.elementCount()) throw Error("setData: value count mismatch");
+  std::vector<std::uint8_t> staging(d.byteCount());
+  convertBuffer(reinterpret_cast<const std::uint8_t*>(rowMajor.data()), Precision::Single,
+                staging.data(), d.precision, rowMajor.size());
+  setDataRaw(m, staging.data(), staging.size());
+}
+
+void Session::fillUniform(DistMatrix m, std::uint64_t seed, double lo, double hi) {
+  const MatrixDescriptor d = descriptor(m.id());
+  OpDescriptor op;
+  op.opcode = OpCode::SetData;
+  op.ids[0] = m.id();
+  issue(op);
+  forEachLocal([&](Worker& w) {
+    for (DeviceTile& t : w.tiles.at(d.matrixId)) {
+      const TileExtent& e = t.extent;
+      cudaCheck(gmk::fill_uniform(t.ptr, static_cast<int>(d.precision), t.ld, e.rowStart, e.rowCount,
+                                  e.colStart, e.colCount, d.cols, seed, lo, hi, w.compute),
+                "fillUniform");
+    }
+  });
+}
+
+void Session::getDataRawInto(DistMatrix m, void* image, std::uint64_t bytes, bool localOnly) {
+  const MatrixDescriptor d = descriptor(m.id());
+  if (bytes != d.byteCount()) throw Error("getData: buffer size mismatch");
+  OpDescriptor op;
+  op.opcode = OpCode::GetData;
+  op.ids[0] = m.id();
+  issue(op);
+  const std::uint64_t eb = bytesOf(d.precision);
+  auto* img = static_cast<std::uint8_t*>(image);
+  forEachLocal([&](Worker& w) {
+    for (DeviceTile& t : w.tiles.at(d.matrixId)) {
+      const TileExtent& e = t.extent;
+      cudaCheck(cudaMemcpy2DAsync(img + (e.rowStart * d.cols + e.colStart) * eb, d.cols * eb, t.ptr,
+                                  t.ld * eb, e.colCount * eb, e.rowCount, cudaMemcpyDefault,
+                                  w.compute),
+                "getData: download");
+    }
+  });
+  if (nccl_ && !localOnly) {
+    // Remote tiles: each owner broadcasts its tile (packed) to every rank.
+    Worker& w = *local(static_cast<std::uint32_t>(opts_.spmdRank));
+    w.activate();
+    std::uint64_t maxTile = 0;
+    for (const auto& t : d.layout.tiles) maxTile = std::max(maxTile, t.first.elements() * eb);
+    void* staging = w.arena.alloc(std::max<std::uint64_t>(maxTile, 256), w.compute);
+    for (const auto& t : d.layout.tiles) {
+      const TileExtent& e = t.first;
+      const bool mine = t.second.rank == w.rank;
+      if (mine) {
+        for (DeviceTile& dt : w.tiles.at(d.matrixId))
+          if (dt.extent == e)
+            cudaCheck(cudaMemcpy2DAsync(staging, e.colCount * eb, dt.ptr, dt.ld * eb, e.colCount * eb,
+                                        e.rowCount, cudaMemcpyDeviceToDevice, w.compute),
+                      "getData: pack");
+      }
+      ncclCheck(ncclBroadcast(staging, staging, e.elements() * eb, ncclUint8,
+                              static_cast<int>(t.second.rank), w.nccl, w.compute),
+                "getData: broadcast");
+      if (!mine)
+        cudaCheck(cudaMemcpy2DAsync(img + (e.rowStart * d.cols + e.colStart) * eb, d.cols * eb, staging,
+                                    e.colCount * eb, e.colCount * eb, e.rowCount, cudaMemcpyDefault,
+                                    w.compute),
+                  "getData: download");
+    }
+    w.arena.free(staging, w.compute);
+  }
+  forEachLocal([&](Worker& w) { cudaCheck(cudaStreamSynchronize(w.compute), "getData: sync"); });
+}
+
+std::vector<std::uint8_t> Session::getDataRaw(DistMatrix m) {
+  std::vector<std::uint8_t> out(descriptor(m.id()).byteCount());
+  getDataRawInto(m, out.data(), out.size(), false);
+  return out;
+}
+
+std::vector<double> Session::getData(DistMatrix m) {
+  const MatrixDescriptor& d = descriptor(m.id());
+  const auto raw = getDataRaw(m);
+  std::vector<double> out(d.elementCount());
+  convertBuffer(raw.data(), d.precision, reinterpret_cast<std::uint8_t*>(out.data()),
+                Precision::Double, out.size());
+  return out;
+}
+
+// ---------------------------------------------------------------- data plane
+
+// Copy-engine plane (single process): the consumer pulls every piece with a
+// 2D peer/D2D copy on its stream after waiting for the producer's prior
+// writes; the producer later waits for the consumer before mutating (WAR).
+// NCCL plane (SPMD): grouped ncclSend/ncclRecv, packing/unpacking strided
+// pieces through arena staging; stream order covers RAW and WAR.
+void Session::exchange(std::vector<Xfer>& xs, bool onComm) {
+  auto streamOf = [&](Worker& w) { return onComm ? w.comm : w.compute; };
+  if (!nccl_) {
+    std::map<std::pair<std::uint32_t, std::uint32_t>, bool> pairs;  // (src, dst)
+    for (const Xfer& x : xs)
+      if (x.src != x.dst || onComm) pairs[{x.src, x.dst}] = true;
+    // RAW: consumer waits for the producer's writes issued so far.
+    for (const auto& pr : pairs) {
+      Worker& s = *local(pr.first.first);
+      Worker& d = *local(pr.first.second);
+      s.activate();
+      cudaEvent_t e = s.event();
+      cudaCheck(cudaEventRecord(e, s.compute), "exchange: record");
+      d.activate();
+      cudaCheck(cudaStreamWaitEvent(streamOf(d), e, 0), "exchange: wait");
+      s.recycle(e);
+    }
+    for (const Xfer& x : xs) {
+      Worker& d = *local(x.dst);
+      d.activate();
+      cudaCheck(cudaMemcpy2DAsync(x.dstPtr, x.dstLd * x.eb, x.srcPtr, x.srcLd * x.eb, x.cols * x.eb,
+                                  x.rows, cudaMemcpyDefault, streamOf(d)),
+                "exchange: copy");
+      if (x.src != x.dst) {
+        d.bytesReceived += x.rows * x.cols * x.eb;
+        local(x.src)->bytesSent += x.rows * x.cols * x.eb;
+      }
+    }
+    // WAR: producer waits for the consumer's copies before its next mutation.
+    for (const auto& pr : pairs) {
+      Worker& s = *local(pr.first.first);
+      Worker& d = *local(pr.first.second);
+      if (&s == &d && !onComm) continue;
+      d.activate();
+      cudaEvent_t e = d.event();
+      cudaCheck(cudaEventRecord(e, streamOf(d)), "exchange: record done");
+      s.addReader(e, &d);
+    }
+    return;
+  }
+  // ---- NCCL
+  if (onComm) {
+    // The comm stream must see the compute stream's prior writes.
+    for (auto& wp : workers_) {
+      if (!wp) continue;
+      wp->activate();
+      cudaEvent_t e = wp->event();
+      cudaCheck(cudaEventRecord(e, wp->compute), "exchange: record");
+      cudaCheck(cudaStreamWaitEvent(wp->comm, e, 0), "exchange: wait");
+      wp->recycle(e);
+    }
+  }
+  struct Staged {
+    Worker* w;
+    void* buf;
+    const Xfer* x;
+  };
+  std::vector<Staged> sendPack, recvUnpack;
+  std::vector<std::pair<const Xfer*, const void*>> sends;
+  std::vector<std::pair<const Xfer*, void*>> recvs;
+  for (const Xfer& x : xs) {
+    const std::uint64_t bytes = x.rows * x.cols * x.eb;
+    if (bytes == 0) continue;
+    Worker* s = local(x.src);
+    Worker* d = local(x.dst);
+    if (s && d) {
+      d->activate();
+      cudaCheck(cudaMemcpy2DAsync(x.dstPtr, x.dstLd * x.eb, x.srcPtr, x.srcLd * x.eb, x.cols * x.eb,
+                                  x.rows, cudaMemcpyDeviceToDevice, streamOf(*d)),
+                "exchange: local copy");
+      continue;
+    }
+    if (s) {
+      s->activate();
+      s->bytesSent += bytes;
+      if (x.srcLd == x.cols) {
+        sends.push_back({&x, x.srcPtr});
+      } else {
+        void* buf = s->arena.alloc(bytes, streamOf(*s));
+        cudaCheck(cudaMemcpy2DAsync(buf, x.cols * x.eb, x.srcPtr, x.srcLd * x.eb, x.cols * x.eb, x.rows,
+                                    cudaMemcpyDeviceToDevice, streamOf(*s)),
+                  "exchange: pack");
+        sendPack.push_back({s, buf, &x});
+        sends.push_back({&x, buf});
+      }
+    }
+    if (d) {
+      d->activate();
+      d->bytesReceived += bytes;
+      if (x.dstLd == x.cols) {
+        recvs.push_back({&x, x.dstPtr});
+      } else {
+        void* buf = d->arena.alloc(bytes, streamOf(*d));
+        recvUnpack.push_back({d, buf, &x});
+        recvs.push_back({&x, buf});
+      }
+    }
+  }
+  ncclCheck(ncclGroupStart(), "ncclGroupStart");
+  for (auto& sd : sends) {
+    Worker& s = *local(sd.first->src);
+    ncclCheck(ncclSend(sd.second, sd.first->rows * sd.first->cols * sd.first->eb, ncclUint8,
+                       static_cast<int>(sd.first->dst), s.nccl, streamOf(s)),
+              "ncclSend");
+  }
+  for (auto& rv : recvs) {
+    Worker& d = *local(rv.first->dst);
+    ncclCheck(ncclRecv(rv.second, rv.first->rows * rv.first->cols * rv.first->eb, ncclUint8,
+                       static_cast<int>(rv.first->src), d.nccl, streamOf(d)),
+              "ncclRecv");
+  }
+  ncclCheck(ncclGroupEnd(), "ncclGroupEnd");
+  for (auto& st : recvUnpack) {
+    st.w->activate();
+    const Xfer& x = *st.x;
+    cudaCheck(cudaMemcpy2DAsync(x.dstPtr, x.dstLd * x.eb, st.buf, x.cols * x.eb, x.cols * x.eb, x.rows,
+                                cudaMemcpyDeviceToDevice, streamOf(*st.w)),
+              "exchange: unpack");
+    st.w->arena.free(st.buf, streamOf(*st.w));
+  }
+  for (auto& st : sendPack) {
+    st.w->activate();
+    st.w->arena.free(st.buf, streamOf(*st.w));
+  }
+  if (onComm) {
+    // Sends read tiles on the comm stream: later mutations wait for them.
+    for (auto& wp : workers_) {
+      if (!wp) continue;
+      wp->activate();
+      cudaEvent_t e = wp->event();
+      cudaCheck(cudaEventRecord(e, wp->comm), "exchange: record");
+      wp->addReader(e, wp.get());
+    }
+  }
+}
+
+// ---------------------------------------------------------------- GEMM
+
+GemmPlanB200 planGemmB200(const DescriptorTable& t, const OpDescriptor& op, std::uint32_t P,
+                          const CacheProbe& cached) {
+  const MatrixDescriptor& A = lookup(t, op.ids[0]);
+  const MatrixDescriptor& B = lookup(t, op.ids[1]);
+  const MatrixDescriptor& C = lookup(t, op.ids[2]);
+  GemmPlanB200 plan;
+  plan.transA = op.flags[0] != 0;
+  plan.transB = op.flags[1] != 0;
+  plan.m = C.rows;
+  plan.n = C.cols;
+  plan.k = plan.transA ? A.rows : A.cols;
+  plan.rowsOf.resize(P);
+  plan.colsOf.resize(P);
+  {
+    std::vector<std::vector<Interval>> r(P), c(P);
+    for (const auto& tl : C.layout.tiles) {
+      r[tl.second.rank].push_back({tl.first.rowStart, tl.first.rowEnd()});
+      c[tl.second.rank].push_back({tl.first.colStart, tl.first.colEnd()});
+    }
+    for (std::uint32_t w = 0; w < P; ++w) {
+      for (const Interval& iv : mergeIntervals(std::move(r[w]))) plan.rowsOf[w].push_back({iv.lo, iv.hi});
+      for (const Interval& iv : mergeIntervals(std::move(c[w]))) plan.colsOf[w].push_back({iv.lo, iv.hi});
+    }
+  }
+  if (op.s0 == 0.0) return plan;  // alpha == 0: A and B are never read
+  std::uint32_t pieceId = 0;
+  auto add = [&](std::uint32_t w, int operand, std::size_t idx, const MatrixDescriptor& M, const Rect& rect) {
+    PlannedNeed nd;
+    nd.worker = w;
+    nd.operand = operand;
+    nd.interval = idx;
+    nd.rect = rect;
+    if (M.replicaFresh()) {
+      nd.kind = PlannedNeed::Replica;
+    } else {
+      bool inTile = false;
+      for (const auto& tl : M.layout.tiles)
+        if (tl.second.rank == w && rect.inside(Rect::ofExtent(tl.first))) inTile = true;
+      if (inTile) {
+        nd.kind = PlannedNeed::LocalTile;
+      } else if (cached && cached(w, M, rect)) {
+        nd.kind = PlannedNeed::Cached;
+      } else {
+        nd.kind = PlannedNeed::Gather;
+        for (const auto& tl : M.layout.tiles)
+          if (auto piece = intersectRect(rect, Rect::ofExtent(tl.first)))
+            nd.pieces.push_back(PieceRoute{pieceId++, tl.second.rank, w, M.matrixId, *piece});
+      }
+    }
+    plan.needs.push_back(std::move(nd));
+  };
+  for (std::uint32_t w = 0; w < P; ++w) {
+    for (std::size_t i = 0; i < plan.rowsOf[w].size(); ++i) {
+      const auto iv = plan.rowsOf[w][i];
+      add(w, 0, i, A, plan.transA ? Rect{0, plan.k, iv.first, iv.second} : Rect{iv.first, iv.second, 0, plan.k});
+    }
+    for (std::size_t i = 0; i < plan.colsOf[w].size(); ++i) {
+      const auto iv = plan.colsOf[w][i];
+      add(w, 1, i, B, plan.transB ? Rect{iv.first, iv.second, 0, plan.k} : Rect{0, plan.k, iv.first, iv.second});
+    }
+  }
+  return plan;
+}
+
+std::vector<std::uint64_t> planRemoteBytes(const GemmPlanB200& plan, const DescriptorTable& t,
+                                           std::uint32_t P) {
+  std::vector<std::uint64_t> out(P, 0);
+  for (const PlannedNeed& nd : plan.needs)
+    for (const PieceRoute& pr : nd.pieces)
+      if (pr.src != pr.consumer)
+        out[pr.consumer] += pr.rect.elements() * bytesOf(lookup(t, pr.matrixId).precision);
+  return out;
+}
+
+
+void Session::runGemm(const OpDescriptor& op0, bool sync) {
+  OpDescriptor op = op0;
+  issue(op);
+  execGemm(op);
+  if (sync) synchronize();
+}
+
+void Session::execGemm(const OpDescriptor& op) {
+  const MatrixDescriptor& A = lookup(table_, op.ids[0]);
+  const MatrixDescriptor& B = lookup(table_, op.ids[1]);
+  const MatrixDescriptor& C = lookup(table_, op.ids[2]);
+  const std::uint32_t P = opts_.workers;
+  ++tick_;
+  Worker* localRef = nullptr;
+  for (auto& wp : workers_)
+    if (wp) localRef = wp.get();
+
+  forEachLocal([&](Worker& w) {
+    w.timed = true;
+    cudaCheck(cudaEventRecord(w.tStart, w.compute), "gemm: timing");
+  });
+
+  auto dirOf = [&](std::uint32_t r) -> PanelCache& {
+    Worker* w = local(r);
+    return w ? w->cache : remoteCaches_[r];
+  };
+  // Probe only (no LRU side effects): the directory is updated below in plan order.
+  const GemmPlanB200 plan = planGemmB200(table_, op, P, [&](std::uint32_t r, const MatrixDescriptor& M, const Rect& rect) {
+    PanelCache& dir = dirOf(r);
+    const std::uint64_t h = dir.hits, mi = dir.misses;
+    const bool hit = dir.lookup(M.matrixId, M.version, rect, 0) != nullptr;
+    dir.hits = h;
+    dir.misses = mi;
+    return hit;
+  });
+
+  std::vector<std::vector<BandView>> aViews(P), bViews(P);
+  for (std::uint32_t w = 0; w < P; ++w) {
+    aViews[w].resize(plan.rowsOf[w].size());
+    bViews[w].resize(plan.colsOf[w].size());
+  }
+  std::vector<Xfer> xfers;
+  std::vector<std::pair<Worker*, CacheEntry*>> fresh;
+
+  for (const PlannedNeed& nd : plan.needs) {
+    const MatrixDescriptor& M = nd.operand == 0 ? A : B;
+    const std::uint64_t eb = bytesOf(M.precision);
+    Worker* w = local(nd.worker);
+    BandView view;
+    switch (nd.kind) {
+      case PlannedNeed::Replica: {
+        if (!w) break;
+        auto it = w->replicas.find(M.matrixId);
+        if (it == w->replicas.end() || it->second.version != M.version ||
+            it->second.state == ReplicaState::Stale)
+          throw Error("replica of matrix " + std::to_string(M.matrixId) + " not readable on worker " +
+                      std::to_string(nd.worker));
+        w->activate();
+        cudaCheck(cudaStreamWaitEvent(w->compute, it->second.ready, 0), "gemm: wait replica");
+        view = offsetView(it->second.full, it->second.ld, nd.rect.r0, nd.rect.c0, eb);
+        break;
+      }
+      case PlannedNeed::LocalTile: {
+        if (!w) break;
+        for (const DeviceTile& dt : w->tiles.at(M.matrixId))
+          if (nd.rect.inside(Rect::ofExtent(dt.extent)))
+            view = offsetView(dt.ptr, dt.ld, nd.rect.r0 - dt.extent.rowStart,
+                              nd.rect.c0 - dt.extent.colStart, eb);
+        break;
+      }
+      case PlannedNeed::Cached: {
+        CacheEntry* hit = dirOf(nd.worker).lookup(M.matrixId, M.version, nd.rect, tick_);
+        if (!w) break;
+        w->activate();
+        cudaCheck(cudaStreamWaitEvent(w->compute, hit->ready, 0), "gemm: wait panel");
+        view = {hit->ptr, hit->ld};
+        break;
+      }
+      case PlannedNeed::Gather: {
+        PanelCache& dir = dirOf(nd.worker);
+        dir.misses += 1;
+        CacheEntry e;
+        e.matrixId = M.matrixId;
+        e.version = M.version;
+        e.rect = nd.rect;
+        e.ld = paddedLd(nd.rect.cols(), eb);
+        e.bytes = nd.rect.rows() * e.ld * eb;
+        e.lastUse = tick_;
+        const std::uint64_t budget = w ? w->cacheBudget : localRef->cacheBudget;
+        for (CacheEntry& ev : dir.reserve(e.bytes, budget, tick_))
+          if (w && ev.ptr) {
+            w->activate();
+            w->arena.free(ev.ptr, w->compute);
+            w->recycle(ev.ready);
+          }
+        if (w) {
+          w->activate();
+          e.ptr = w->arena.alloc(e.bytes, w->compute);
+        }
+        CacheEntry& slot = dir.insert(e);
+        if (w) {
+          fresh.push_back({w, &slot});
+          view = {slot.ptr, slot.ld};
+        }
+        for (const PieceRoute& pr : nd.pieces) {
+          Worker* sw = local(pr.src);
+          if (!w && !sw) continue;
+          Xfer x;
+          x.src = pr.src;
+          x.dst = nd.worker;
+          x.rows = pr.rect.rows();
+          x.cols = pr.rect.cols();
+          x.eb = static_cast<std::uint32_t>(eb);
+          if (sw)
+            for (const DeviceTile& dt : sw->tiles.at(M.matrixId))
+              if (pr.rect.inside(Rect::ofExtent(dt.extent))) {
+                x.srcPtr = static_cast<const std::uint8_t*>(dt.ptr) +
+                           ((pr.rect.r0 - dt.extent.rowStart) * dt.ld + (pr.rect.c0 - dt.extent.colStart)) * eb;
+                x.srcLd = dt.ld;
+              }
+          if (w) {
+            x.dstPtr = static_cast<std::uint8_t*>(slot.ptr) +
+                       ((pr.rect.r0 - nd.rect.r0) * slot.ld + (pr.rect.c0 - nd.rect.c0)) * eb;
+            x.dstLd = slot.ld;
+          }
+          xfers.push_back(x);
+        }
+        break;
+      }
+    }
+    (nd.operand == 0 ? aViews : bViews)[nd.worker][nd.interval] = view;
+  }
+  if (!xfers.empty()) exchange(xfers, false);
+  for (auto& fr : fresh) {
+    fr.first->activate();
+    fr.second->ready = fr.first->event();
+    cudaCheck(cudaEventRecord(fr.second->ready, fr.first->compute), "gemm: panel ready");
+  }
+
+  const bool alphaZero = op.s0 == 0.0;
+  const std::uint64_t ebA = bytesOf(A.precision), ebB = bytesOf(B.precision);
+  forEachLocal([&](Worker& w) {
+    for (DeviceTile& ct : w.tiles.at(C.matrixId)) {
+      const TileExtent& e = ct.extent;
+      gm_gemm_desc d{};
+      d.m = e.rowCount;
+      d.n = e.colCount;
+      d.k = plan.k;
+      d.trans_a = plan.transA;
+      d.trans_b = plan.transB;
+      d.prec_a = static_cast<int>(A.precision);
+      d.prec_b = static_cast<int>(B.precision);
+      d.prec_c = static_cast<int>(C.precision);
+      d.math = op.flags[3];
+      d.cta_group = 2;
+      d.max_ctas = opts_.gemmMaxCtas;
+      d.alpha = op.s0;
+      d.beta = op.s1;
+      d.ldc = ct.ld;
+      const void* ap = nullptr;
+      const void* bp = nullptr;
+      if (!alphaZero) {
+        std::size_t ri = 0, ci = 0;
+        while (!(e.rowStart >= plan.rowsOf[w.rank][ri].first && e.rowStart < plan.rowsOf[w.rank][ri].second)) ++ri;
+        while (!(e.colStart >= plan.colsOf[w.rank][ci].first && e.colStart < plan.colsOf[w.rank][ci].second)) ++ci;
+        const BandView av = aViews[w.rank][ri];
+        const BandView bv = bViews[w.rank][ci];
+        const std::uint64_t roff = e.rowStart - plan.rowsOf[w.rank][ri].first;
+        const std::uint64_t coff = e.colStart - plan.colsOf[w.rank][ci].first;
+        ap = plan.transA ? static_cast<const std::uint8_t*>(av.ptr) + roff * ebA
+                         : static_cast<const std::uint8_t*>(av.ptr) + roff * av.ld * ebA;
+        bp = plan.transB ? static_cast<const std::uint8_t*>(bv.ptr) + coff * bv.ld * ebB
+                         : static_cast<const std::uint8_t*>(bv.ptr) + coff * ebB;
+        d.lda = av.ld;
+        d.ldb = bv.ld;
+      }
+      const std::uint64_t wsb = alphaZero ? 0 : gemmWorkspaceBytes(d, ap, bp);
+      void* ws = wsb ? w.workspace(wsb) : nullptr;
+      gemmLocal(d, ap, bp, ct.ptr, ws, wsb, w.compute);
+    }
+    cudaCheck(cudaEventRecord(w.tEnd, w.compute), "gemm: timing");
+  });
+}
+
+void Session::synchronize() {
+  forEachLocal([&](Worker& w) {
+    cudaCheck(cudaStreamSynchronize(w.comm), "sync comm");
+    cudaCheck(cudaStreamSynchronize(w.compute), "sync compute");
+  });
+}
+
+std::vector<float> Session::lastOpDeviceMs() {
+  std::vector<float> out;
+  forEachLocal([&](Worker& w) {
+    float ms = 0.0f;
+    if (w.timed) {
+      cudaCheck(cudaEventSynchronize(w.tEnd), "timing sync");
+      cudaCheck(cudaEventElapsedTime(&ms, w.tStart, w.tEnd), "timing");
+    }
+    out.push_back(ms);
+  });
+  return out;
+}
+
+// ---------------------------------------------------------------- replication
+
+ReplicationHandle Session::replicateAsync(DistMatrix m) {
+  const MatrixDescriptor& d = descriptor(m.id());
+  const ReplicationHandle h{m.id(), d.version};
+  if (d.replicaFresh()) return h;  // coalesce onto the existing job / replica
+  OpDescriptor op;
+  op.opcode = OpCode::ReplicateStart;
+  op.ids[0] = m.id();
+  op.ids[1] = opts_.replicationChunkBytes;
+  issue(op);
+  execReplicate(m.id());
+  return h;
+}
+
+void Session::execReplicate(std::uint64_t id) {
+  const MatrixDescriptor& M = lookup(table_, id);
+  const std::uint64_t eb = bytesOf(M.precision);
+  std::vector<Xfer> xs;
+  std::vector<Worker*> targets;
+  for (std::uint32_t r = 0; r < opts_.workers; ++r) {
+    Worker* w = local(r);
+    ReplicaEntry* entry = nullptr;
+    if (w) {
+      w->activate();
+      ReplicaEntry& e = w->replicas[id];
+      const std::uint64_t ld = paddedLd(M.cols, eb);
+      if (!e.full || e.ld != ld) {
+        if (e.full) w->arena.free(e.full, w->comm);
+        e.full = w->arena.alloc(M.rows * ld * eb, w->comm);
+        e.ld = ld;
+      }
+      if (!e.ready) cudaCheck(cudaEventCreateWithFlags(&e.ready, cudaEventDisableTiming), "replica event");
+      e.version = M.version;
+      e.state = ReplicaState::Pending;
+      entry = &e;
+      targets.push_back(w);
+    }
+    for (const auto& t : M.layout.tiles) {
+      const std::uint32_t src = t.second.rank;
+      Worker* sw = local(src);
+      if (!w && !sw) continue;
+      Xfer x;
+      x.src = src;
+      x.dst = r;
+      x.rows = t.first.rowCount;
+      x.cols = t.first.colCount;
+      x.eb = static_cast<std::uint32_t>(eb);
+      if (sw)
+        for (const DeviceTile& dt : sw->tiles.at(id))
+          if (dt.extent == t.first) {
+            x.srcPtr = dt.ptr;
+            x.srcLd = dt.ld;
+          }
+      if (entry) {
+        x.dstPtr = static_cast<std::uint8_t*>(entry->full) + (t.first.rowStart * entry->ld + t.first.colStart) * eb;
+        x.dstLd = entry->ld;
+      }
+      xs.push_back(x);
+    }
+  }
+  exchange(xs, true);
+  for (Worker* w : targets) {
+    w->activate();
+    cudaCheck(cudaEventRecord(w->replicas[id].ready, w->comm), "replica ready");
+  }
+}
+
+ReplState Session::handleState(const ReplicationHandle& h) {
+  if (replFailed_.count({h.matrixId, h.version})) return ReplState::Failed;
+  auto it = table_.find(h.matrixId);
+  if (it == table_.end()) return ReplState::Failed;
+  bool inflight = false;
+  for (auto& wp : workers_) {
+    if (!wp) continue;
+    auto rit = wp->replicas.find(h.matrixId);
+    if (rit == wp->replicas.end()) return ReplState::Failed;
+    ReplicaEntry& e = rit->second;
+    if (e.version < h.version) return ReplState::Failed;
+    if (e.version > h.version) continue;  // superseded by a newer completed job
+    if (e.state == ReplicaState::Stale) return ReplState::Failed;
+    if (e.state == ReplicaState::Pending) {
+      wp->activate();
+      const cudaError_t q = cudaEventQuery(e.ready);
+      if (q == cudaSuccess) e.state = ReplicaState::Valid;
+      else if (q == cudaErrorNotReady) inflight = true;
+      else throw Error(std::string("replica: ") + cudaGetErrorString(q));
+    }
+  }
+  return inflight ? ReplState::InFlight : ReplState::Done;
+}
+
+ReplState Session::wait(const ReplicationHandle& h) {
+  for (auto& wp : workers_) {
+    if (!wp) continue;
+    auto rit = wp->replicas.find(h.matrixId);
+    if (rit != wp->replicas.end() && rit->second.version == h.version &&
+        rit->second.state == ReplicaState::Pending) {
+      wp->activate();
+      cudaCheck(cudaEventSynchronize(rit->second.ready), "replica wait");
+    }
+  }
+  return handleState(h);
+}
+
+void Session::replicateSync(DistMatrix m) {
+  if (wait(replicateAsync(m)) != ReplState::Done) throw Error("replication failed");
+}
+
+// ---------------------------------------------------------------- introspection
+
+void Session::verifyMetadataConsistency() {
+  const std::uint64_t expected = tableHash(table_);
+  for (auto& w : workers_)
+    if (w && tableHash(w->descs) != expected)
+      throw Error("metadata divergence on worker " + std::to_string(w->rank));
+}
+
+std::vector<WorkerStatsRow> Session::queryWorkerStats() {
+  std::vector<WorkerStatsRow> rows;
+  for (auto& w : workers_) {
+    if (!w) continue;
+    const gm_arena_stats s = w->arena.stats();
+    WorkerStatsRow r;
+    r.osAllocations = s.allocations_from_os;
+    r.reuses = s.reuses;
+    r.frees = s.frees;
+    r.heldBytes = s.held_bytes;
+    r.residentBytes = w->residentBytes;
+    r.cacheHits = w->cache.hits;
+    r.cacheMisses = w->cache.misses;
+    r.cacheBytes = w->cache.bytes();
+    r.bytesSent = w->bytesSent;
+    r.bytesReceived = w->bytesReceived;
+    rows.push_back(r);
+  }
+  return rows;
+}
+
+// ---------------------------------------------------------------- free function
+
+void gemm(Session& s, DistMatrix a, DistMatrix b, DistMatrix c, double alpha, double beta,
+          bool transA, bool transB) {
+  OpDescriptor op;
+  op.opcode = OpCode::Gemm;
+  op.ids[0] = a.id();
+  op.ids[1] = b.id();
+  op.ids[2] = c.id();
+  op.s0 = alpha;
+  op.s1 = beta;
+  op.flags[0] = transA ? 1 : 0;
+  op.flags[1] = transB ? 1 : 0;
+  op.flags[2] = s.deterministic() ? 1 : 0;
+  s.runGemm(op, true);
+}
+
+}  // namespace gridmath

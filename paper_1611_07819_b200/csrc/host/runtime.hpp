@@ -1,0 +1,287 @@
+// SPDX-License-Identifier: Apache-2.0
+// Master / worker runtime of the B200 drop-in (namespace gridmath).
+//
+// Reference structure kept (proj/include/gridmath/session.hpp:62-179,
+// worker.hpp:63-139): a master `Session` owns the descriptor table and issues
+// OpDescriptors; every worker mirrors the table via applyOpMetadata and
+// executes the op on its own tiles. What changes is where things live:
+//   * one worker per GPU slot: tiles, replicas and cached panels are device
+//     buffers from a per-worker pooled arena (DeviceArena);
+//   * a worker's "thread" is its pair of CUDA streams (compute + comm); the
+//     master enqueues async device work instead of waking host threads;
+//   * the data plane is copy-engine peer copies (all workers in one
+//     process) or NCCL point-to-point / broadcast (one process per GPU,
+//     SPMD: every process runs the master logic redundantly -- planning is a
+//     pure function of the replicated descriptor table, so all ranks agree on
+//     every transfer without negotiation, like the reference's
+//     "same pure planning functions on every actor", pieces.hpp:29-31).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <array>
+#include <cstdint>
+#include <functional>
+#include <list>
+#include <map>
+#include <memory>
+#include <set>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "../../../include/gridmath_b200.h"
+#include "core.hpp"
+#include "device.hpp"
+#include "ops.hpp"
+
+namespace gridmath {
+
+class Session;
+
+class DistMatrix {
+ public:
+  DistMatrix() = default;
+  DistMatrix(Session* s, std::uint64_t id) : session_(s), id_(id) {}
+  std::uint64_t id() const { return id_; }
+  std::uint64_t rows() const;
+  std::uint64_t cols() const;
+  Precision precision() const;
+  bool valid() const { return session_ != nullptr; }
+
+ private:
+  Session* session_ = nullptr;
+  std::uint64_t id_ = 0;
+};
+
+enum class ReplState : std::uint8_t { InFlight, Done, Failed };
+
+struct ReplicationHandle {
+  std::uint64_t matrixId = 0;
+  std::uint64_t version = 0;
+};
+
+struct SessionOptions {
+  std::uint32_t workers = 1;
+  bool deterministic = true;
+  std::uint64_t replicationChunkBytes = 1ull << 20;
+  std::uint64_t rootSeed = 0;
+  bool checkMetadataEveryOp = false;
+  // --- B200 placement / data plane ---
+  int spmdRank = -1;                  // >= 0: this process hosts only worker spmdRank
+  std::vector<int> devices;           // worker r -> devices[r % size]; empty = all visible
+  std::array<std::uint8_t, 128> ncclId{};
+  int gemmMaxCtas = 0;                // cap the GEMM grid (0 = all SMs)
+  std::uint64_t panelCacheBytes = 0;  // per worker; 0 = 1/4 of device memory
+  int transport = 0;                  // 0 auto, 1 NCCL, 2 copy engine
+  int pipelineChunks = 0;             // SUMMA row chunks (0 = auto)
+};
+
+struct WorkerStatsRow {
+  std::uint64_t osAllocations = 0, reuses = 0, frees = 0, heldBytes = 0, residentBytes = 0;
+  std::uint64_t cacheHits = 0, cacheMisses = 0, cacheBytes = 0;
+  std::uint64_t bytesSent = 0, bytesReceived = 0;
+};
+
+struct DeviceTile {
+  TileExtent extent;
+  void* ptr = nullptr;
+  std::uint64_t ld = 0;  // pitch in elements (16-byte multiple when possible)
+};
+
+// "Keep what you've seen": operand bands a worker gathered for a GEMM stay
+// resident, keyed by (matrix, version, rect), and are reused by later GEMMs
+// that need the same region (e.g. W gathered in the forward pass, read again
+// transposed by the backward dX GEMM). Entries die when the matrix version
+// moves or the matrix is destroyed; LRU eviction keeps the cache within its
+// byte budget. The directory is replicated on every SPMD rank (metadata
+// only for non-local workers) and updated by the same deterministic rules,
+// so every rank knows which transfers a peer will post.
+struct CacheEntry {
+  std::uint64_t matrixId = 0, version = 0;
+  Rect rect;
+  std::uint64_t bytes = 0;
+  std::uint64_t lastUse = 0;
+  void* ptr = nullptr;  // local workers only
+  std::uint64_t ld = 0;
+  cudaEvent_t ready = nullptr;
+};
+
+class PanelCache {
+ public:
+  CacheEntry* lookup(std::uint64_t id, std::uint64_t version, const Rect& r, std::uint64_t tick);
+  // Returns entries evicted to make room (caller frees their buffers).
+  std::vector<CacheEntry> reserve(std::uint64_t bytes, std::uint64_t budget, std::uint64_t protectTick);
+  CacheEntry& insert(CacheEntry e);
+  std::vector<CacheEntry> dropMatrix(std::uint64_t id, bool keepCurrent, std::uint64_t version);
+  std::vector<CacheEntry> dropAll();
+  std::uint64_t bytes() const { return bytes_; }
+  std::uint64_t hits = 0, misses = 0;
+
+ private:
+  std::list<CacheEntry> entries_;
+  std::uint64_t bytes_ = 0;
+};
+
+enum class ReplicaState : std::uint8_t { Valid = 0, Pending = 1, Stale = 2 };
+
+struct ReplicaEntry {
+  void* full = nullptr;  // whole matrix, row-major, pitch `ld`
+  std::uint64_t ld = 0;
+  std::uint64_t version = 0;
+  ReplicaState state = ReplicaState::Pending;
+  cudaEvent_t ready = nullptr;
+};
+
+struct BandView {
+  const void* ptr = nullptr;
+  std::uint64_t ld = 0;
+};
+
+// Per-worker device state (reference WorkerRuntime, worker.hpp:63-139).
+class Worker {
+ public:
+  Worker(std::uint32_t rank, int device, std::uint64_t cacheBudget);
+  ~Worker();
+  Worker(const Worker&) = delete;
+  Worker& operator=(const Worker&) = delete;
+
+  void activate() const;
+  cudaEvent_t event();            // from a recycled pool
+  void recycle(cudaEvent_t e);
+  void* workspace(std::uint64_t bytes);
+  // Stream-ordered WAR guard: readers of this worker's tiles register their
+  // completion events; the compute stream waits on them before any mutation.
+  // `owner` is the worker whose pool the event came from (recycled there).
+  void addReader(cudaEvent_t e, Worker* owner) { readers_.push_back({e, owner}); }
+  void beforeMutation();
+  void releaseReaders();
+
+  std::uint32_t rank;
+  int device;
+  cudaStream_t compute = nullptr, comm = nullptr;
+  DeviceArena arena;
+  DescriptorTable descs;
+  std::map<std::uint64_t, std::vector<DeviceTile>> tiles;
+  std::map<std::uint64_t, ReplicaEntry> replicas;
+  PanelCache cache;
+  std::uint64_t cacheBudget;
+  std::uint64_t residentBytes = 0, bytesSent = 0, bytesReceived = 0;
+  cudaEvent_t tStart = nullptr, tEnd = nullptr;
+  bool timed = false;
+  ncclComm_t nccl = nullptr;
+
+ private:
+  std::vector<cudaEvent_t> pool_;
+  std::vector<std::pair<cudaEvent_t, Worker*>> readers_;
+  void* ws_ = nullptr;
+  std::uint64_t wsBytes_ = 0;
+};
+
+// One movement of a sub-rectangle between workers (reference PieceRoute,
+// pieces.hpp:33-40). Pointers are valid only on the side that is local.
+struct Xfer {
+  std::uint32_t src = 0, dst = 0;
+  const void* srcPtr = nullptr;
+  std::uint64_t srcLd = 0;
+  void* dstPtr = nullptr;
+  std::uint64_t dstLd = 0;
+  std::uint64_t rows = 0, cols = 0;
+  std::uint32_t eb = 0;
+};
+
+// Pure GEMM planning (no device state): merged C row/col intervals per
+// worker and one need per interval over the full k range, resolved to the
+// replica, a containing local tile, a cached panel (probe callback), or a
+// gather from the owners of the intersecting tiles (reference planGemm,
+// kernels.cpp:204-251, and NeedPlanner::addNeed, pieces.cpp:14-30).
+struct PlannedNeed {
+  enum Kind : std::uint8_t { Replica, LocalTile, Cached, Gather } kind = Gather;
+  std::uint32_t worker = 0;
+  int operand = 0;  // 0 = A, 1 = B
+  std::size_t interval = 0;
+  Rect rect;
+  std::vector<PieceRoute> pieces;  // Gather only (src == worker allowed)
+};
+
+struct GemmPlanB200 {
+  std::uint64_t m = 0, n = 0, k = 0;
+  bool transA = false, transB = false;
+  std::vector<std::vector<std::pair<std::uint64_t, std::uint64_t>>> rowsOf, colsOf;
+  std::vector<PlannedNeed> needs;  // worker-major: A intervals then B intervals
+};
+
+using CacheProbe = std::function<bool(std::uint32_t worker, const MatrixDescriptor&, const Rect&)>;
+GemmPlanB200 planGemmB200(const DescriptorTable& t, const OpDescriptor& op, std::uint32_t workers,
+                          const CacheProbe& cached);
+// Remote bytes each worker receives under `plan` (the panel-traffic figure).
+std::vector<std::uint64_t> planRemoteBytes(const GemmPlanB200& plan, const DescriptorTable& t,
+                                           std::uint32_t workers);
+
+class Session {
+ public:
+  explicit Session(SessionOptions opts = {});
+  ~Session();
+  Session(const Session&) = delete;
+  Session& operator=(const Session&) = delete;
+
+  DistMatrix createMatrix(std::uint64_t rows, std::uint64_t cols, Precision p, const Layout& layout);
+  void destroy(DistMatrix m);
+  void setData(DistMatrix m, const std::vector<double>& rowMajor);
+  void setDataF32(DistMatrix m, const std::vector<float>& rowMajor);
+  void setDataRaw(DistMatrix m, const void* image, std::uint64_t bytes);
+  void fillUniform(DistMatrix m, std::uint64_t seed, double lo, double hi);
+  std::vector<double> getData(DistMatrix m);
+  std::vector<std::uint8_t> getDataRaw(DistMatrix m);
+  void getDataRawInto(DistMatrix m, void* image, std::uint64_t bytes, bool localOnly);
+
+  ReplicationHandle replicateAsync(DistMatrix m);
+  void replicateSync(DistMatrix m);
+  ReplState wait(const ReplicationHandle& h);
+  ReplState handleState(const ReplicationHandle& h);
+
+  void verifyMetadataConsistency();
+  std::vector<WorkerStatsRow> queryWorkerStats();
+  const MatrixDescriptor& descriptor(std::uint64_t id) const;
+  const DescriptorTable& table() const { return table_; }
+  std::uint32_t workerCount() const { return opts_.workers; }
+  bool deterministic() const { return opts_.deterministic; }
+  const SessionOptions& options() const { return opts_; }
+  std::vector<std::uint32_t> localRanks() const;
+
+  // Issues a Gemm op (gemm() below wraps it). sync: wait for completion
+  // like the reference's acked gemm(); otherwise stream-ordered only.
+  void runGemm(const OpDescriptor& op, bool sync);
+  void synchronize();
+  std::vector<float> lastOpDeviceMs();
+
+ private:
+  std::uint64_t issue(OpDescriptor& op);  // validate + metadata + per-worker mirror
+  Worker* local(std::uint32_t rank) const;
+  bool isLocal(std::uint32_t rank) const;
+  void execCreate(const OpDescriptor& op);
+  void execDestroy(std::uint64_t id);
+  void execGemm(const OpDescriptor& op);
+  void execReplicate(std::uint64_t id);
+  void mutationHook(std::uint64_t id, std::uint64_t oldVersion);
+  void exchange(std::vector<Xfer>& xs, bool onComm);
+  void forEachLocal(const std::function<void(Worker&)>& f);
+  void checkErrors(std::vector<std::string>& errs);
+
+  SessionOptions opts_;
+  DescriptorTable table_;
+  std::vector<std::unique_ptr<Worker>> workers_;  // indexed by rank; null if remote
+  std::vector<PanelCache> remoteCaches_;          // directory for non-local workers (SPMD)
+  std::map<std::pair<std::uint64_t, std::uint64_t>, bool> replFailed_;
+  std::uint64_t nextMatrixId_ = 1;
+  std::uint64_t nextExec_ = 1;
+  std::uint64_t tick_ = 0;
+  bool nccl_ = false;
+  bool peerCopies_ = false;
+};
+
+void gemm(Session& s, DistMatrix a, DistMatrix b, DistMatrix c, double alpha, double beta,
+          bool transA = false, bool transB = false);
+
+}  // namespace gridmath

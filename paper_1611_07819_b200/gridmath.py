@@ -1,0 +1,304 @@
+# SPDX-License-Identifier: Apache-2.0
+"""Python mirror of the reference's gridmath master API over the C ABI.
+
+Names and argument meaning follow the reference C++ library
+(/root/reference/proj/include/gridmath/session.hpp:21-179, layout.hpp:62-85,
+precision.hpp:12) so parity tests read like the reference's own usage:
+
+    s = Session(workers=4)
+    A = s.createMatrix(m, k, Precision.BF16, makeGridLayout(m, k, 2, 2, makeWorkerGroup(4)))
+    s.setDataRaw(A, image)
+    gemm(s, A, B, C, 1.0, 0.0)
+    out = s.getDataRaw(C)
+
+Every call goes through libgridmath_b200.so (include/gridmath_b200.h); there
+is no Python compute path. Errors raise GmError (the reference's
+gridmath::Error).
+"""
+from __future__ import annotations
+
+import ctypes
+import enum
+from dataclasses import dataclass
+from typing import List, Optional, Sequence
+
+import numpy as np
+
+from . import _lib
+from ._lib import GmError, check
+
+__all__ = ["Precision", "TileExtent", "Layout", "makeWorkerGroup", "makeRowBlockLayout",
+           "makeColBlockLayout", "makeGridLayout", "makeSingleTileLayout", "validateLayout",
+           "Session", "DistMatrix", "ReplicationHandle", "ReplState", "gemm", "GmError",
+           "nccl_unique_id", "np_storage_dtype"]
+
+
+class Precision(enum.IntEnum):
+    Half = _lib.GM_HALF
+    Single = _lib.GM_SINGLE
+    Double = _lib.GM_DOUBLE
+    BF16 = _lib.GM_BF16
+
+
+def np_storage_dtype(p: Precision):
+    """numpy container of a storage precision (bf16 held as raw uint16)."""
+    return {Precision.Half: np.float16, Precision.Single: np.float32,
+            Precision.Double: np.float64, Precision.BF16: np.uint16}[Precision(p)]
+
+
+def bytes_of(p: Precision) -> int:
+    return {Precision.Half: 2, Precision.Single: 4, Precision.Double: 8, Precision.BF16: 2}[Precision(p)]
+
+
+class ReplState(enum.IntEnum):
+    InFlight = _lib.GM_REPL_IN_FLIGHT
+    Done = _lib.GM_REPL_DONE
+    Failed = _lib.GM_REPL_FAILED
+
+
+@dataclass(frozen=True)
+class TileExtent:
+    rowStart: int
+    rowCount: int
+    colStart: int
+    colCount: int
+
+
+@dataclass
+class Layout:
+    tiles: List[tuple]  # [(TileExtent, owner rank)]
+
+    def as_c(self):
+        arr = (_lib.gm_tile * max(1, len(self.tiles)))()
+        for i, (e, w) in enumerate(self.tiles):
+            arr[i] = _lib.gm_tile(e.rowStart, e.rowCount, e.colStart, e.colCount, int(w))
+        return arr
+
+    def as_tuples(self):
+        return [(e.rowStart, e.rowCount, e.colStart, e.colCount, int(w)) for e, w in self.tiles]
+
+
+def _from_c(arr, n) -> Layout:
+    return Layout([(TileExtent(t.row_start, t.row_count, t.col_start, t.col_count), t.owner)
+                   for t in arr[:n]])
+
+
+def makeWorkerGroup(count: int) -> List[int]:
+    return list(range(count))
+
+
+def _call_layout(fn, *args) -> Layout:
+    lib = _lib.load()
+    cap = 4096
+    arr = (_lib.gm_tile * cap)()
+    n = ctypes.c_uint32()
+    check(getattr(lib, fn)(*args, arr, cap, ctypes.byref(n)))
+    return _from_c(arr, n.value)
+
+
+def makeRowBlockLayout(rows: int, cols: int, workers: Sequence[int]) -> Layout:
+    return _call_layout("gm_layout_row_block", rows, cols, len(workers))
+
+
+def makeColBlockLayout(rows: int, cols: int, workers: Sequence[int]) -> Layout:
+    return _call_layout("gm_layout_col_block", rows, cols, len(workers))
+
+
+def makeGridLayout(rows: int, cols: int, pr: int, pc: int, workers: Sequence[int]) -> Layout:
+    if pr * pc != len(workers):
+        raise GmError("makeGridLayout: pr*pc must equal worker count")
+    return _call_layout("gm_layout_grid", rows, cols, pr, pc)
+
+
+def makeSingleTileLayout(rows: int, cols: int, owner: int) -> Layout:
+    return Layout([(TileExtent(0, rows, 0, cols), owner)])
+
+
+def validateLayout(rows: int, cols: int, layout: Layout, workerCount: int = 0) -> int:
+    """0 ok, 1 overlap, 2 gap, 3 out of range, 4 unknown worker."""
+    v = ctypes.c_int32()
+    check(_lib.load().gm_layout_validate(rows, cols, layout.as_c(), len(layout.tiles), workerCount,
+                                         ctypes.byref(v)))
+    return v.value
+
+
+def nccl_unique_id() -> bytes:
+    buf = (ctypes.c_uint8 * 128)()
+    check(_lib.load().gm_nccl_unique_id(ctypes.byref(buf)))
+    return bytes(buf)
+
+
+@dataclass(frozen=True)
+class DistMatrix:
+    session: "Session"
+    id: int
+
+    def info(self):
+        rows, cols, ver, rv = ctypes.c_uint64(), ctypes.c_uint64(), ctypes.c_uint64(), ctypes.c_uint64()
+        prec = ctypes.c_int32()
+        check(_lib.load().gm_matrix_info(self.session._h, self.id, ctypes.byref(rows), ctypes.byref(cols),
+                                         ctypes.byref(prec), ctypes.byref(ver), ctypes.byref(rv)))
+        return rows.value, cols.value, Precision(prec.value), ver.value, rv.value
+
+    def rows(self) -> int:
+        return self.info()[0]
+
+    def cols(self) -> int:
+        return self.info()[1]
+
+    def precision(self) -> Precision:
+        return self.info()[2]
+
+    def version(self) -> int:
+        return self.info()[3]
+
+
+@dataclass(frozen=True)
+class ReplicationHandle:
+    matrixId: int
+    version: int
+
+
+class Session:
+    """gridmath::Session. workers = P. spmd_rank >= 0 selects one-process-per-GPU
+    mode (this process hosts worker spmd_rank on `devices[0]`)."""
+
+    def __init__(self, workers: int = 1, deterministic: bool = True, devices: Optional[Sequence[int]] = None,
+                 spmd_rank: int = -1, nccl_id: Optional[bytes] = None, gemm_max_ctas: int = 0,
+                 transport: int = 0, check_metadata_every_op: bool = False):
+        lib = _lib.load()
+        o = _lib.gm_session_options()
+        lib.gm_session_options_default(ctypes.byref(o))
+        o.workers = workers
+        o.deterministic = 1 if deterministic else 0
+        o.spmd_rank = spmd_rank
+        o.check_metadata_every_op = 1 if check_metadata_every_op else 0
+        devs = list(devices or [])
+        o.num_devices = len(devs)
+        for i, d in enumerate(devs[:16]):
+            o.devices[i] = d
+        if nccl_id is not None:
+            ctypes.memmove(o.nccl_unique_id, nccl_id, 128)
+        o.gemm_max_ctas = gemm_max_ctas
+        o.transport = transport
+        self._h = ctypes.c_void_p()
+        check(lib.gm_session_create(ctypes.byref(o), ctypes.byref(self._h)))
+        self.workers = workers
+        self.deterministic = deterministic
+
+    def close(self):
+        if self._h:
+            check(_lib.load().gm_session_destroy(self._h))
+            self._h = ctypes.c_void_p()
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # --- lifecycle ------------------------------------------------------------
+    def createMatrix(self, rows: int, cols: int, prec: Precision, layout: Layout) -> DistMatrix:
+        mid = ctypes.c_uint64()
+        check(_lib.load().gm_matrix_create(self._h, rows, cols, int(prec), layout.as_c(),
+                                           len(layout.tiles), ctypes.byref(mid)))
+        return DistMatrix(self, mid.value)
+
+    def destroy(self, m: DistMatrix):
+        check(_lib.load().gm_matrix_destroy(self._h, m.id))
+
+    def setDataRaw(self, m: DistMatrix, image: np.ndarray):
+        img = np.ascontiguousarray(image)
+        check(_lib.load().gm_matrix_set_raw(self._h, m.id, img.ctypes.data, img.nbytes))
+
+    def setDataRawPtr(self, m: DistMatrix, ptr: int, nbytes: int):
+        check(_lib.load().gm_matrix_set_raw(self._h, m.id, ptr, nbytes))
+
+    def setData(self, m: DistMatrix, values):
+        v = np.ascontiguousarray(values, dtype=np.float64).ravel()
+        check(_lib.load().gm_matrix_set_f64(self._h, m.id, v.ctypes.data, v.size))
+
+    def setDataF32(self, m: DistMatrix, values):
+        v = np.ascontiguousarray(values, dtype=np.float32).ravel()
+        check(_lib.load().gm_matrix_set_f32(self._h, m.id, v.ctypes.data, v.size))
+
+    def fillUniform(self, m: DistMatrix, seed: int, lo: float = -1.0, hi: float = 1.0):
+        check(_lib.load().gm_matrix_fill_uniform(self._h, m.id, seed, lo, hi))
+
+    def getDataRaw(self, m: DistMatrix, local_only: bool = False) -> np.ndarray:
+        rows, cols, prec, _, _ = m.info()
+        out = np.zeros((rows, cols), dtype=np_storage_dtype(prec))
+        fn = _lib.load().gm_matrix_get_local_raw if local_only else _lib.load().gm_matrix_get_raw
+        check(fn(self._h, m.id, out.ctypes.data, out.nbytes))
+        return out
+
+    def getDataRawPtr(self, m: DistMatrix, ptr: int, nbytes: int, local_only: bool = True):
+        fn = _lib.load().gm_matrix_get_local_raw if local_only else _lib.load().gm_matrix_get_raw
+        check(fn(self._h, m.id, ptr, nbytes))
+
+    def getData(self, m: DistMatrix) -> np.ndarray:
+        raw = self.getDataRaw(m)
+        if m.precision() == Precision.BF16:
+            return (raw.astype(np.uint32) << 16).view(np.float32).astype(np.float64)
+        return raw.astype(np.float64)
+
+    # --- replication -------------------------------------------------------------
+    def replicateAsync(self, m: DistMatrix) -> ReplicationHandle:
+        v = ctypes.c_uint64()
+        check(_lib.load().gm_replicate_async(self._h, m.id, ctypes.byref(v)))
+        return ReplicationHandle(m.id, v.value)
+
+    def replicateSync(self, m: DistMatrix):
+        check(_lib.load().gm_replicate_sync(self._h, m.id))
+
+    def wait(self, h: ReplicationHandle) -> ReplState:
+        st = ctypes.c_int32()
+        check(_lib.load().gm_replicate_wait(self._h, h.matrixId, h.version, ctypes.byref(st)))
+        return ReplState(st.value)
+
+    def handleState(self, h: ReplicationHandle) -> ReplState:
+        st = ctypes.c_int32()
+        check(_lib.load().gm_replicate_state(self._h, h.matrixId, h.version, ctypes.byref(st)))
+        return ReplState(st.value)
+
+    # --- introspection -----------------------------------------------------------
+    def queryWorkerStats(self):
+        rows = (_lib.gm_worker_stats * 64)()
+        n = ctypes.c_uint32()
+        check(_lib.load().gm_query_worker_stats(self._h, rows, 64, ctypes.byref(n)))
+        keys = [f[0] for f in _lib.gm_worker_stats._fields_]
+        return [{k: getattr(r, k) for k in keys} for r in rows[: n.value]]
+
+    def verifyMetadataConsistency(self):
+        check(_lib.load().gm_verify_metadata(self._h))
+
+    def localWorkers(self) -> List[int]:
+        arr = (ctypes.c_uint32 * 64)()
+        n = ctypes.c_uint32()
+        check(_lib.load().gm_session_local_workers(self._h, arr, 64, ctypes.byref(n)))
+        return list(arr[: n.value])
+
+    def synchronize(self):
+        check(_lib.load().gm_session_synchronize(self._h))
+
+    def lastOpDeviceMs(self) -> List[float]:
+        arr = (ctypes.c_float * 64)()
+        n = ctypes.c_uint32()
+        check(_lib.load().gm_last_op_device_ms(self._h, arr, 64, ctypes.byref(n)))
+        return list(arr[: n.value])
+
+    def gemmAsync(self, a: DistMatrix, b: DistMatrix, c: DistMatrix, alpha=1.0, beta=0.0,
+                  transA=False, transB=False):
+        check(_lib.load().gm_gemm_async(self._h, a.id, b.id, c.id, alpha, beta, int(transA), int(transB)))
+
+
+def gemm(s: Session, a: DistMatrix, b: DistMatrix, c: DistMatrix, alpha: float, beta: float,
+         transA: bool = False, transB: bool = False, math: int = _lib.GM_MATH_DEFAULT):
+    """gridmath::gemm (session.hpp:161-162): C = alpha*op(A)*op(B) + beta*C."""
+    check(_lib.load().gm_gemm_ex(s._h, a.id, b.id, c.id, alpha, beta, int(transA), int(transB), math))

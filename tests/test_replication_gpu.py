@@ -1,0 +1,128 @@
+# SPDX-License-Identifier: Apache-2.0
+"""Replication, the "keep what you've seen" panel cache and the pooled
+arena (reference session.cpp:329-375, worker.cpp:245-448, pool.cpp; spec
+acceptance #4 and #5)."""
+import numpy as np
+import pytest
+
+import oracle as O
+from paper_1611_07819_b200 import gridmath as G
+
+pytestmark = pytest.mark.gpu
+
+
+def _fc_setup(s, batch, fan_in, fan_out, p, prec=G.Precision.BF16):
+    g = G.makeWorkerGroup(p)
+    X = s.createMatrix(batch, fan_in, prec, G.makeRowBlockLayout(batch, fan_in, g))
+    W = s.createMatrix(fan_in, fan_out, prec, G.makeColBlockLayout(fan_in, fan_out, g))
+    Z = s.createMatrix(batch, fan_out, G.Precision.Single, G.makeRowBlockLayout(batch, fan_out, g))
+    D = s.createMatrix(batch, fan_out, prec, G.makeRowBlockLayout(batch, fan_out, g))
+    dW = s.createMatrix(fan_in, fan_out, G.Precision.Single, G.makeColBlockLayout(fan_in, fan_out, g))
+    dX = s.createMatrix(batch, fan_in, G.Precision.Single, G.makeRowBlockLayout(batch, fan_in, g))
+    return X, W, Z, D, dW, dX
+
+
+def test_replica_bytes_and_gemm_via_replica():
+    p, batch, fi, fo = 4, 256, 384, 320
+    with G.Session(workers=p) as s:
+        X, W, Z, D, dW, dX = _fc_setup(s, batch, fi, fo, p)
+        s.fillUniform(X, 1)
+        s.fillUniform(W, 2, -0.05, 0.05)
+        before = s.queryWorkerStats()
+        h = s.replicateAsync(W)
+        assert s.wait(h) == G.ReplState.Done
+        after = s.queryWorkerStats()
+        wbytes = fi * fo * 2
+        moved = sum(a["bytes_received"] - b["bytes_received"] for a, b in zip(after, before))
+        assert moved == (p - 1) * wbytes  # reference acceptance #4: (P-1) * bytes exactly
+        G.gemm(s, X, W, Z, 1.0, 0.0)      # forward reads W from the local replica
+        mid = s.queryWorkerStats()
+        assert sum(m["bytes_received"] - a["bytes_received"] for m, a in zip(mid, after)) == 0
+        x = s.getDataRaw(X)
+        w = s.getDataRaw(W)
+        z = s.getDataRaw(Z)
+    want = O.gemm_c(batch, fo, fi, x, 3, w, 3, np.zeros((batch, fo), np.float32), 1, 1.0, 0.0, 0, 0)
+    assert O.rel_fro(z, want) <= 1e-5
+
+
+def test_backward_reuses_forward_panels_without_replication():
+    # No replicateAsync: the forward GEMM gathers the full W band on every
+    # worker; the backward dX = dY W^T needs the same W rectangle and must
+    # hit the panel cache (0 bytes moved for W).
+    p, batch, fi, fo = 4, 256, 384, 320
+    with G.Session(workers=p) as s:
+        X, W, Z, D, dW, dX = _fc_setup(s, batch, fi, fo, p)
+        s.fillUniform(X, 1)
+        s.fillUniform(W, 2, -0.05, 0.05)
+        s.fillUniform(D, 3)
+        G.gemm(s, X, W, Z, 1.0, 0.0)
+        st1 = s.queryWorkerStats()
+        G.gemm(s, D, W, dX, 1.0, 0.0, False, True)
+        st2 = s.queryWorkerStats()
+        assert sum(b["cache_hits"] - a["cache_hits"] for a, b in zip(st1, st2)) >= p
+        assert sum(b["bytes_received"] - a["bytes_received"] for a, b in zip(st1, st2)) == 0
+        G.gemm(s, X, D, dW, 1.0, 0.0, True, False)  # dW = X^T dY gathers X and a dY band
+        x, w, d, dx, dw = (s.getDataRaw(m) for m in (X, W, D, dX, dW))
+    want_dx = O.gemm_c(batch, fi, fo, d, 3, w, 3, np.zeros((batch, fi), np.float32), 1, 1.0, 0.0, 0, 1)
+    want_dw = O.gemm_c(fi, fo, batch, x, 3, d, 3, np.zeros((fi, fo), np.float32), 1, 1.0, 0.0, 1, 0)
+    assert O.rel_fro(dx, want_dx) <= 1e-5
+    assert O.rel_fro(dw, want_dw) <= 1e-5
+
+
+def test_mutation_invalidates_replica_and_cache():
+    p, n = 2, 192
+    with G.Session(workers=p) as s:
+        g = G.makeWorkerGroup(p)
+        A = s.createMatrix(n, n, G.Precision.Single, G.makeRowBlockLayout(n, n, g))
+        B = s.createMatrix(n, n, G.Precision.Single, G.makeColBlockLayout(n, n, g))
+        C = s.createMatrix(n, n, G.Precision.Single, G.makeRowBlockLayout(n, n, g))
+        s.fillUniform(A, 1)
+        s.fillUniform(B, 2)
+        h = s.replicateAsync(B)
+        s.wait(h)
+        G.gemm(s, A, B, C, 1.0, 0.0)
+        s.fillUniform(B, 3)  # SetData bumps B.version: replica stale, not read
+        assert B.info()[4] != B.version()
+        G.gemm(s, A, B, C, 1.0, 0.0)
+        a, b, c = s.getDataRaw(A), s.getDataRaw(B), s.getDataRaw(C)
+        # replicate again at the new version
+        h2 = s.replicateAsync(B)
+        assert h2.version == h.version + 1 and s.wait(h2) == G.ReplState.Done
+    want = O.gemm_c(n, n, n, a, 1, b, 1, np.zeros((n, n), np.float32), 1, 1.0, 0.0, 0, 0)
+    assert O.rel_fro(c, want) <= 1e-5
+
+
+def test_pool_zero_allocations_after_warmup():
+    # Reference acceptance #5: after one warm-up iteration, identical
+    # iterations perform no OS-level allocations (arena counters).
+    p, batch, fi, fo = 4, 256, 384, 320
+    with G.Session(workers=p) as s:
+        X, W, Z, D, dW, dX = _fc_setup(s, batch, fi, fo, p)
+        s.fillUniform(W, 2, -0.05, 0.05)
+
+        def step(i):
+            s.fillUniform(X, 10 + i)
+            s.fillUniform(D, 20 + i)
+            s.wait(s.replicateAsync(W))
+            G.gemm(s, X, W, Z, 1.0, 0.0)
+            G.gemm(s, X, D, dW, 1.0, 0.0, True, False)
+            G.gemm(s, D, W, dX, 1.0, 0.0, False, True)
+
+        step(0)
+        step(1)
+        base = [r["os_allocations"] for r in s.queryWorkerStats()]
+        for i in range(2, 12):
+            step(i)
+        assert [r["os_allocations"] for r in s.queryWorkerStats()] == base
+
+
+def test_destroy_frees_and_reuses():
+    with G.Session(workers=2) as s:
+        lay = G.makeRowBlockLayout(512, 512, [0, 1])
+        for i in range(5):
+            M = s.createMatrix(512, 512, G.Precision.Single, lay)
+            s.fillUniform(M, i)
+            s.destroy(M)
+        st = s.queryWorkerStats()
+        assert all(r["reuses"] >= 4 for r in st)
+        assert all(r["resident_bytes"] == 0 for r in st)
