@@ -220,6 +220,13 @@ int gm_matrix_get_raw(gm_session* s, uint64_t id, void* host, uint64_t bytes);
 /* Copy only the locally owned tiles into `host` (a full-size image); the
  * remaining bytes are left untouched. */
 int gm_matrix_get_local_raw(gm_session* s, uint64_t id, void* host, uint64_t bytes);
+/* Packed local-tile I/O for one-process-per-GPU use: `host` holds this
+ * process's tiles back to back in layout order, each row-major and dense
+ * (rowCount x colCount). Bytes must equal the local tiles' total. The
+ * matrix version moves exactly like setData. */
+int gm_matrix_local_bytes(gm_session* s, uint64_t id, uint64_t* bytes);
+int gm_matrix_set_local_packed(gm_session* s, uint64_t id, const void* host, uint64_t bytes);
+int gm_matrix_get_local_packed(gm_session* s, uint64_t id, void* host, uint64_t bytes);
 int gm_matrix_info(gm_session* s, uint64_t id, uint64_t* rows, uint64_t* cols, int32_t* prec,
                    uint64_t* version, uint64_t* replicated_version);
 
@@ -254,6 +261,18 @@ int gm_session_local_workers(gm_session* s, uint32_t* ranks, uint32_t cap, uint3
 /* Device time of the last gm_gemm/gm_gemm_async per local worker (ms),
  * measured with CUDA events on the worker's compute stream. */
 int gm_last_op_device_ms(gm_session* s, float* ms, uint32_t cap, uint32_t* n);
+/* Same, restricted to the local GEMM kernels of the last gemm (no exchange). */
+int gm_last_op_kernel_ms(gm_session* s, float* ms, uint32_t cap, uint32_t* n);
+
+/* Device timer over everything enqueued on the local workers' compute
+ * streams between start and stop (CUDA events on those streams). stop
+ * synchronizes and returns the max over local workers, in ms. */
+int gm_timer_start(gm_session* s);
+int gm_timer_stop(gm_session* s, float* max_ms);
+
+/* Number of this library's kernels launched by this process so far (GEMM,
+ * conversion, staging kernels). */
+int gm_kernel_launches(uint64_t* count);
 
 #ifdef __cplusplus
 }

@@ -111,6 +111,9 @@ _SIGNATURES = {
     "gm_matrix_fill_uniform": ([c_void_p, c_uint64, c_uint64, c_double, c_double], c_int32),
     "gm_matrix_get_raw": ([c_void_p, c_uint64, c_void_p, c_uint64], c_int32),
     "gm_matrix_get_local_raw": ([c_void_p, c_uint64, c_void_p, c_uint64], c_int32),
+    "gm_matrix_local_bytes": ([c_void_p, c_uint64, _P(c_uint64)], c_int32),
+    "gm_matrix_set_local_packed": ([c_void_p, c_uint64, c_void_p, c_uint64], c_int32),
+    "gm_matrix_get_local_packed": ([c_void_p, c_uint64, c_void_p, c_uint64], c_int32),
     "gm_matrix_info": ([c_void_p, c_uint64, _P(c_uint64), _P(c_uint64), _P(c_int32),
                         _P(c_uint64), _P(c_uint64)], c_int32),
     "gm_gemm": ([c_void_p, c_uint64, c_uint64, c_uint64, c_double, c_double, c_int32, c_int32],
@@ -127,6 +130,10 @@ _SIGNATURES = {
     "gm_query_worker_stats": ([c_void_p, _P(gm_worker_stats), c_uint32, _P(c_uint32)], c_int32),
     "gm_verify_metadata": ([c_void_p], c_int32),
     "gm_session_local_workers": ([c_void_p, _P(c_uint32), c_uint32, _P(c_uint32)], c_int32),
+    "gm_last_op_kernel_ms": ([c_void_p, _P(ctypes.c_float), c_uint32, _P(c_uint32)], c_int32),
+    "gm_timer_start": ([c_void_p], c_int32),
+    "gm_timer_stop": ([c_void_p, _P(ctypes.c_float)], c_int32),
+    "gm_kernel_launches": ([_P(c_uint64)], c_int32),
     "gm_last_op_device_ms": ([c_void_p, _P(ctypes.c_float), c_uint32, _P(c_uint32)], c_int32),
 }
 

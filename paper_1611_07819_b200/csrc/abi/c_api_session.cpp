@@ -6,6 +6,7 @@
 
 #include <cstring>
 
+#include "../cuda/convert.h"
 #include "../host/runtime.hpp"
 #include "abi_util.hpp"
 
@@ -143,6 +144,18 @@ int gm_matrix_get_raw(gm_session* s, uint64_t id, void* host, uint64_t bytes) {
 
 int gm_matrix_get_local_raw(gm_session* s, uint64_t id, void* host, uint64_t bytes) {
   return guard([&] { s->s->getDataRawInto(handle(s, id), host, bytes, true); });
+}
+
+int gm_matrix_local_bytes(gm_session* s, uint64_t id, uint64_t* bytes) {
+  return guard([&] { *bytes = s->s->localBytes(handle(s, id)); });
+}
+
+int gm_matrix_set_local_packed(gm_session* s, uint64_t id, const void* host, uint64_t bytes) {
+  return guard([&] { s->s->setLocalPacked(handle(s, id), host, bytes); });
+}
+
+int gm_matrix_get_local_packed(gm_session* s, uint64_t id, void* host, uint64_t bytes) {
+  return guard([&] { s->s->getLocalPacked(handle(s, id), host, bytes); });
 }
 
 int gm_matrix_info(gm_session* s, uint64_t id, uint64_t* rows, uint64_t* cols, int32_t* prec,
@@ -301,6 +314,26 @@ int gm_convert_host(const void* src, int32_t src_prec, void* dst, int32_t dst_pr
                             static_cast<uint8_t*>(dst), gridmath::precisionFromTag(static_cast<uint8_t>(dst_prec)),
                             count);
   });
+}
+
+int gm_last_op_kernel_ms(gm_session* s, float* ms, uint32_t cap, uint32_t* n) {
+  return guard([&] {
+    const auto v = s->s->lastOpKernelMs();
+    *n = static_cast<uint32_t>(v.size());
+    for (uint32_t i = 0; i < v.size() && i < cap; ++i) ms[i] = v[i];
+  });
+}
+
+int gm_timer_start(gm_session* s) {
+  return guard([&] { s->s->timerStart(); });
+}
+
+int gm_timer_stop(gm_session* s, float* max_ms) {
+  return guard([&] { *max_ms = s->s->timerStop(); });
+}
+
+int gm_kernel_launches(uint64_t* count) {
+  return guard([&] { *count = gmk::kernel_launches(); });
 }
 
 }  // extern "C"

@@ -14,6 +14,7 @@
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
+#include <atomic>
 #include <cstdint>
 
 #include "convert.h"
@@ -194,6 +195,13 @@ __global__ void scale_rect_kernel(void* __restrict__ c, int prec, uint64_t ld, u
 }
 
 namespace {
+std::atomic<uint64_t> g_launches{0};
+}  // namespace
+
+uint64_t kernel_launches() { return g_launches.load(); }
+void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+
+namespace {
 unsigned grid_for(uint64_t total) {
   uint64_t g = (total + 255) / 256;
   if (g > 148ull * 16) g = 148ull * 16;
@@ -206,6 +214,7 @@ cudaError_t convert_rect(const void* src, int sp, uint64_t sld, void* dst, int d
                          uint64_t rows, uint64_t cols, cudaStream_t s) {
   if (rows == 0 || cols == 0) return cudaSuccess;
   convert_rect_kernel<<<grid_for(rows * cols), 256, 0, s>>>(src, sp, sld, dst, dp, dld, rows, cols);
+  count_launch();
   return cudaGetLastError();
 }
 
@@ -213,6 +222,7 @@ cudaError_t split_tf32(const void* src, int sp, uint64_t sld, float* hi, float* 
                        uint64_t rows, uint64_t cols, cudaStream_t s) {
   if (rows == 0 || cols == 0) return cudaSuccess;
   split_tf32_kernel<<<grid_for(rows * cols), 256, 0, s>>>(src, sp, sld, hi, lo, dld, rows, cols);
+  count_launch();
   return cudaGetLastError();
 }
 
@@ -221,6 +231,7 @@ cudaError_t split_tf32_t(const void* src, int sp, uint64_t sld, float* hi, float
   if (rows == 0 || cols == 0) return cudaSuccess;
   dim3 grid(static_cast<unsigned>((cols + 31) / 32), static_cast<unsigned>((rows + 31) / 32));
   split_tf32_t_kernel<<<grid, dim3(32, 8), 0, s>>>(src, sp, sld, hi, lo, dld, rows, cols, split ? 1 : 0);
+  count_launch();
   return cudaGetLastError();
 }
 
@@ -230,6 +241,7 @@ cudaError_t fill_uniform(void* dst, int prec, uint64_t ld, uint64_t r0, uint64_t
   if (rows == 0 || cols == 0) return cudaSuccess;
   fill_uniform_kernel<<<grid_for(rows * cols), 256, 0, s>>>(dst, prec, ld, r0, rows, c0, cols,
                                                             full_cols, seed, lo, hi);
+  count_launch();
   return cudaGetLastError();
 }
 
@@ -237,6 +249,7 @@ cudaError_t scale_rect(void* c, int prec, uint64_t ld, uint64_t rows, uint64_t c
                        cudaStream_t s) {
   if (rows == 0 || cols == 0) return cudaSuccess;
   scale_rect_kernel<<<grid_for(rows * cols), 256, 0, s>>>(c, prec, ld, rows, cols, beta);
+  count_launch();
   return cudaGetLastError();
 }
 

@@ -17,4 +17,7 @@ cudaError_t fill_uniform(void* dst, int prec, uint64_t ld, uint64_t r0, uint64_t
                          cudaStream_t s);
 cudaError_t scale_rect(void* c, int prec, uint64_t ld, uint64_t rows, uint64_t cols, double beta,
                        cudaStream_t s);
+// Process-wide count of kernels this library launched.
+uint64_t kernel_launches();
+void count_launch();
 }  // namespace gmk

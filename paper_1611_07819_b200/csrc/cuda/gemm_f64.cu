@@ -17,6 +17,7 @@
 
 #include <cstdint>
 
+#include "convert.h"
 #include "gemm_f64.h"
 
 namespace gmk {
@@ -217,6 +218,7 @@ int f64_gemm(const F64GemmArgs& g, cudaStream_t stream, const char** err) {
   auto pick = [&](auto kern) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     kern<<<grid, kThreads, smem, stream>>>(p);
+    count_launch();
   };
   if (!g.trans_a && !g.trans_b) pick(f64_gemm_kernel<false, false>);
   else if (!g.trans_a && g.trans_b) pick(f64_gemm_kernel<false, true>);

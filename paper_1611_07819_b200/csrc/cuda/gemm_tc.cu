@@ -34,6 +34,7 @@
 #include <cstdlib>
 #include <mutex>
 
+#include "convert.h"
 #include "gemm_tc.h"
 #include "ptx.cuh"
 
@@ -459,6 +460,7 @@ int launch(const TcOperand& a, const TcOperand& b, const TcOperand* a_lo, const 
                  kCG, kElemBytes, kSplit, p.m, p.n, p.k, ctas, dev < 64 ? resident[dev] : -1,
                  Cfg::kStages, Cfg::kSmemBytes);
   cudaError_t e = cudaLaunchKernelEx(&cfg, kern, ma, mb, mal, mbl, p);
+  count_launch();
   if (e != cudaSuccess) {
     *err = cudaGetErrorString(e);
     return 1;

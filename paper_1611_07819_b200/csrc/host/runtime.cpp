@@ -189,6 +189,9 @@ Worker::Worker(std::uint32_t r, int dev, std::uint64_t budget)
   cudaCheck(cudaStreamCreateWithPriority(&comm, cudaStreamNonBlocking, hi), "worker: comm stream");
   cudaCheck(cudaEventCreate(&tStart), "worker: event");
   cudaCheck(cudaEventCreate(&tEnd), "worker: event");
+  cudaCheck(cudaEventCreate(&uStart), "worker: event");
+  cudaCheck(cudaEventCreate(&uEnd), "worker: event");
+  cudaCheck(cudaEventCreate(&kStart), "worker: event");
 }
 
 Worker::~Worker() {
@@ -204,6 +207,9 @@ Worker::~Worker() {
   for (cudaEvent_t e : pool_) cudaEventDestroy(e);
   cudaEventDestroy(tStart);
   cudaEventDestroy(tEnd);
+  cudaEventDestroy(uStart);
+  cudaEventDestroy(uEnd);
+  cudaEventDestroy(kStart);
   cudaStreamDestroy(compute);
   cudaStreamDestroy(comm);
 }
@@ -986,6 +992,7 @@ void Session::execGemm(const OpDescriptor& op) {
   const bool alphaZero = op.s0 == 0.0;
   const std::uint64_t ebA = bytesOf(A.precision), ebB = bytesOf(B.precision);
   forEachLocal([&](Worker& w) {
+    cudaCheck(cudaEventRecord(w.kStart, w.compute), "gemm: timing");
     for (DeviceTile& ct : w.tiles.at(C.matrixId)) {
       const TileExtent& e = ct.extent;
       gm_gemm_desc d{};
@@ -1046,6 +1053,100 @@ std::vector<float> Session::lastOpDeviceMs() {
     out.push_back(ms);
   });
   return out;
+}
+
+std::vector<float> Session::lastOpKernelMs() {
+  std::vector<float> out;
+  forEachLocal([&](Worker& w) {
+    float ms = 0.0f;
+    if (w.timed) {
+      cudaCheck(cudaEventSynchronize(w.tEnd), "timing sync");
+      cudaCheck(cudaEventElapsedTime(&ms, w.kStart, w.tEnd), "timing");
+    }
+    out.push_back(ms);
+  });
+  return out;
+}
+
+std::uint64_t Session::localBytes(DistMatrix m) const {
+  const MatrixDescriptor& d = descriptor(m.id());
+  std::uint64_t b = 0;
+  for (const auto& t : d.layout.tiles)
+    if (isLocal(t.second.rank)) b += t.first.elements() * bytesOf(d.precision);
+  return b;
+}
+
+void Session::setLocalPacked(DistMatrix m, const void* host, std::uint64_t bytes) {
+  const MatrixDescriptor d = descriptor(m.id());
+  if (bytes != localBytes(m)) throw Error("setLocalPacked: byte count mismatch");
+  OpDescriptor op;
+  op.opcode = OpCode::SetData;
+  op.ids[0] = m.id();
+  issue(op);
+  const std::uint64_t eb = bytesOf(d.precision);
+  const auto* src = static_cast<const std::uint8_t*>(host);
+  for (const auto& t : d.layout.tiles) {
+    Worker* w = local(t.second.rank);
+    if (!w) continue;
+    w->activate();
+    for (DeviceTile& dt : w->tiles.at(d.matrixId))
+      if (dt.extent == t.first)
+        cudaCheck(cudaMemcpy2DAsync(dt.ptr, dt.ld * eb, src, t.first.colCount * eb, t.first.colCount * eb,
+                                    t.first.rowCount, cudaMemcpyDefault, w->compute),
+                  "setLocalPacked");
+    src += t.first.elements() * eb;
+  }
+  forEachLocal([&](Worker& w) { cudaCheck(cudaStreamSynchronize(w.compute), "setLocalPacked: sync"); });
+}
+
+void Session::getLocalPacked(DistMatrix m, void* host, std::uint64_t bytes) {
+  const MatrixDescriptor d = descriptor(m.id());
+  if (bytes != localBytes(m)) throw Error("getLocalPacked: byte count mismatch");
+  OpDescriptor op;
+  op.opcode = OpCode::GetData;
+  op.ids[0] = m.id();
+  issue(op);
+  const std::uint64_t eb = bytesOf(d.precision);
+  auto* dst = static_cast<std::uint8_t*>(host);
+  for (const auto& t : d.layout.tiles) {
+    Worker* w = local(t.second.rank);
+    if (!w) continue;
+    w->activate();
+    for (DeviceTile& dt : w->tiles.at(d.matrixId))
+      if (dt.extent == t.first)
+        cudaCheck(cudaMemcpy2DAsync(dst, t.first.colCount * eb, dt.ptr, dt.ld * eb, t.first.colCount * eb,
+                                    t.first.rowCount, cudaMemcpyDefault, w->compute),
+                  "getLocalPacked");
+    dst += t.first.elements() * eb;
+  }
+  forEachLocal([&](Worker& w) { cudaCheck(cudaStreamSynchronize(w.compute), "getLocalPacked: sync"); });
+}
+
+void Session::timerStart() {
+  forEachLocal([&](Worker& w) {
+    // The comm stream's prior work is part of "before": fold it in.
+    cudaEvent_t e = w.event();
+    cudaCheck(cudaEventRecord(e, w.comm), "timer");
+    cudaCheck(cudaStreamWaitEvent(w.compute, e, 0), "timer");
+    w.recycle(e);
+    cudaCheck(cudaEventRecord(w.uStart, w.compute), "timer start");
+  });
+}
+
+float Session::timerStop() {
+  float best = 0.0f;
+  forEachLocal([&](Worker& w) {
+    cudaEvent_t e = w.event();
+    cudaCheck(cudaEventRecord(e, w.comm), "timer");
+    cudaCheck(cudaStreamWaitEvent(w.compute, e, 0), "timer");
+    w.recycle(e);
+    cudaCheck(cudaEventRecord(w.uEnd, w.compute), "timer stop");
+    cudaCheck(cudaEventSynchronize(w.uEnd), "timer sync");
+    float ms = 0.0f;
+    cudaCheck(cudaEventElapsedTime(&ms, w.uStart, w.uEnd), "timer elapsed");
+    best = std::max(best, ms);
+  });
+  return best;
 }
 
 // ---------------------------------------------------------------- replication

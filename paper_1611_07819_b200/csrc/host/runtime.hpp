@@ -168,7 +168,8 @@ class Worker {
   PanelCache cache;
   std::uint64_t cacheBudget;
   std::uint64_t residentBytes = 0, bytesSent = 0, bytesReceived = 0;
-  cudaEvent_t tStart = nullptr, tEnd = nullptr;
+  cudaEvent_t tStart = nullptr, tEnd = nullptr, uStart = nullptr, uEnd = nullptr;
+  cudaEvent_t kStart = nullptr;  // compute phase of the last gemm (ends at tEnd)
   bool timed = false;
   ncclComm_t nccl = nullptr;
 
@@ -255,6 +256,12 @@ class Session {
   void runGemm(const OpDescriptor& op, bool sync);
   void synchronize();
   std::vector<float> lastOpDeviceMs();
+  std::vector<float> lastOpKernelMs();
+  std::uint64_t localBytes(DistMatrix m) const;
+  void setLocalPacked(DistMatrix m, const void* host, std::uint64_t bytes);
+  void getLocalPacked(DistMatrix m, void* host, std::uint64_t bytes);
+  void timerStart();
+  float timerStop();
 
  private:
   std::uint64_t issue(OpDescriptor& op);  // validate + metadata + per-worker mirror

@@ -30,7 +30,7 @@ from ._lib import GmError, check
 __all__ = ["Precision", "TileExtent", "Layout", "makeWorkerGroup", "makeRowBlockLayout",
            "makeColBlockLayout", "makeGridLayout", "makeSingleTileLayout", "validateLayout",
            "Session", "DistMatrix", "ReplicationHandle", "ReplState", "gemm", "GmError",
-           "nccl_unique_id", "np_storage_dtype"]
+           "nccl_unique_id", "np_storage_dtype", "kernel_launches"]
 
 
 class Precision(enum.IntEnum):
@@ -293,9 +293,40 @@ class Session:
         check(_lib.load().gm_last_op_device_ms(self._h, arr, 64, ctypes.byref(n)))
         return list(arr[: n.value])
 
+    def lastOpKernelMs(self) -> List[float]:
+        arr = (ctypes.c_float * 64)()
+        n = ctypes.c_uint32()
+        check(_lib.load().gm_last_op_kernel_ms(self._h, arr, 64, ctypes.byref(n)))
+        return list(arr[: n.value])
+
+    def localBytes(self, m: DistMatrix) -> int:
+        b = ctypes.c_uint64()
+        check(_lib.load().gm_matrix_local_bytes(self._h, m.id, ctypes.byref(b)))
+        return b.value
+
+    def setLocalPacked(self, m: DistMatrix, ptr: int, nbytes: int):
+        check(_lib.load().gm_matrix_set_local_packed(self._h, m.id, ptr, nbytes))
+
+    def getLocalPacked(self, m: DistMatrix, ptr: int, nbytes: int):
+        check(_lib.load().gm_matrix_get_local_packed(self._h, m.id, ptr, nbytes))
+
+    def timerStart(self):
+        check(_lib.load().gm_timer_start(self._h))
+
+    def timerStop(self) -> float:
+        ms = ctypes.c_float()
+        check(_lib.load().gm_timer_stop(self._h, ctypes.byref(ms)))
+        return ms.value
+
     def gemmAsync(self, a: DistMatrix, b: DistMatrix, c: DistMatrix, alpha=1.0, beta=0.0,
                   transA=False, transB=False):
         check(_lib.load().gm_gemm_async(self._h, a.id, b.id, c.id, alpha, beta, int(transA), int(transB)))
+
+
+def kernel_launches() -> int:
+    n = ctypes.c_uint64()
+    check(_lib.load().gm_kernel_launches(ctypes.byref(n)))
+    return n.value
 
 
 def gemm(s: Session, a: DistMatrix, b: DistMatrix, c: DistMatrix, alpha: float, beta: float,
