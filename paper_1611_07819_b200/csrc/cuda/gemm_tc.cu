@@ -41,23 +41,31 @@
 namespace gmk {
 
 constexpr uint32_t kBlockMcta = 128;  // accumulator rows per CTA (TMEM lanes)
-constexpr uint32_t kBlockN = 256;     // MMA N (TMEM columns per accumulator)
+constexpr uint32_t kMmaN = 256;       // N of one tcgen05.mma (TMEM columns per chunk)
 constexpr uint32_t kSwizzleBytes = 128;
 constexpr uint32_t kNumThreads = 192;  // 6 warps
 
 // Operand element = 2 bytes (kind::f16) or 4 bytes (kind::tf32). A k-block
 // is one 128-byte swizzle row: 64 x 16-bit or 32 x 32-bit elements.
-template <int kCG, int kElemBytes, int kSplit>
+// kChunks = UMMAs (N = 256 each) per k-step: the CTA(-pair) tile is
+// (128 * kCG) x (256 * kChunks). kChunks = 2 fills all 512 TMEM columns with
+// one accumulator (no accumulator double-buffering); kChunks = 1 keeps two
+// accumulators so the epilogue of tile t overlaps the MMAs of tile t+1.
+template <int kCG, int kElemBytes, int kSplit, int kChunks>
 struct TcCfg {
   static constexpr uint32_t kBlockK = kSwizzleBytes / kElemBytes;
   static constexpr uint32_t kMmaK = 32 / kElemBytes;  // 16 (f16) or 8 (tf32)
-  static constexpr uint32_t kBlockNcta = kBlockN / kCG;
+  static constexpr uint32_t kBlockN = kMmaN * kChunks;  // tile N of the CTA pair
+  static constexpr uint32_t kChunkNcta = kMmaN / kCG;   // B columns per CTA per chunk
+  static constexpr uint32_t kAccStages = 2 / kChunks;
   static constexpr uint32_t kBytesA = kBlockMcta * kSwizzleBytes;  // per operand part
-  static constexpr uint32_t kBytesB = kBlockNcta * kSwizzleBytes;
+  static constexpr uint32_t kBytesBChunk = kChunkNcta * kSwizzleBytes;
+  static constexpr uint32_t kBytesB = kBytesBChunk * kChunks;
   static constexpr uint32_t kParts = kSplit ? 2 : 1;               // hi (+ lo)
   static constexpr uint32_t kStageBytes = kParts * (kBytesA + kBytesB);
   static constexpr uint32_t kStages = (196u * 1024u) / kStageBytes;
   static constexpr uint32_t kSmemBytes = kStages * kStageBytes + 1024 + 256;
+  static_assert(kAccStages * kChunks * kMmaN <= 512, "TMEM columns");
 };
 
 struct TcParams {
@@ -69,17 +77,19 @@ struct TcParams {
   uint64_t ldc;
   uint32_t c_dtype;  // 0 f16, 1 bf16, 2 f32
   uint32_t c_vec;    // 16B vector stores legal
-  uint32_t num_m_blocks, num_n_blocks;  // in units of (kBlockMcta*kCG) x kBlockN
+  uint32_t num_m_blocks, num_n_blocks;  // in units of the CTA(-pair) tile
+  uint32_t group;                       // raster group (M-blocks)
 };
 
 __device__ __forceinline__ void tile_coords(uint32_t t, const TcParams& p, uint32_t& mb,
                                             uint32_t& nb) {
-  // Group 16 M-blocks together so consecutive tiles share B panels in L2.
-  constexpr uint32_t kGroup = 16;
-  const uint32_t per_group = kGroup * p.num_n_blocks;
+  // Rasterize in groups of `group` M-blocks (m-fastest inside a group) so the
+  // tiles that run concurrently share A and B k-slabs in L2.
+  const uint32_t group = p.group;
+  const uint32_t per_group = group * p.num_n_blocks;
   const uint32_t g = t / per_group;
-  const uint32_t first_m = g * kGroup;
-  const uint32_t gsize = min(kGroup, p.num_m_blocks - first_m);
+  const uint32_t first_m = g * group;
+  const uint32_t gsize = min(group, p.num_m_blocks - first_m);
   const uint32_t r = t % per_group;
   mb = first_m + r % gsize;
   nb = r / gsize;
@@ -142,23 +152,25 @@ __device__ __forceinline__ void store_row32(const TcParams& p, uint32_t row, uin
 }
 
 // kSplit: 3xTF32 (maps a_hi/a_lo, b_hi/b_lo). Otherwise a single pair.
-template <int kCG, int kElemBytes, int kSplit>
+template <int kCG, int kElemBytes, int kSplit, int kChunks>
 __global__ void __launch_bounds__(kNumThreads, 1)
     tc_gemm_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid_constant__ CUtensorMap tm_b,
                    const __grid_constant__ CUtensorMap tm_a_lo,
                    const __grid_constant__ CUtensorMap tm_b_lo, const TcParams p) {
-  using Cfg = TcCfg<kCG, kElemBytes, kSplit>;
+  using Cfg = TcCfg<kCG, kElemBytes, kSplit, kChunks>;
   constexpr uint32_t kStages = Cfg::kStages;
   constexpr uint32_t kBlockK = Cfg::kBlockK;
   constexpr uint32_t kMmaK = Cfg::kMmaK;
-  constexpr uint32_t kBlockNcta = Cfg::kBlockNcta;
+  constexpr uint32_t kChunkNcta = Cfg::kChunkNcta;
+  constexpr uint32_t kAcc = Cfg::kAccStages;
+  constexpr uint32_t kElems128 = kSwizzleBytes / kElemBytes;  // elements per 128B row
 
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + kStages * Cfg::kStageBytes);
   uint64_t* empty_bar = full_bar + kStages;
-  uint64_t* tfull_bar = empty_bar + kStages;  // [2]
-  uint64_t* tempty_bar = tfull_bar + 2;       // [2]
+  uint64_t* tfull_bar = empty_bar + kStages;  // [kAcc]
+  uint64_t* tempty_bar = tfull_bar + 2;       // [kAcc]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty_bar + 2);
 
   const uint32_t warp = warp_id_sync();
@@ -177,7 +189,7 @@ __global__ void __launch_bounds__(kNumThreads, 1)
       mbar_init(&full_bar[s], 1);
       mbar_init(&empty_bar[s], 1);
     }
-    for (int a = 0; a < 2; ++a) {
+    for (uint32_t a = 0; a < kAcc; ++a) {
       mbar_init(&tfull_bar[a], 1);
       mbar_init(&tempty_bar[a], 4 * kCG);
     }
@@ -204,7 +216,6 @@ __global__ void __launch_bounds__(kNumThreads, 1)
         uint32_t mb, nb;
         tile_coords(t, p, mb, nb);
         const int32_t m0 = static_cast<int32_t>(mb * kBlockMcta * kCG + rank * kBlockMcta);
-        const int32_t n0 = static_cast<int32_t>(nb * kBlockN + rank * kBlockNcta);
         for (uint32_t kb = 0; kb < num_kb; ++kb) {
           mbar_wait(&empty_bar[stage], phase ^ 1);
           uint8_t* sa = smem + stage * Cfg::kStageBytes;
@@ -222,28 +233,33 @@ __global__ void __launch_bounds__(kNumThreads, 1)
               if (kCG == 2) tma_load_2d_2sm(da, ma, &full_bar[stage], k0, m0);
               else tma_load_2d(da, ma, &full_bar[stage], k0, m0);
             } else {
-              // MN-major: boxes of (64 B-elements of M) x kBlockK rows of K.
-              constexpr uint32_t kChunk = kSwizzleBytes / kElemBytes;
+              // MN-major: boxes of (128 B of M) x kBlockK rows of K.
 #pragma unroll
-              for (uint32_t j = 0; j < kBlockMcta / kChunk; ++j) {
+              for (uint32_t j = 0; j < kBlockMcta / kElems128; ++j) {
                 if (kCG == 2)
-                  tma_load_2d_2sm(da + j * kBlockK * kSwizzleBytes, ma, &full_bar[stage], m0 + j * kChunk, k0);
+                  tma_load_2d_2sm(da + j * kBlockK * kSwizzleBytes, ma, &full_bar[stage], m0 + j * kElems128, k0);
                 else
-                  tma_load_2d(da + j * kBlockK * kSwizzleBytes, ma, &full_bar[stage], m0 + j * kChunk, k0);
+                  tma_load_2d(da + j * kBlockK * kSwizzleBytes, ma, &full_bar[stage], m0 + j * kElems128, k0);
               }
             }
-            if (p.b_mn_major) {
-              constexpr uint32_t kChunk = kSwizzleBytes / kElemBytes;
+            // B: chunk c of this CTA covers global columns
+            // nb*kBlockN + c*256 + rank*kChunkNcta + [0, kChunkNcta).
 #pragma unroll
-              for (uint32_t j = 0; j < kBlockNcta / kChunk; ++j) {
-                if (kCG == 2)
-                  tma_load_2d_2sm(db + j * kBlockK * kSwizzleBytes, mbm, &full_bar[stage], n0 + j * kChunk, k0);
-                else
-                  tma_load_2d(db + j * kBlockK * kSwizzleBytes, mbm, &full_bar[stage], n0 + j * kChunk, k0);
+            for (uint32_t c = 0; c < kChunks; ++c) {
+              const int32_t n0 = static_cast<int32_t>(nb * Cfg::kBlockN + c * kMmaN + rank * kChunkNcta);
+              uint8_t* dc = db + c * Cfg::kBytesBChunk;
+              if (p.b_mn_major) {
+#pragma unroll
+                for (uint32_t j = 0; j < kChunkNcta / kElems128; ++j) {
+                  if (kCG == 2)
+                    tma_load_2d_2sm(dc + j * kBlockK * kSwizzleBytes, mbm, &full_bar[stage], n0 + j * kElems128, k0);
+                  else
+                    tma_load_2d(dc + j * kBlockK * kSwizzleBytes, mbm, &full_bar[stage], n0 + j * kElems128, k0);
+                }
+              } else {
+                if (kCG == 2) tma_load_2d_2sm(dc, mbm, &full_bar[stage], k0, n0);
+                else tma_load_2d(dc, mbm, &full_bar[stage], k0, n0);
               }
-            } else {
-              if (kCG == 2) tma_load_2d_2sm(db, mbm, &full_bar[stage], k0, n0);
-              else tma_load_2d(db, mbm, &full_bar[stage], k0, n0);
             }
           }
           if (++stage == kStages) {
@@ -266,7 +282,7 @@ __global__ void __launch_bounds__(kNumThreads, 1)
       for (uint32_t t = unit; t < num_tiles; t += num_units) {
         mbar_wait(&tempty_bar[acc], acc_phase ^ 1);
         tc_fence_after();
-        const uint32_t tmem_d = tmem_base + acc * kBlockN;
+        const uint32_t tmem_acc = tmem_base + acc * kChunks * kMmaN;
         for (uint32_t kb = 0; kb < num_kb; ++kb) {
           mbar_wait(&full_bar[stage], phase);
           tc_fence_after();
@@ -276,17 +292,22 @@ __global__ void __launch_bounds__(kNumThreads, 1)
           for (uint32_t kk = 0; kk < kBlockK / kMmaK; ++kk) {
             const uint32_t first = (kb | kk) == 0 ? 0u : 1u;
             const uint64_t ah = sdesc_sw128(sa + kk * a_step, a_lbo, 1024);
-            const uint64_t bh = sdesc_sw128(sb + kk * b_step, b_lbo, 1024);
-            if constexpr (kSplit) {
-              const uint64_t al = sdesc_sw128(sa + Cfg::kBytesA + kk * a_step, a_lbo, 1024);
-              const uint64_t bl = sdesc_sw128(sb + Cfg::kBytesB + kk * b_step, b_lbo, 1024);
-              mma_tf32<kCG>(tmem_d, al, bh, p.idesc, first);
-              mma_tf32<kCG>(tmem_d, ah, bl, p.idesc, 1u);
-              mma_tf32<kCG>(tmem_d, ah, bh, p.idesc, 1u);
-            } else if constexpr (kElemBytes == 4) {
-              mma_tf32<kCG>(tmem_d, ah, bh, p.idesc, first);
-            } else {
-              mma_f16<kCG>(tmem_d, ah, bh, p.idesc, first);
+#pragma unroll
+            for (uint32_t c = 0; c < kChunks; ++c) {
+              const uint32_t tmem_d = tmem_acc + c * kMmaN;
+              const uint32_t bc = sb + c * Cfg::kBytesBChunk;
+              const uint64_t bh = sdesc_sw128(bc + kk * b_step, b_lbo, 1024);
+              if constexpr (kSplit) {
+                const uint64_t al = sdesc_sw128(sa + Cfg::kBytesA + kk * a_step, a_lbo, 1024);
+                const uint64_t bl = sdesc_sw128(bc + Cfg::kBytesB + kk * b_step, b_lbo, 1024);
+                mma_tf32<kCG>(tmem_d, al, bh, p.idesc, first);
+                mma_tf32<kCG>(tmem_d, ah, bl, p.idesc, 1u);
+                mma_tf32<kCG>(tmem_d, ah, bh, p.idesc, 1u);
+              } else if constexpr (kElemBytes == 4) {
+                mma_tf32<kCG>(tmem_d, ah, bh, p.idesc, first);
+              } else {
+                mma_f16<kCG>(tmem_d, ah, bh, p.idesc, first);
+              }
             }
           }
           if constexpr (kCG == 2) mma_commit_2sm(&empty_bar[stage], 0x3);
@@ -300,8 +321,10 @@ __global__ void __launch_bounds__(kNumThreads, 1)
             phase ^= 1;
           }
         }
-        acc ^= 1;
-        if (acc == 0) acc_phase ^= 1;
+        if (++acc == kAcc) {
+          acc = 0;
+          acc_phase ^= 1;
+        }
       }
     }
   } else {
@@ -314,14 +337,14 @@ __global__ void __launch_bounds__(kNumThreads, 1)
       mbar_wait(&tfull_bar[acc], acc_phase);
       tc_fence_after();
       const uint32_t row = mb * kBlockMcta * kCG + rank * kBlockMcta + lane_grp * 32 + lane;
-      const uint32_t taddr = tmem_base + ((lane_grp * 32) << 16) + acc * kBlockN;
+      const uint32_t taddr = tmem_base + ((lane_grp * 32) << 16) + acc * kChunks * kMmaN;
 #pragma unroll 1
-      for (uint32_t c = 0; c < kBlockN; c += 32) {
+      for (uint32_t c = 0; c < Cfg::kBlockN; c += 32) {
         uint32_t v[32];
         __syncwarp();
         tmem_ld_32x32b_x32(taddr + c, v);
         tmem_wait_ld();
-        store_row32(p, row, nb * kBlockN + c, v);
+        store_row32(p, row, nb * Cfg::kBlockN + c, v);
       }
       tc_fence_before();
       __syncwarp();
@@ -329,8 +352,10 @@ __global__ void __launch_bounds__(kNumThreads, 1)
         if (kCG == 2 && !leader) mbar_arrive_cluster(&tempty_bar[acc], 0);
         else mbar_arrive(&tempty_bar[acc]);
       }
-      acc ^= 1;
-      if (acc == 0) acc_phase ^= 1;
+      if (++acc == kAcc) {
+        acc = 0;
+        acc_phase ^= 1;
+      }
     }
   }
 
@@ -376,9 +401,17 @@ int make_map_2d(CUtensorMap* map, const void* ptr, CUtensorMapDataType dt, uint3
   cuuint64_t strides[1] = {pitch_elems * esize};
   cuuint32_t box[2] = {box_inner, box_outer};
   cuuint32_t estr[2] = {1, 1};
+  static const int promo = [] {
+    const char* e = std::getenv("GM_L2_PROMO");
+    return e ? std::atoi(e) : 128;
+  }();
+  const CUtensorMapL2promotion pr = promo == 0 ? CU_TENSOR_MAP_L2_PROMOTION_NONE
+                                    : promo == 64 ? CU_TENSOR_MAP_L2_PROMOTION_L2_64B
+                                    : promo == 128 ? CU_TENSOR_MAP_L2_PROMOTION_L2_128B
+                                                   : CU_TENSOR_MAP_L2_PROMOTION_L2_256B;
   CUresult r = fn(map, dt, 2, const_cast<void*>(ptr), dims, strides, box, estr,
-                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, pr,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) {
     *err = "cuTensorMapEncodeTiled failed (alignment or stride)";
     return 1;
@@ -393,10 +426,10 @@ int sm_count(int dev) {
   return counts[dev];
 }
 
-template <int kCG, int kElemBytes, int kSplit>
+template <int kCG, int kElemBytes, int kSplit, int kChunks>
 int launch(const TcOperand& a, const TcOperand& b, const TcOperand* a_lo, const TcOperand* b_lo,
            const TcParams& p0, int max_ctas, cudaStream_t stream, const char** err) {
-  using Cfg = TcCfg<kCG, kElemBytes, kSplit>;
+  using Cfg = TcCfg<kCG, kElemBytes, kSplit, kChunks>;
   const CUtensorMapDataType dt = kElemBytes == 4 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32
                                                  : CU_TENSOR_MAP_DATA_TYPE_UINT16;
   constexpr uint32_t kChunk = kSwizzleBytes / kElemBytes;
@@ -410,7 +443,7 @@ int launch(const TcOperand& a, const TcOperand& b, const TcOperand* a_lo, const 
   auto map_b = [&](CUtensorMap* m, const TcOperand& op) {
     // B logical K x N. MN-major: stored K rows x N cols; K-major: N rows x K cols.
     if (p.b_mn_major) return make_map_2d(m, op.ptr, dt, kElemBytes, p.n, p.k, op.ld, kChunk, Cfg::kBlockK, err);
-    return make_map_2d(m, op.ptr, dt, kElemBytes, p.k, p.n, op.ld, Cfg::kBlockK, Cfg::kBlockNcta, err);
+    return make_map_2d(m, op.ptr, dt, kElemBytes, p.k, p.n, op.ld, Cfg::kBlockK, Cfg::kChunkNcta, err);
   };
   if (map_a(&ma, a) || map_b(&mb, b)) return 1;
   if (kSplit) {
@@ -420,11 +453,19 @@ int launch(const TcOperand& a, const TcOperand& b, const TcOperand* a_lo, const 
     mbl = mb;
   }
   p.num_m_blocks = (p.m + kBlockMcta * kCG - 1) / (kBlockMcta * kCG);
-  p.num_n_blocks = (p.n + kBlockN - 1) / kBlockN;
+  {
+    static const uint32_t env_group = [] {
+      const char* e = std::getenv("GM_RASTER_GROUP");
+      return e ? static_cast<uint32_t>(std::atoi(e)) : 0u;
+    }();
+    p.group = env_group ? env_group : 32;
+    if (p.group > p.num_m_blocks) p.group = p.num_m_blocks;
+  }
+  p.num_n_blocks = (p.n + Cfg::kBlockN - 1) / Cfg::kBlockN;
   const uint32_t tiles = p.num_m_blocks * p.num_n_blocks;
   int dev = 0;
   cudaGetDevice(&dev);
-  auto kern = tc_gemm_kernel<kCG, kElemBytes, kSplit>;
+  auto kern = tc_gemm_kernel<kCG, kElemBytes, kSplit, kChunks>;
   // Persistent grid = the number of CTAs (CTA pairs) that are co-resident.
   static int resident[64] = {0};
   cudaLaunchConfig_t cfg{};
@@ -456,8 +497,8 @@ int launch(const TcOperand& a, const TcOperand& b, const TcOperand* a_lo, const 
   cfg.gridDim = dim3(ctas, 1, 1);
   static const bool debug = std::getenv("GM_DEBUG") != nullptr;
   if (debug)
-    std::fprintf(stderr, "[gm] tc_gemm cg=%d elem=%d split=%d m=%u n=%u k=%u grid=%d resident=%d stages=%u smem=%u\n",
-                 kCG, kElemBytes, kSplit, p.m, p.n, p.k, ctas, dev < 64 ? resident[dev] : -1,
+    std::fprintf(stderr, "[gm] tc_gemm cg=%d elem=%d split=%d chunks=%d m=%u n=%u k=%u grid=%d resident=%d stages=%u smem=%u\n",
+                 kCG, kElemBytes, kSplit, kChunks, p.m, p.n, p.k, ctas, dev < 64 ? resident[dev] : -1,
                  Cfg::kStages, Cfg::kSmemBytes);
   cudaError_t e = cudaLaunchKernelEx(&cfg, kern, ma, mb, mal, mbl, p);
   count_launch();
@@ -486,18 +527,30 @@ int tc_gemm(const TcGemmArgs& g, cudaStream_t stream, const char** err) {
   p.c_vec = ((reinterpret_cast<uintptr_t>(g.c) % 16) == 0 && (g.ldc * cb) % 16 == 0) ? 1 : 0;
   const int cg = g.cta_group == 1 ? 1 : 2;
   const uint32_t mrows = kBlockMcta * cg;
+  // Wide tiles (256 x 512 per CTA pair, two UMMAs per k-step) halve the
+  // distinct A panels in flight and cut L2->SMEM traffic by a quarter; their
+  // single accumulator leaves the epilogue unoverlapped, which only pays off
+  // when the k loop is long. GM_TC_CHUNKS=1|2 overrides.
+  static const int env_chunks = [] {
+    const char* e = std::getenv("GM_TC_CHUNKS");
+    return e ? std::atoi(e) : 0;
+  }();
   if (g.kind == TcKind::F16 || g.kind == TcKind::BF16) {
     const uint32_t fmt = g.kind == TcKind::BF16 ? 1 : 0;
-    p.idesc = make_idesc(fmt, fmt, p.a_mn_major, p.b_mn_major, mrows, kBlockN);
-    return cg == 1 ? launch<1, 2, 0>(g.a, g.b, nullptr, nullptr, p, g.max_ctas, stream, err)
-                   : launch<2, 2, 0>(g.a, g.b, nullptr, nullptr, p, g.max_ctas, stream, err);
+    p.idesc = make_idesc(fmt, fmt, p.a_mn_major, p.b_mn_major, mrows, kMmaN);
+    const bool wide = env_chunks ? env_chunks == 2 : (g.k >= 4096 && g.n > kMmaN);
+    if (cg == 1)
+      return wide ? launch<1, 2, 0, 2>(g.a, g.b, nullptr, nullptr, p, g.max_ctas, stream, err)
+                  : launch<1, 2, 0, 1>(g.a, g.b, nullptr, nullptr, p, g.max_ctas, stream, err);
+    return wide ? launch<2, 2, 0, 2>(g.a, g.b, nullptr, nullptr, p, g.max_ctas, stream, err)
+                : launch<2, 2, 0, 1>(g.a, g.b, nullptr, nullptr, p, g.max_ctas, stream, err);
   }
-  p.idesc = make_idesc(2, 2, p.a_mn_major, p.b_mn_major, mrows, kBlockN);
+  p.idesc = make_idesc(2, 2, p.a_mn_major, p.b_mn_major, mrows, kMmaN);
   if (g.kind == TcKind::TF32)
-    return cg == 1 ? launch<1, 4, 0>(g.a, g.b, nullptr, nullptr, p, g.max_ctas, stream, err)
-                   : launch<2, 4, 0>(g.a, g.b, nullptr, nullptr, p, g.max_ctas, stream, err);
-  return cg == 1 ? launch<1, 4, 1>(g.a, g.b, &g.a_lo, &g.b_lo, p, g.max_ctas, stream, err)
-                 : launch<2, 4, 1>(g.a, g.b, &g.a_lo, &g.b_lo, p, g.max_ctas, stream, err);
+    return cg == 1 ? launch<1, 4, 0, 1>(g.a, g.b, nullptr, nullptr, p, g.max_ctas, stream, err)
+                   : launch<2, 4, 0, 1>(g.a, g.b, nullptr, nullptr, p, g.max_ctas, stream, err);
+  return cg == 1 ? launch<1, 4, 1, 1>(g.a, g.b, &g.a_lo, &g.b_lo, p, g.max_ctas, stream, err)
+                 : launch<2, 4, 1, 1>(g.a, g.b, &g.a_lo, &g.b_lo, p, g.max_ctas, stream, err);
 }
 
 }  // namespace gmk
