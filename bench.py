@@ -218,8 +218,11 @@ def run_ours(args):
         obj = [G.nccl_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(obj, src=0)
         nccl_id = obj[0]
+    # Panel cache off: A and B do not change between steps, so with the cache
+    # on every step after the first would skip the panel exchange. Each
+    # timed step must move its panels.
     s = G.Session(workers=world, spmd_rank=rank if world > 1 else -1, devices=[local], nccl_id=nccl_id,
-                  gemm_max_ctas=args.gemm_max_ctas)
+                  gemm_max_ctas=args.gemm_max_ctas, panel_cache_bytes=1, pipeline_chunks=args.pipeline_chunks)
     n = args.n
     pr, pc = grid_for(world)
     lay = G.makeGridLayout(n, n, pr, pc, G.makeWorkerGroup(world))
@@ -364,6 +367,7 @@ def main():
     ap.add_argument("--n", type=int, default=32768)
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--gemm-max-ctas", type=int, default=0)
+    ap.add_argument("--pipeline-chunks", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", dest="cpu_baseline", action="store_false")
     ap.add_argument("--no-c2", dest="c2", action="store_false")
     args = ap.parse_args()

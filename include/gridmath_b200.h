@@ -194,6 +194,8 @@ typedef struct {
   uint64_t arena_slab_bytes;        /* 0 = default */
   int32_t gemm_max_ctas;            /* 0 = all SMs (cap leaves SMs for NCCL) */
   int32_t transport;                /* 0 = auto, 1 = NCCL, 2 = copy-engine peer pulls */
+  uint64_t panel_cache_bytes;       /* per-worker panel cache budget; 0 = 1/4 of HBM, 1 = off */
+  int32_t pipeline_chunks;          /* SUMMA overlap chunks per band (0 = auto, 1 = off) */
 } gm_session_options;
 
 void gm_session_options_default(gm_session_options* o);

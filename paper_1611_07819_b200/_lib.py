@@ -48,7 +48,8 @@ class gm_session_options(Structure):
                 ("check_metadata_every_op", c_int32), ("spmd_rank", c_int32),
                 ("num_devices", c_int32), ("devices", c_int32 * 16),
                 ("nccl_unique_id", c_uint8 * 128), ("arena_slab_bytes", c_uint64),
-                ("gemm_max_ctas", c_int32), ("transport", c_int32)]
+                ("gemm_max_ctas", c_int32), ("transport", c_int32), ("panel_cache_bytes", c_uint64),
+                ("pipeline_chunks", c_int32)]
 
 
 class gm_worker_stats(Structure):

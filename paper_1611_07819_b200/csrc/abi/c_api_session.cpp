@@ -91,6 +91,8 @@ int gm_session_create(const gm_session_options* o, gm_session** out) {
     std::memcpy(opts.ncclId.data(), o->nccl_unique_id, 128);
     opts.gemmMaxCtas = o->gemm_max_ctas;
     opts.transport = o->transport;
+    opts.panelCacheBytes = o->panel_cache_bytes;
+    opts.pipelineChunks = o->pipeline_chunks;
     auto* s = new gm_session;
     try {
       s->s = std::make_unique<gridmath::Session>(opts);

@@ -121,6 +121,12 @@ Precision DistMatrix::precision() const { return session_->descriptor(id_).preci
 
 // ---------------------------------------------------------------- PanelCache
 
+bool PanelCache::contains(std::uint64_t id, std::uint64_t version, const Rect& r) const {
+  for (const CacheEntry& e : entries_)
+    if (e.matrixId == id && e.version == version && e.rect == r) return true;
+  return false;
+}
+
 CacheEntry* PanelCache::lookup(std::uint64_t id, std::uint64_t version, const Rect& r,
                                std::uint64_t tick) {
   for (CacheEntry& e : entries_)
@@ -876,23 +882,36 @@ void Session::execGemm(const OpDescriptor& op) {
     Worker* w = local(r);
     return w ? w->cache : remoteCaches_[r];
   };
-  // Probe only (no LRU side effects): the directory is updated below in plan order.
   const GemmPlanB200 plan = planGemmB200(table_, op, P, [&](std::uint32_t r, const MatrixDescriptor& M, const Rect& rect) {
-    PanelCache& dir = dirOf(r);
-    const std::uint64_t h = dir.hits, mi = dir.misses;
-    const bool hit = dir.lookup(M.matrixId, M.version, rect, 0) != nullptr;
-    dir.hits = h;
-    dir.misses = mi;
-    return hit;
+    return dirOf(r).contains(M.matrixId, M.version, rect);
   });
+
+  // SUMMA-style overlap: gathered bands move on the comm stream in groups --
+  // first every gathered B band, then the gathered A bands in `S` row chunks
+  // (m direction). The compute stream runs the GEMM of C rows chunk j as soon
+  // as chunk j has landed. Every rank issues the same groups in the same
+  // order, so the NCCL point-to-point calls match.
+  std::uint32_t S = opts_.pipelineChunks > 0 ? static_cast<std::uint32_t>(opts_.pipelineChunks) : 2u;
+  bool anyGather = false;
+  for (const PlannedNeed& nd : plan.needs)
+    if (nd.kind == PlannedNeed::Gather) anyGather = true;
+  if (!anyGather || plan.m < 512 * S) S = 1;
 
   std::vector<std::vector<BandView>> aViews(P), bViews(P);
   for (std::uint32_t w = 0; w < P; ++w) {
     aViews[w].resize(plan.rowsOf[w].size());
     bViews[w].resize(plan.colsOf[w].size());
   }
-  std::vector<Xfer> xfers;
-  std::vector<std::pair<Worker*, CacheEntry*>> fresh;
+  // groups[0] = B bands, groups[1 + j] = A chunk j.
+  std::vector<std::vector<Xfer>> groups(1 + S);
+  std::vector<CacheEntry*> freshEntries;
+  std::vector<Worker*> freshOwners;
+
+  // m-chunk j of the interval [lo, hi): [lo + j*len/S, lo + (j+1)*len/S).
+  auto chunkRange = [&](std::uint64_t lo, std::uint64_t hi, std::uint32_t j) {
+    const std::uint64_t len = hi - lo;
+    return std::make_pair(lo + len * j / S, lo + len * (j + 1) / S);
+  };
 
   for (const PlannedNeed& nd : plan.needs) {
     const MatrixDescriptor& M = nd.operand == 0 ? A : B;
@@ -938,101 +957,173 @@ void Session::execGemm(const OpDescriptor& op) {
         e.ld = paddedLd(nd.rect.cols(), eb);
         e.bytes = nd.rect.rows() * e.ld * eb;
         e.lastUse = tick_;
+        // Allocate before evicting so back-to-back ops double-buffer their
+        // bands (the next op's gather does not wait for this op's GEMM).
+        if (w) {
+          w->activate();
+          e.ptr = w->arena.alloc(e.bytes, w->comm);
+        }
         const std::uint64_t budget = w ? w->cacheBudget : localRef->cacheBudget;
         for (CacheEntry& ev : dir.reserve(e.bytes, budget, tick_))
           if (w && ev.ptr) {
-            w->activate();
             w->arena.free(ev.ptr, w->compute);
             w->recycle(ev.ready);
           }
-        if (w) {
-          w->activate();
-          e.ptr = w->arena.alloc(e.bytes, w->compute);
-        }
         CacheEntry& slot = dir.insert(e);
         if (w) {
-          fresh.push_back({w, &slot});
+          freshEntries.push_back(&slot);
+          freshOwners.push_back(w);
           view = {slot.ptr, slot.ld};
         }
+        // Which group each piece belongs to: B whole; A split by m rows
+        // (stored rows for A, stored columns for transposed A).
         for (const PieceRoute& pr : nd.pieces) {
           Worker* sw = local(pr.src);
           if (!w && !sw) continue;
-          Xfer x;
-          x.src = pr.src;
-          x.dst = nd.worker;
-          x.rows = pr.rect.rows();
-          x.cols = pr.rect.cols();
-          x.eb = static_cast<std::uint32_t>(eb);
-          if (sw)
-            for (const DeviceTile& dt : sw->tiles.at(M.matrixId))
-              if (pr.rect.inside(Rect::ofExtent(dt.extent))) {
-                x.srcPtr = static_cast<const std::uint8_t*>(dt.ptr) +
-                           ((pr.rect.r0 - dt.extent.rowStart) * dt.ld + (pr.rect.c0 - dt.extent.colStart)) * eb;
-                x.srcLd = dt.ld;
+          std::vector<std::pair<std::uint32_t, Rect>> parts;
+          if (nd.operand == 1 || S == 1) {
+            parts.push_back({nd.operand == 1 ? 0u : 1u, pr.rect});
+          } else {
+            for (std::uint32_t j = 0; j < S; ++j) {
+              Rect sub = pr.rect;
+              if (!plan.transA) {
+                const auto rg = chunkRange(nd.rect.r0, nd.rect.r1, j);
+                sub.r0 = std::max(sub.r0, rg.first);
+                sub.r1 = std::min(sub.r1, rg.second);
+              } else {
+                const auto rg = chunkRange(nd.rect.c0, nd.rect.c1, j);
+                sub.c0 = std::max(sub.c0, rg.first);
+                sub.c1 = std::min(sub.c1, rg.second);
               }
-          if (w) {
-            x.dstPtr = static_cast<std::uint8_t*>(slot.ptr) +
-                       ((pr.rect.r0 - nd.rect.r0) * slot.ld + (pr.rect.c0 - nd.rect.c0)) * eb;
-            x.dstLd = slot.ld;
+              if (!sub.empty()) parts.push_back({1 + j, sub});
+            }
           }
-          xfers.push_back(x);
+          for (const auto& part : parts) {
+            const Rect& r = part.second;
+            Xfer x;
+            x.src = pr.src;
+            x.dst = nd.worker;
+            x.rows = r.rows();
+            x.cols = r.cols();
+            x.eb = static_cast<std::uint32_t>(eb);
+            if (sw)
+              for (const DeviceTile& dt : sw->tiles.at(M.matrixId))
+                if (r.inside(Rect::ofExtent(dt.extent))) {
+                  x.srcPtr = static_cast<const std::uint8_t*>(dt.ptr) +
+                             ((r.r0 - dt.extent.rowStart) * dt.ld + (r.c0 - dt.extent.colStart)) * eb;
+                  x.srcLd = dt.ld;
+                }
+            if (w) {
+              x.dstPtr = static_cast<std::uint8_t*>(slot.ptr) + ((r.r0 - nd.rect.r0) * slot.ld + (r.c0 - nd.rect.c0)) * eb;
+              x.dstLd = slot.ld;
+            }
+            groups[part.first].push_back(x);
+          }
         }
         break;
       }
     }
     (nd.operand == 0 ? aViews : bViews)[nd.worker][nd.interval] = view;
   }
-  if (!xfers.empty()) exchange(xfers, false);
-  for (auto& fr : fresh) {
-    fr.first->activate();
-    fr.second->ready = fr.first->event();
-    cudaCheck(cudaEventRecord(fr.second->ready, fr.first->compute), "gemm: panel ready");
+
+  // Comm stream: B bands, then A chunks; an event per group per local worker.
+  std::vector<std::vector<cudaEvent_t>> groupDone(1 + S);
+  for (std::uint32_t gi = 0; gi <= S; ++gi) {
+    if (groups[gi].empty()) continue;
+    exchange(groups[gi], true);
+    for (auto& wp : workers_) {
+      if (!wp) continue;
+      wp->activate();
+      cudaEvent_t ev = wp->event();
+      cudaCheck(cudaEventRecord(ev, wp->comm), "gemm: group done");
+      groupDone[gi].push_back(ev);
+    }
   }
+  // Gathered bands become cache entries ready when the last group lands.
+  for (std::size_t i = 0; i < freshEntries.size(); ++i) {
+    Worker* w = freshOwners[i];
+    w->activate();
+    freshEntries[i]->ready = w->event();
+    cudaCheck(cudaEventRecord(freshEntries[i]->ready, w->comm), "gemm: panel ready");
+  }
+  auto waitGroup = [&](Worker& w, std::uint32_t gi) {
+    if (groupDone[gi].empty()) return;
+    std::size_t idx = 0;
+    for (auto& wp : workers_) {
+      if (!wp) continue;
+      if (wp.get() == &w) {
+        cudaCheck(cudaStreamWaitEvent(w.compute, groupDone[gi][idx], 0), "gemm: wait group");
+        return;
+      }
+      ++idx;
+    }
+  };
 
   const bool alphaZero = op.s0 == 0.0;
-  const std::uint64_t ebA = bytesOf(A.precision), ebB = bytesOf(B.precision);
+  const std::uint64_t ebA = bytesOf(A.precision), ebB = bytesOf(B.precision), ebC = bytesOf(C.precision);
   forEachLocal([&](Worker& w) {
+    waitGroup(w, 0);
     cudaCheck(cudaEventRecord(w.kStart, w.compute), "gemm: timing");
-    for (DeviceTile& ct : w.tiles.at(C.matrixId)) {
-      const TileExtent& e = ct.extent;
-      gm_gemm_desc d{};
-      d.m = e.rowCount;
-      d.n = e.colCount;
-      d.k = plan.k;
-      d.trans_a = plan.transA;
-      d.trans_b = plan.transB;
-      d.prec_a = static_cast<int>(A.precision);
-      d.prec_b = static_cast<int>(B.precision);
-      d.prec_c = static_cast<int>(C.precision);
-      d.math = op.flags[3];
-      d.cta_group = 2;
-      d.max_ctas = opts_.gemmMaxCtas;
-      d.alpha = op.s0;
-      d.beta = op.s1;
-      d.ldc = ct.ld;
-      const void* ap = nullptr;
-      const void* bp = nullptr;
-      if (!alphaZero) {
+    for (std::uint32_t j = 0; j < S; ++j) {
+      waitGroup(w, 1 + j);
+      for (DeviceTile& ct : w.tiles.at(C.matrixId)) {
+        const TileExtent& e = ct.extent;
         std::size_t ri = 0, ci = 0;
-        while (!(e.rowStart >= plan.rowsOf[w.rank][ri].first && e.rowStart < plan.rowsOf[w.rank][ri].second)) ++ri;
-        while (!(e.colStart >= plan.colsOf[w.rank][ci].first && e.colStart < plan.colsOf[w.rank][ci].second)) ++ci;
-        const BandView av = aViews[w.rank][ri];
-        const BandView bv = bViews[w.rank][ci];
-        const std::uint64_t roff = e.rowStart - plan.rowsOf[w.rank][ri].first;
-        const std::uint64_t coff = e.colStart - plan.colsOf[w.rank][ci].first;
-        ap = plan.transA ? static_cast<const std::uint8_t*>(av.ptr) + roff * ebA
-                         : static_cast<const std::uint8_t*>(av.ptr) + roff * av.ld * ebA;
-        bp = plan.transB ? static_cast<const std::uint8_t*>(bv.ptr) + coff * bv.ld * ebB
-                         : static_cast<const std::uint8_t*>(bv.ptr) + coff * ebB;
-        d.lda = av.ld;
-        d.ldb = bv.ld;
+        if (!alphaZero || true) {
+          while (!(e.rowStart >= plan.rowsOf[w.rank][ri].first && e.rowStart < plan.rowsOf[w.rank][ri].second)) ++ri;
+          while (!(e.colStart >= plan.colsOf[w.rank][ci].first && e.colStart < plan.colsOf[w.rank][ci].second)) ++ci;
+        }
+        // Rows of this C tile inside m-chunk j of its row interval.
+        const auto rg = chunkRange(plan.rowsOf[w.rank][ri].first, plan.rowsOf[w.rank][ri].second, j);
+        const std::uint64_t r0 = std::max<std::uint64_t>(e.rowStart, rg.first);
+        const std::uint64_t r1 = std::min<std::uint64_t>(e.rowEnd(), rg.second);
+        if (r0 >= r1) continue;
+        gm_gemm_desc d{};
+        d.m = r1 - r0;
+        d.n = e.colCount;
+        d.k = plan.k;
+        d.trans_a = plan.transA;
+        d.trans_b = plan.transB;
+        d.prec_a = static_cast<int>(A.precision);
+        d.prec_b = static_cast<int>(B.precision);
+        d.prec_c = static_cast<int>(C.precision);
+        d.math = op.flags[3];
+        d.cta_group = 2;
+        d.max_ctas = opts_.gemmMaxCtas;
+        d.alpha = op.s0;
+        d.beta = op.s1;
+        d.ldc = ct.ld;
+        void* cp = static_cast<std::uint8_t*>(ct.ptr) + (r0 - e.rowStart) * ct.ld * ebC;
+        const void* ap = nullptr;
+        const void* bp = nullptr;
+        if (!alphaZero) {
+          const BandView av = aViews[w.rank][ri];
+          const BandView bv = bViews[w.rank][ci];
+          const std::uint64_t roff = r0 - plan.rowsOf[w.rank][ri].first;
+          const std::uint64_t coff = e.colStart - plan.colsOf[w.rank][ci].first;
+          ap = plan.transA ? static_cast<const std::uint8_t*>(av.ptr) + roff * ebA
+                           : static_cast<const std::uint8_t*>(av.ptr) + roff * av.ld * ebA;
+          bp = plan.transB ? static_cast<const std::uint8_t*>(bv.ptr) + coff * bv.ld * ebB
+                           : static_cast<const std::uint8_t*>(bv.ptr) + coff * ebB;
+          d.lda = av.ld;
+          d.ldb = bv.ld;
+        }
+        const std::uint64_t wsb = alphaZero ? 0 : gemmWorkspaceBytes(d, ap, bp);
+        void* ws = wsb ? w.workspace(wsb) : nullptr;
+        gemmLocal(d, ap, bp, cp, ws, wsb, w.compute);
       }
-      const std::uint64_t wsb = alphaZero ? 0 : gemmWorkspaceBytes(d, ap, bp);
-      void* ws = wsb ? w.workspace(wsb) : nullptr;
-      gemmLocal(d, ap, bp, ct.ptr, ws, wsb, w.compute);
     }
     cudaCheck(cudaEventRecord(w.tEnd, w.compute), "gemm: timing");
   });
+  // Group events go back to their pools (waits are already enqueued).
+  for (auto& evs : groupDone) {
+    std::size_t idx = 0;
+    for (auto& wp : workers_) {
+      if (!wp) continue;
+      if (idx < evs.size()) wp->recycle(evs[idx]);
+      ++idx;
+    }
+  }
 }
 
 void Session::synchronize() {

@@ -111,6 +111,7 @@ struct CacheEntry {
 class PanelCache {
  public:
   CacheEntry* lookup(std::uint64_t id, std::uint64_t version, const Rect& r, std::uint64_t tick);
+  bool contains(std::uint64_t id, std::uint64_t version, const Rect& r) const;
   // Returns entries evicted to make room (caller frees their buffers).
   std::vector<CacheEntry> reserve(std::uint64_t bytes, std::uint64_t budget, std::uint64_t protectTick);
   CacheEntry& insert(CacheEntry e);

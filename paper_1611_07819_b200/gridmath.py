@@ -165,7 +165,8 @@ class Session:
 
     def __init__(self, workers: int = 1, deterministic: bool = True, devices: Optional[Sequence[int]] = None,
                  spmd_rank: int = -1, nccl_id: Optional[bytes] = None, gemm_max_ctas: int = 0,
-                 transport: int = 0, check_metadata_every_op: bool = False):
+                 transport: int = 0, check_metadata_every_op: bool = False, panel_cache_bytes: int = 0,
+                 pipeline_chunks: int = 0):
         lib = _lib.load()
         o = _lib.gm_session_options()
         lib.gm_session_options_default(ctypes.byref(o))
@@ -181,6 +182,8 @@ class Session:
             ctypes.memmove(o.nccl_unique_id, nccl_id, 128)
         o.gemm_max_ctas = gemm_max_ctas
         o.transport = transport
+        o.panel_cache_bytes = panel_cache_bytes
+        o.pipeline_chunks = pipeline_chunks
         self._h = ctypes.c_void_p()
         check(lib.gm_session_create(ctypes.byref(o), ctypes.byref(self._h)))
         self.workers = workers
