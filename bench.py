@@ -358,6 +358,78 @@ def run_ours(args):
         dist.destroy_process_group()
 
 
+def run_extra_config(args):
+    """Secondary configs (not the driver's bench line): BASELINE configs[3]
+    (FC fwd+bwd, batch 4096, 9216 -> 4096, replicated W, panel cache) and
+    configs[4] (fp64 16384^3 on DMMA). Same timing rules; prints one line."""
+    import torch
+
+    rank, world, local, dist = dist_setup(args.gpus)
+    torch.cuda.set_device(local)
+    from paper_1611_07819_b200 import gridmath as G
+    nccl_id = None
+    if world > 1:
+        obj = [G.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        nccl_id = obj[0]
+    g = G.makeWorkerGroup(world)
+    s = G.Session(workers=world, spmd_rank=rank if world > 1 else -1, devices=[local], nccl_id=nccl_id)
+    if args.config == "fc":
+        batch, fi, fo = 4096, 9216, 4096
+        X = s.createMatrix(batch, fi, G.Precision.BF16, G.makeRowBlockLayout(batch, fi, g))
+        W = s.createMatrix(fi, fo, G.Precision.BF16, G.makeColBlockLayout(fi, fo, g))
+        Y = s.createMatrix(batch, fo, G.Precision.BF16, G.makeRowBlockLayout(batch, fo, g))
+        D = s.createMatrix(batch, fo, G.Precision.BF16, G.makeRowBlockLayout(batch, fo, g))
+        dW = s.createMatrix(fi, fo, G.Precision.BF16, G.makeColBlockLayout(fi, fo, g))
+        dX = s.createMatrix(batch, fi, G.Precision.BF16, G.makeRowBlockLayout(batch, fi, g))
+        s.fillUniform(X, 1)
+        s.fillUniform(D, 3)
+        bound = 1.0 / math.sqrt(fi)
+
+        def step(i):
+            s.fillUniform(W, 100 + i, -bound, bound)  # stand-in for the SGD update (new W version)
+            s.replicateAsync(W)                       # W replicated to every worker (async)
+            s.gemmAsync(X, W, Y)                      # forward reads the replica
+            s.gemmAsync(X, D, dW, 1.0, 0.0, True, False)   # dW = X^T dY (gathers X)
+            s.gemmAsync(D, W, dX, 1.0, 0.0, False, True)   # dX = dY W^T (replica again)
+
+        flops = 3 * 2.0 * batch * fi * fo
+        workload = f"FC fwd+bwd bf16 batch {batch}, {fi}->{fo}, W col-block + replicated, X/Y row-block"
+    else:
+        n = 16384 if args.n == 32768 else args.n
+        pr, pc = grid_for(world)
+        lay = G.makeGridLayout(n, n, pr, pc, g)
+        A = s.createMatrix(n, n, G.Precision.Double, lay)
+        B = s.createMatrix(n, n, G.Precision.Double, lay)
+        C = s.createMatrix(n, n, G.Precision.Double, lay)
+        s.fillUniform(A, 1)
+        s.fillUniform(B, 2)
+
+        def step(i):
+            s.gemmAsync(A, B, C)
+
+        flops = 2.0 * n ** 3
+        workload = f"fp64 GEMM {n}^3 (DMMA) on a {pr}x{pc} grid"
+    for i in range(args.warmup):
+        step(i)
+    s.synchronize()
+    if dist is not None:
+        dist.barrier()
+    s.timerStart()
+    for i in range(args.steps):
+        step(args.warmup + i)
+    ms = allreduce_max(dist, s.timerStop())
+    st = s.queryWorkerStats()
+    if rank == 0:
+        print(json.dumps({"metric": METRIC, "config": {"workload": workload}, "n_gpus": world,
+                          "value": round(flops * args.steps / (ms / 1e3) / 1e12, 3), "unit": "TFLOP/s",
+                          "ms_per_step": round(ms / args.steps, 4), "steps": args.steps, "warmup": args.warmup,
+                          "worker0_stats": st[0]}), flush=True)
+    s.close()
+    if dist is not None:
+        dist.destroy_process_group()
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -370,11 +442,14 @@ def main():
     ap.add_argument("--pipeline-chunks", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", dest="cpu_baseline", action="store_false")
     ap.add_argument("--no-c2", dest="c2", action="store_false")
+    ap.add_argument("--config", default="c3", choices=["c3", "fc", "fp64"])
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
     if args.impl == "reference":
         run_reference(args)
+    elif args.config != "c3":
+        run_extra_config(args)
     else:
         run_ours(args)
 
