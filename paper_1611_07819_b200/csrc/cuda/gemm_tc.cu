@@ -79,6 +79,7 @@ struct TcParams {
   uint32_t c_vec;    // 16B vector stores legal
   uint32_t num_m_blocks, num_n_blocks;  // in units of the CTA(-pair) tile
   uint32_t group;                       // raster group (M-blocks)
+  uint32_t hint_a, hint_b;              // L2 policy for A / B loads (0 normal, 1 evict_last, 2 evict_first)
 };
 
 __device__ __forceinline__ void tile_coords(uint32_t t, const TcParams& p, uint32_t& mb,
@@ -212,6 +213,8 @@ __global__ void __launch_bounds__(kNumThreads, 1)
     // ------------------------------------------------------------ producer
     if (lane == 0) {
       uint32_t stage = 0, phase = 0;
+      const uint64_t pol_a = l2_policy(static_cast<int>(p.hint_a));
+      const uint64_t pol_b = l2_policy(static_cast<int>(p.hint_b));
       for (uint32_t t = unit; t < num_tiles; t += num_units) {
         uint32_t mb, nb;
         tile_coords(t, p, mb, nb);
@@ -230,7 +233,7 @@ __global__ void __launch_bounds__(kNumThreads, 1)
             uint8_t* da = sa + part * Cfg::kBytesA;
             uint8_t* db = sb + part * Cfg::kBytesB;
             if (!p.a_mn_major) {
-              if (kCG == 2) tma_load_2d_2sm(da, ma, &full_bar[stage], k0, m0);
+              if (kCG == 2) tma_load_2d_2sm_hint(da, ma, &full_bar[stage], k0, m0, pol_a);
               else tma_load_2d(da, ma, &full_bar[stage], k0, m0);
             } else {
               // MN-major: boxes of (128 B of M) x kBlockK rows of K.
@@ -252,7 +255,7 @@ __global__ void __launch_bounds__(kNumThreads, 1)
 #pragma unroll
                 for (uint32_t j = 0; j < kChunkNcta / kElems128; ++j) {
                   if (kCG == 2)
-                    tma_load_2d_2sm(dc + j * kBlockK * kSwizzleBytes, mbm, &full_bar[stage], n0 + j * kElems128, k0);
+                    tma_load_2d_2sm_hint(dc + j * kBlockK * kSwizzleBytes, mbm, &full_bar[stage], n0 + j * kElems128, k0, pol_b);
                   else
                     tma_load_2d(dc + j * kBlockK * kSwizzleBytes, mbm, &full_bar[stage], n0 + j * kElems128, k0);
                 }
@@ -459,6 +462,10 @@ int launch(const TcOperand& a, const TcOperand& b, const TcOperand* a_lo, const 
       return e ? static_cast<uint32_t>(std::atoi(e)) : 0u;
     }();
     p.group = env_group ? env_group : 32;
+    static const uint32_t ha = std::getenv("GM_HINT_A") ? std::atoi(std::getenv("GM_HINT_A")) : 0;
+    static const uint32_t hb = std::getenv("GM_HINT_B") ? std::atoi(std::getenv("GM_HINT_B")) : 0;
+    p.hint_a = ha;
+    p.hint_b = hb;
     if (p.group > p.num_m_blocks) p.group = p.num_m_blocks;
   }
   p.num_n_blocks = (p.n + Cfg::kBlockN - 1) / Cfg::kBlockN;

@@ -233,3 +233,24 @@ def test_kernel_numerics_vs_torch_fp32():
         torch.cuda.synchronize()
         ref = (A.float().T if ta else A.float()) @ (B.float().T if tb else B.float())
         assert ((C - ref).norm() / ref.norm()).item() <= 1e-5
+
+
+def test_layout_invariance_bitwise_wide_tiles():
+    # k >= 4096 selects the 256x512 (two-UMMA) tile for C tiles wider than 256
+    # columns and the 256x256 tile otherwise; both give the same bits.
+    m, n, k = 1024, 768, 4608
+    a = O.fill_uniform(m, k, 3, 41)
+    b = O.fill_uniform(k, n, 3, 42)
+    c = np.zeros((m, n), dtype=np.float32)
+    outs = [
+        run_session_gemm(1, a, 3, [(0, m, 0, k, 0)], b, 3, [(0, k, 0, n, 0)], c, 1, [(0, m, 0, n, 0)], 1.0, 0.0, 0, 0),
+        run_session_gemm(4, a, 3, O.grid_tiles(m, k, 2, 2), b, 3, O.grid_tiles(k, n, 2, 2), c, 1,
+                         O.grid_tiles(m, n, 2, 2), 1.0, 0.0, 0, 0),
+        run_session_gemm(8, a, 3, O.row_block_tiles(m, k, 8), b, 3, O.col_block_tiles(k, n, 8), c, 1,
+                         O.col_block_tiles(m, n, 8), 1.0, 0.0, 0, 0),
+    ]
+    for o in outs[1:]:
+        assert np.array_equal(o.view(np.uint32), outs[0].view(np.uint32))
+    rows = (100, 116)
+    want = O.gemm_c(m, n, k, a, 3, b, 3, c, 1, 1.0, 0.0, 0, 0, rows)
+    assert O.rel_fro(outs[0][rows[0]:rows[1]], want[rows[0]:rows[1]]) < 1e-5
