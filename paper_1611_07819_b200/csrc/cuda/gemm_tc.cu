@@ -51,7 +51,7 @@ constexpr uint32_t kNumThreads = 192;  // 6 warps
 // (128 * kCG) x (256 * kChunks). kChunks = 2 fills all 512 TMEM columns with
 // one accumulator (no accumulator double-buffering); kChunks = 1 keeps two
 // accumulators so the epilogue of tile t overlaps the MMAs of tile t+1.
-template <int kCG, int kElemBytes, int kSplit, int kChunks>
+template <int kCG, int kElemBytes, int kSplit, int kChunks, int kPairs = 1>
 struct TcCfg {
   static constexpr uint32_t kBlockK = kSwizzleBytes / kElemBytes;
   static constexpr uint32_t kMmaK = 32 / kElemBytes;  // 16 (f16) or 8 (tf32)
@@ -65,7 +65,9 @@ struct TcCfg {
   static constexpr uint32_t kStageBytes = kParts * (kBytesA + kBytesB);
   static constexpr uint32_t kStages = (196u * 1024u) / kStageBytes;
   static constexpr uint32_t kSmemBytes = kStages * kStageBytes + 1024 + 256;
+  static constexpr uint32_t kClusterCtas = kCG * kPairs;
   static_assert(kAccStages * kChunks * kMmaN <= 512, "TMEM columns");
+  static_assert(kPairs == 1 || kCG == 2, "A multicast across pairs needs 2-SM pairs");
 };
 
 struct TcParams {
@@ -80,14 +82,40 @@ struct TcParams {
   uint32_t num_m_blocks, num_n_blocks;  // in units of the CTA(-pair) tile
   uint32_t group;                       // raster group (M-blocks)
   uint32_t hint_a, hint_b;              // L2 policy for A / B loads (0 normal, 1 evict_last, 2 evict_first)
+  uint32_t* sync_ctr;                   // lockstep counter (zeroed per launch) or null
+  uint32_t sync_every;                  // k-blocks per lockstep checkpoint
 };
 
-__device__ __forceinline__ void tile_coords(uint32_t t, const TcParams& p, uint32_t& mb,
-                                            uint32_t& nb) {
+// Lockstep: persistent CTA pairs run ~100 tiles back to back and drift apart,
+// after which pairs that share a panel no longer read it while it is in L2.
+// Every `sync_every` k-blocks the pair leader's producer checks in and waits
+// until all pairs reached the previous checkpoint. The wait is bounded
+// (~40 us) and a pair whose wait ever times out stops waiting for the rest of
+// the launch, so a pair that is not resident (SMs held by another kernel) or
+// a finished tail delays the others at most once and never blocks them.
+// Returns false on timeout.
+__device__ __forceinline__ bool lockstep(uint32_t* ctr, uint32_t checkpoint, uint32_t units) {
+  atomicAdd(ctr, 1u);
+  const uint32_t target = checkpoint * units;
+  uint64_t t0;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  for (;;) {
+    uint32_t v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(ctr) : "memory");
+    if (v >= target) return true;
+    uint64_t t1;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+    if (t1 - t0 > 40000) return false;
+    __nanosleep(64);
+  }
+}
+
+__device__ __forceinline__ void tile_coords(uint32_t t, const TcParams& p, uint32_t num_n,
+                                            uint32_t& mb, uint32_t& nb) {
   // Rasterize in groups of `group` M-blocks (m-fastest inside a group) so the
   // tiles that run concurrently share A and B k-slabs in L2.
   const uint32_t group = p.group;
-  const uint32_t per_group = group * p.num_n_blocks;
+  const uint32_t per_group = group * num_n;
   const uint32_t g = t / per_group;
   const uint32_t first_m = g * group;
   const uint32_t gsize = min(group, p.num_m_blocks - first_m);
@@ -153,12 +181,16 @@ __device__ __forceinline__ void store_row32(const TcParams& p, uint32_t row, uin
 }
 
 // kSplit: 3xTF32 (maps a_hi/a_lo, b_hi/b_lo). Otherwise a single pair.
-template <int kCG, int kElemBytes, int kSplit, int kChunks>
+// kPairs = 2: a 4-CTA cluster holds two UMMA pairs that compute the same
+// M-block and adjacent N-blocks; each CTA fetches half of the A slab its
+// counterpart in the other pair also needs and multicasts it (A leaves L2 once
+// per cluster, and the two pairs stay in lockstep, so their A reuse holds).
+template <int kCG, int kElemBytes, int kSplit, int kChunks, int kPairs>
 __global__ void __launch_bounds__(kNumThreads, 1)
     tc_gemm_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid_constant__ CUtensorMap tm_b,
                    const __grid_constant__ CUtensorMap tm_a_lo,
                    const __grid_constant__ CUtensorMap tm_b_lo, const TcParams p) {
-  using Cfg = TcCfg<kCG, kElemBytes, kSplit, kChunks>;
+  using Cfg = TcCfg<kCG, kElemBytes, kSplit, kChunks, kPairs>;
   constexpr uint32_t kStages = Cfg::kStages;
   constexpr uint32_t kBlockK = Cfg::kBlockK;
   constexpr uint32_t kMmaK = Cfg::kMmaK;
@@ -176,8 +208,12 @@ __global__ void __launch_bounds__(kNumThreads, 1)
 
   const uint32_t warp = warp_id_sync();
   const uint32_t lane = threadIdx.x & 31;
-  const uint32_t rank = (kCG == 2) ? cluster_ctarank() : 0;
+  const uint32_t crank = (kCG == 2) ? cluster_ctarank() : 0;  // rank in cluster
+  const uint32_t rank = crank & (kCG - 1);                      // rank in the UMMA pair
+  const uint32_t pair = crank / kCG;                            // pair in the cluster
   const bool leader = rank == 0;
+  const uint16_t pair_mask = static_cast<uint16_t>(((1u << kCG) - 1) << (pair * kCG));
+  const uint16_t all_mask = static_cast<uint16_t>((1u << Cfg::kClusterCtas) - 1);
 
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tm_a);
@@ -188,7 +224,7 @@ __global__ void __launch_bounds__(kNumThreads, 1)
     }
     for (uint32_t s = 0; s < kStages; ++s) {
       mbar_init(&full_bar[s], 1);
-      mbar_init(&empty_bar[s], 1);
+      mbar_init(&empty_bar[s], kPairs);  // a commit from every pair that reads the slot
     }
     for (uint32_t a = 0; a < kAcc; ++a) {
       mbar_init(&tfull_bar[a], 1);
@@ -205,9 +241,12 @@ __global__ void __launch_bounds__(kNumThreads, 1)
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
-  const uint32_t num_tiles = p.num_m_blocks * p.num_n_blocks;
+  // Work units: (M-block, group of kPairs N-blocks); pair `pair` takes N-block
+  // nbu * kPairs + pair of the unit.
+  const uint32_t num_nbu = (p.num_n_blocks + kPairs - 1) / kPairs;
+  const uint32_t num_tiles = p.num_m_blocks * num_nbu;
   const uint32_t num_kb = (p.k + kBlockK - 1) / kBlockK;
-  const uint32_t unit = blockIdx.x / kCG, num_units = gridDim.x / kCG;
+  const uint32_t unit = blockIdx.x / Cfg::kClusterCtas, num_units = gridDim.x / Cfg::kClusterCtas;
 
   if (warp == 0) {
     // ------------------------------------------------------------ producer
@@ -215,11 +254,18 @@ __global__ void __launch_bounds__(kNumThreads, 1)
       uint32_t stage = 0, phase = 0;
       const uint64_t pol_a = l2_policy(static_cast<int>(p.hint_a));
       const uint64_t pol_b = l2_policy(static_cast<int>(p.hint_b));
-      for (uint32_t t = unit; t < num_tiles; t += num_units) {
-        uint32_t mb, nb;
-        tile_coords(t, p, mb, nb);
+      bool sync = p.sync_ctr != nullptr && crank == 0;
+      const bool synced = sync;
+      const uint32_t cps_per_tile = sync ? (num_kb + p.sync_every - 1) / p.sync_every : 0;
+      uint32_t local_tile = 0;
+      for (uint32_t t = unit; t < num_tiles; t += num_units, ++local_tile) {
+        uint32_t mb, nbu;
+        tile_coords(t, p, num_nbu, mb, nbu);
+        const uint32_t nb = nbu * kPairs + pair;
         const int32_t m0 = static_cast<int32_t>(mb * kBlockMcta * kCG + rank * kBlockMcta);
         for (uint32_t kb = 0; kb < num_kb; ++kb) {
+          if (sync && kb % p.sync_every == 0)
+            sync = lockstep(p.sync_ctr, local_tile * cps_per_tile + kb / p.sync_every, num_units);
           mbar_wait(&empty_bar[stage], phase ^ 1);
           uint8_t* sa = smem + stage * Cfg::kStageBytes;
           uint8_t* sb = sa + Cfg::kParts * Cfg::kBytesA;
@@ -232,7 +278,18 @@ __global__ void __launch_bounds__(kNumThreads, 1)
             const CUtensorMap* mbm = part ? &tm_b_lo : &tm_b;
             uint8_t* da = sa + part * Cfg::kBytesA;
             uint8_t* db = sb + part * Cfg::kBytesB;
-            if (!p.a_mn_major) {
+            if constexpr (kPairs == 2) {
+              // This CTA loads half of the A slab (its pair index picks the
+              // half) into both pairs' CTAs with the same in-pair rank.
+              const uint16_t mc = static_cast<uint16_t>((1u << rank) | (1u << (kCG + rank)));
+              if (!p.a_mn_major) {
+                tma_load_2d_2sm_mc(da + pair * (kBlockMcta / 2) * kSwizzleBytes, ma, &full_bar[stage], k0,
+                                   m0 + static_cast<int32_t>(pair * (kBlockMcta / 2)), mc, pol_a);
+              } else {
+                tma_load_2d_2sm_mc(da + pair * kBlockK * kSwizzleBytes, ma, &full_bar[stage],
+                                   m0 + static_cast<int32_t>(pair * kElems128), k0, mc, pol_a);
+              }
+            } else if (!p.a_mn_major) {
               if (kCG == 2) tma_load_2d_2sm_hint(da, ma, &full_bar[stage], k0, m0, pol_a);
               else tma_load_2d(da, ma, &full_bar[stage], k0, m0);
             } else {
@@ -271,6 +328,7 @@ __global__ void __launch_bounds__(kNumThreads, 1)
           }
         }
       }
+      if (synced) atomicAdd(p.sync_ctr, 1u << 24);  // finished: release the others' waits
     }
   } else if (warp == 1) {
     // ------------------------------------------------------------ MMA issuer
@@ -313,10 +371,10 @@ __global__ void __launch_bounds__(kNumThreads, 1)
               }
             }
           }
-          if constexpr (kCG == 2) mma_commit_2sm(&empty_bar[stage], 0x3);
+          if constexpr (kCG == 2) mma_commit_2sm(&empty_bar[stage], all_mask);
           else mma_commit(&empty_bar[stage]);
           if (kb + 1 == num_kb) {
-            if constexpr (kCG == 2) mma_commit_2sm(&tfull_bar[acc], 0x3);
+            if constexpr (kCG == 2) mma_commit_2sm(&tfull_bar[acc], pair_mask);
             else mma_commit(&tfull_bar[acc]);
           }
           if (++stage == kStages) {
@@ -335,8 +393,9 @@ __global__ void __launch_bounds__(kNumThreads, 1)
     const uint32_t lane_grp = warp & 3;  // TMEM lanes [32*lane_grp, +32)
     uint32_t acc = 0, acc_phase = 0;
     for (uint32_t t = unit; t < num_tiles; t += num_units) {
-      uint32_t mb, nb;
-      tile_coords(t, p, mb, nb);
+      uint32_t mb, nbu;
+      tile_coords(t, p, num_nbu, mb, nbu);
+      const uint32_t nb = nbu * kPairs + pair;
       mbar_wait(&tfull_bar[acc], acc_phase);
       tc_fence_after();
       const uint32_t row = mb * kBlockMcta * kCG + rank * kBlockMcta + lane_grp * 32 + lane;
@@ -352,7 +411,7 @@ __global__ void __launch_bounds__(kNumThreads, 1)
       tc_fence_before();
       __syncwarp();
       if (lane == 0) {
-        if (kCG == 2 && !leader) mbar_arrive_cluster(&tempty_bar[acc], 0);
+        if (kCG == 2 && !leader) mbar_arrive_cluster(&tempty_bar[acc], pair * kCG);
         else mbar_arrive(&tempty_bar[acc]);
       }
       if (++acc == kAcc) {
@@ -429,10 +488,10 @@ int sm_count(int dev) {
   return counts[dev];
 }
 
-template <int kCG, int kElemBytes, int kSplit, int kChunks>
+template <int kCG, int kElemBytes, int kSplit, int kChunks, int kPairs = 1>
 int launch(const TcOperand& a, const TcOperand& b, const TcOperand* a_lo, const TcOperand* b_lo,
            const TcParams& p0, int max_ctas, cudaStream_t stream, const char** err) {
-  using Cfg = TcCfg<kCG, kElemBytes, kSplit, kChunks>;
+  using Cfg = TcCfg<kCG, kElemBytes, kSplit, kChunks, kPairs>;
   const CUtensorMapDataType dt = kElemBytes == 4 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32
                                                  : CU_TENSOR_MAP_DATA_TYPE_UINT16;
   constexpr uint32_t kChunk = kSwizzleBytes / kElemBytes;
@@ -440,7 +499,7 @@ int launch(const TcOperand& a, const TcOperand& b, const TcOperand* a_lo, const 
   CUtensorMap ma, mb, mal, mbl;
   auto map_a = [&](CUtensorMap* m, const TcOperand& op) {
     // A logical M x K. K-major: stored M rows x K cols; MN-major: K rows x M cols.
-    if (!p.a_mn_major) return make_map_2d(m, op.ptr, dt, kElemBytes, p.k, p.m, op.ld, Cfg::kBlockK, kBlockMcta, err);
+    if (!p.a_mn_major) return make_map_2d(m, op.ptr, dt, kElemBytes, p.k, p.m, op.ld, Cfg::kBlockK, kBlockMcta / kPairs, err);
     return make_map_2d(m, op.ptr, dt, kElemBytes, p.m, p.k, op.ld, kChunk, Cfg::kBlockK, err);
   };
   auto map_b = [&](CUtensorMap* m, const TcOperand& op) {
@@ -466,13 +525,17 @@ int launch(const TcOperand& a, const TcOperand& b, const TcOperand* a_lo, const 
     static const uint32_t hb = std::getenv("GM_HINT_B") ? std::atoi(std::getenv("GM_HINT_B")) : 0;
     p.hint_a = ha;
     p.hint_b = hb;
+    // Lockstep every 16 k-blocks for long-k launches (default; GM_TC_SYNC=0 off).
+    static const int se = std::getenv("GM_TC_SYNC") ? std::atoi(std::getenv("GM_TC_SYNC")) : -1;
+    const uint32_t kblocks = (p.k + Cfg::kBlockK - 1) / Cfg::kBlockK;
+    p.sync_every = se >= 0 ? static_cast<uint32_t>(se) : (kblocks >= 64 && kChunks == 2 ? 16u : 0u);
+    p.sync_ctr = nullptr;
     if (p.group > p.num_m_blocks) p.group = p.num_m_blocks;
   }
   p.num_n_blocks = (p.n + Cfg::kBlockN - 1) / Cfg::kBlockN;
-  const uint32_t tiles = p.num_m_blocks * p.num_n_blocks;
   int dev = 0;
   cudaGetDevice(&dev);
-  auto kern = tc_gemm_kernel<kCG, kElemBytes, kSplit, kChunks>;
+  auto kern = tc_gemm_kernel<kCG, kElemBytes, kSplit, kChunks, kPairs>;
   // Persistent grid = the number of CTAs (CTA pairs) that are co-resident.
   static int resident[64] = {0};
   cudaLaunchConfig_t cfg{};
@@ -481,7 +544,7 @@ int launch(const TcOperand& a, const TcOperand& b, const TcOperand* a_lo, const 
   cfg.stream = stream;
   cudaLaunchAttribute attrs[1];
   attrs[0].id = cudaLaunchAttributeClusterDimension;
-  attrs[0].val.clusterDim.x = kCG;
+  attrs[0].val.clusterDim.x = Cfg::kClusterCtas;
   attrs[0].val.clusterDim.y = 1;
   attrs[0].val.clusterDim.z = 1;
   cfg.attrs = attrs;
@@ -492,20 +555,28 @@ int launch(const TcOperand& a, const TcOperand& b, const TcOperand* a_lo, const 
     cfg.gridDim = dim3(sm_count(dev), 1, 1);
     if (cudaOccupancyMaxActiveClusters(&clusters, kern, &cfg) != cudaSuccess || clusters <= 0) {
       cudaGetLastError();
-      clusters = sm_count(dev) / kCG;
+      clusters = sm_count(dev) / Cfg::kClusterCtas;
     }
-    resident[dev] = clusters * kCG;
+    resident[dev] = clusters * Cfg::kClusterCtas;
   }
   int ctas = dev < 64 ? resident[dev] : sm_count(dev);
   if (max_ctas > 0 && max_ctas < ctas) ctas = max_ctas;
-  ctas = (ctas / kCG) * kCG;
-  const int need = static_cast<int>(tiles) * kCG;
+  ctas = (ctas / Cfg::kClusterCtas) * Cfg::kClusterCtas;
+  const int need = static_cast<int>((p.num_n_blocks + kPairs - 1) / kPairs * p.num_m_blocks) * Cfg::kClusterCtas;
   if (need < ctas) ctas = need;
   cfg.gridDim = dim3(ctas, 1, 1);
+  if (p.sync_every > 0) {
+    static uint32_t* ctr[64] = {nullptr};
+    if (dev < 64 && !ctr[dev]) cudaMalloc(&ctr[dev], 256);
+    if (dev < 64 && ctr[dev]) {
+      p.sync_ctr = ctr[dev];
+      cudaMemsetAsync(p.sync_ctr, 0, 4, stream);
+    }
+  }
   static const bool debug = std::getenv("GM_DEBUG") != nullptr;
   if (debug)
-    std::fprintf(stderr, "[gm] tc_gemm cg=%d elem=%d split=%d chunks=%d m=%u n=%u k=%u grid=%d resident=%d stages=%u smem=%u\n",
-                 kCG, kElemBytes, kSplit, kChunks, p.m, p.n, p.k, ctas, dev < 64 ? resident[dev] : -1,
+    std::fprintf(stderr, "[gm] tc_gemm cg=%d elem=%d split=%d chunks=%d pairs=%d m=%u n=%u k=%u grid=%d resident=%d stages=%u smem=%u\n",
+                 kCG, kElemBytes, kSplit, kChunks, kPairs, p.m, p.n, p.k, ctas, dev < 64 ? resident[dev] : -1,
                  Cfg::kStages, Cfg::kSmemBytes);
   cudaError_t e = cudaLaunchKernelEx(&cfg, kern, ma, mb, mal, mbl, p);
   count_launch();
@@ -546,6 +617,15 @@ int tc_gemm(const TcGemmArgs& g, cudaStream_t stream, const char** err) {
     const uint32_t fmt = g.kind == TcKind::BF16 ? 1 : 0;
     p.idesc = make_idesc(fmt, fmt, p.a_mn_major, p.b_mn_major, mrows, kMmaN);
     const bool wide = env_chunks ? env_chunks == 2 : (g.k >= 4096 && g.n > kMmaN);
+    static const int env_pairs = [] {
+      const char* e = std::getenv("GM_TC_PAIRS");
+      return e ? std::atoi(e) : 0;
+    }();
+    // Two pairs per cluster sharing A (multicast) once there are enough
+    // N-blocks for both pairs.
+    const bool pairs2 = env_pairs == 2;  // 4-CTA clusters place only 132 SMs: opt-in
+    if (cg == 2 && wide && pairs2)
+      return launch<2, 2, 0, 2, 2>(g.a, g.b, nullptr, nullptr, p, g.max_ctas, stream, err);
     if (cg == 1)
       return wide ? launch<1, 2, 0, 2>(g.a, g.b, nullptr, nullptr, p, g.max_ctas, stream, err)
                   : launch<1, 2, 0, 1>(g.a, g.b, nullptr, nullptr, p, g.max_ctas, stream, err);

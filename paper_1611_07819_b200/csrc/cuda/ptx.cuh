@@ -117,6 +117,18 @@ __device__ __forceinline__ void tma_load_2d_2sm_hint(void* dst, const CUtensorMa
       : "memory");
 }
 
+// 2-SM + multicast: the box lands at the same smem offset in every CTA of
+// `mask`; each destination pair's leader barrier receives the bytes.
+__device__ __forceinline__ void tma_load_2d_2sm_mc(void* dst, const CUtensorMap* m, uint64_t* bar,
+                                                   int32_t x, int32_t y, uint16_t mask, uint64_t pol) {
+  const uint32_t bar_addr = smem_u32(bar) & 0xFEFFFFFFu;
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+      ".multicast::cluster.L2::cache_hint [%0], [%1, {%4, %5}], [%2], %3, %6;" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(m)), "r"(bar_addr), "h"(mask), "r"(x), "r"(y), "l"(pol)
+      : "memory");
+}
+
 // 2-SM variant: the completion is signalled on the barrier of the leader CTA
 // (the barrier address is masked to the peer-0 shared window).
 __device__ __forceinline__ void tma_load_2d_2sm(void* dst, const CUtensorMap* m, uint64_t* bar,
