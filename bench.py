@@ -58,9 +58,14 @@ def measured_peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks/throttle sampling during the timed region."""
+    """nvidia-smi clocks/throttle sampling (50 ms) around the timed region.
 
-    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+    Started before the warm-up so the stream is already flowing; `stop()`
+    keeps the samples whose timestamps fall inside [t0, t1] (the timed
+    region), widening the window to the surrounding warm-up load only if the
+    region is shorter than the sampling period."""
+
+    FIELDS = ("timestamp,index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
               "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
               "clocks_event_reasons.sw_power_cap")
 
@@ -72,7 +77,7 @@ class ClockSampler:
     def start(self):
         try:
             self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
-                                          "-lms", "200", "-i", str(self.gpu)], stdout=subprocess.PIPE,
+                                          "-lms", "50", "-i", str(self.gpu)], stdout=subprocess.PIPE,
                                          stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
@@ -81,33 +86,42 @@ class ClockSampler:
 
     def _read(self):
         for line in self.proc.stdout:
-            self.lines.append(line.strip())
+            self.lines.append((time.time(), line.strip()))
 
-    def stop(self):
+    def stop(self, t0=None, t1=None):
         if not self.proc:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.12)
         self.proc.terminate()
         try:
             self.proc.wait(timeout=5)
         except Exception:
             self.proc.kill()
-        sm, mx, reasons = [], None, set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
+        parsed = []
+        for ts, ln in self.lines:
             parts = [p.strip() for p in ln.split(",")]
-            if len(parts) < 8:
+            if len(parts) < 9:
                 continue
             try:
-                sm.append(float(parts[1]))
-                mx = float(parts[2])
+                parsed.append((ts, float(parts[2]), float(parts[3]), float(parts[4]), parts[5:9]))
             except ValueError:
                 continue
-            for nm, v in zip(names, parts[4:8]):
+        window = "timed region"
+        sel = [x for x in parsed if t0 is None or (t0 <= x[0] <= t1 + 0.06)]
+        if not sel and parsed:
+            sel = [x for x in parsed if t0 - 1.0 <= x[0] <= t1 + 0.2] or parsed[-3:]
+            window = "warm-up + timed region (region shorter than the 50 ms sampling period)"
+        reasons = set()
+        for x in sel:
+            for nm, v in zip(names, x[4]):
                 if v.lower().startswith("active"):
                     reasons.add(nm)
-        busy = [x for x in sm if mx and x > 0.3 * mx] or sm
-        return {"sm_mhz": statistics.median(busy) if busy else None, "sm_max_mhz": mx,
-                "reasons": sorted(reasons), "samples": len(sm)}
+        sm = [x[1] for x in sel]
+        mx = sel[-1][2] if sel else None
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx,
+                "power_w_max": max((x[3] for x in sel), default=None),
+                "reasons": sorted(reasons), "samples": len(sel), "window": window}
 
 
 def dist_setup(n_gpus):
@@ -239,18 +253,21 @@ def run_ours(args):
             dist.barrier()
             torch.cuda.synchronize()
 
+    clocks = ClockSampler(local)
+    clocks.start()
+    time.sleep(0.3)
     for _ in range(args.warmup):
         s.gemmAsync(A, B, C)
     barrier()
 
-    clocks = ClockSampler(local)
     launches0 = G.kernel_launches()
-    clocks.start()
+    t_start = time.time()
     s.timerStart()
     for _ in range(args.steps):
         s.gemmAsync(A, B, C)
     ms = s.timerStop()
-    clk = clocks.stop()
+    t_end = time.time()
+    clk = clocks.stop(t_start, t_end)
     launches = G.kernel_launches() - launches0
     kernel_ms = max(s.lastOpKernelMs())
     barrier()
