@@ -1,0 +1,119 @@
+# SPDX-License-Identifier: Apache-2.0
+"""Device-layer checks through the C ABI: storage conversions (device vs the
+host convertBuffer restatement, bitwise, with edge values), the SplitMix64
+generator (device vs oracle, every precision), the pooled arena, and
+stream-ordered gemm_async chains with beta accumulation."""
+import ctypes
+
+import numpy as np
+import pytest
+
+import oracle as O
+from paper_1611_07819_b200 import _lib
+from paper_1611_07819_b200 import gridmath as G
+
+pytestmark = pytest.mark.gpu
+
+DT = {0: np.uint16, 1: np.float32, 2: np.float64, 3: np.uint16}
+
+
+def _edge_values():
+    v = [0.0, -0.0, 1.0, -1.0, 65504.0, 65519.99, 65520.0, -70000.0, 1e30, -1e-30, 6.0e-5, 5.96e-8,
+         2.98e-8, 1e-45, 3.4e38, float("inf"), float("-inf"), 1.0 / 3.0, 2.0 ** -24, 2.0 ** -25]
+    rng = np.random.default_rng(3)
+    v += list(rng.standard_normal(4000) * 100) + list(rng.uniform(-1e-4, 1e-4, 2000))
+    return np.array(v, dtype=np.float64)
+
+
+def _to_prec(x64, p):
+    out = np.empty(x64.size, dtype=DT[p])
+    _lib.check(_lib.load().gm_convert_host(x64.ctypes.data, 2, out.ctypes.data, p, x64.size))
+    return out
+
+
+def test_device_convert_matches_host_bitwise():
+    import torch
+    lib = _lib.load()
+    x64 = _edge_values()
+    for sp in (0, 1, 2, 3):
+        src = _to_prec(x64, sp)
+        for dp in (0, 1, 2, 3):
+            want = np.empty(src.size, dtype=DT[dp])
+            _lib.check(lib.gm_convert_host(src.ctypes.data, sp, want.ctypes.data, dp, src.size))
+            d_src = torch.from_numpy(src.view(np.uint8).copy()).cuda()
+            d_dst = torch.empty(want.nbytes, dtype=torch.uint8, device="cuda")
+            _lib.check(lib.gm_convert(d_src.data_ptr(), sp, d_dst.data_ptr(), dp, src.size, None))
+            torch.cuda.synchronize()
+            got = d_dst.cpu().numpy().view(DT[dp])
+            assert np.array_equal(got.view(np.uint8), want.view(np.uint8)), (sp, dp)
+
+
+def test_device_generator_matches_oracle_every_precision():
+    with G.Session(workers=3) as s:
+        for p in (0, 1, 2, 3):
+            M = s.createMatrix(37, 53, G.Precision(p), G.makeGridLayout(37, 53, 1, 3, G.makeWorkerGroup(3)))
+            s.fillUniform(M, 17, -2.0, 3.0)
+            got = s.getDataRaw(M)
+            want = O.fill_uniform(37, 53, p, 17, -2.0, 3.0)
+            assert np.array_equal(got.view(np.uint8), want.view(np.uint8)), p
+
+
+def test_arena_reuse_and_counters():
+    lib = _lib.load()
+    a = ctypes.c_void_p()
+    _lib.check(lib.gm_arena_create(0, 0, ctypes.byref(a)))
+    ptrs = []
+    for sz in (1000, 5000, 1 << 20, 3 << 20):
+        p = ctypes.c_void_p()
+        _lib.check(lib.gm_arena_alloc(a, sz, ctypes.byref(p)))
+        ptrs.append(p.value)
+    for p in ptrs:
+        _lib.check(lib.gm_arena_free(a, p))
+    for sz in (1000, 5000, 1 << 20, 3 << 20):
+        p = ctypes.c_void_p()
+        _lib.check(lib.gm_arena_alloc(a, sz, ctypes.byref(p)))
+        assert p.value in ptrs
+    st = _lib.gm_arena_stats()
+    _lib.check(lib.gm_arena_get_stats(a, ctypes.byref(st)))
+    assert st.allocations_from_os == 4 and st.reuses == 4 and st.frees == 4
+    with pytest.raises(_lib.GmError):
+        _lib.check(lib.gm_arena_free(a, 12345))
+    _lib.check(lib.gm_arena_destroy(a))
+
+
+def test_async_chain_with_beta_accumulation():
+    # C <- A B + C three times through the stream-ordered API (one sync at the end).
+    m, n, k, p = 640, 512, 768, 4
+    a = O.fill_uniform(m, k, 3, 61)
+    b = O.fill_uniform(k, n, 3, 62)
+    c0 = O.fill_uniform(m, n, 1, 63)
+    with G.Session(workers=p) as s:
+        A = s.createMatrix(m, k, G.Precision.BF16, G.makeGridLayout(m, k, 2, 2, G.makeWorkerGroup(p)))
+        B = s.createMatrix(k, n, G.Precision.BF16, G.makeRowBlockLayout(k, n, G.makeWorkerGroup(p)))
+        C = s.createMatrix(m, n, G.Precision.Single, G.makeColBlockLayout(m, n, G.makeWorkerGroup(p)))
+        s.setDataRaw(A, a)
+        s.setDataRaw(B, b)
+        s.setDataRaw(C, c0)
+        for _ in range(3):
+            s.gemmAsync(A, B, C, 1.0, 1.0)
+        s.synchronize()
+        got = s.getDataRaw(C)
+        assert C.version() == 4  # setData + 3 gemms
+    want = c0
+    for _ in range(3):
+        want = O.gemm_c(m, n, k, a, 3, b, 3, want, 1, 1.0, 1.0, 0, 0)
+    assert O.rel_fro(got, want) <= 1e-5
+
+
+def test_get_data_roundtrip_all_layouts():
+    rng = np.random.default_rng(9)
+    img = rng.standard_normal((97, 61)).astype(np.float32)
+    with G.Session(workers=4) as s:
+        for lay in (G.makeRowBlockLayout(97, 61, G.makeWorkerGroup(4)), G.makeColBlockLayout(97, 61, G.makeWorkerGroup(4)),
+                    G.makeGridLayout(97, 61, 2, 2, G.makeWorkerGroup(4)), G.makeSingleTileLayout(97, 61, 3)):
+            M = s.createMatrix(97, 61, G.Precision.Single, lay)
+            s.setDataRaw(M, img)
+            assert np.array_equal(s.getDataRaw(M), img)
+            s.setData(M, img.astype(np.float64) * 2)
+            assert np.array_equal(s.getData(M), (img * 2).astype(np.float64))
+            s.destroy(M)
