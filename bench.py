@@ -1,7 +1,7 @@
 # SPDX-License-Identifier: Apache-2.0
 """Benchmark: distributed GEMM TFLOP/s on 1/2/4/8 B200 (BASELINE.json metric).
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--n 32768]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--size 32768]
     torchrun --nproc-per-node N bench.py --gpus N ...   (one process per GPU)
 
 Workload (BASELINE.json configs[2], the north-star target): bf16 GEMM
@@ -453,7 +453,7 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--n", type=int, default=32768)
+    ap.add_argument("--size", dest="n", type=int, default=32768)
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--gemm-max-ctas", type=int, default=0)
     ap.add_argument("--pipeline-chunks", type=int, default=0)
