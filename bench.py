@@ -160,11 +160,8 @@ def allreduce_sum(dist, x):
 # ------------------------------------------------------------------ reference arm
 
 def cpu_threads():
-    n = os.cpu_count() or 1
-    p = 1
-    while p * 2 <= min(n, 64):
-        p *= 2
-    return p
+    """All host cores (one reference worker thread each), capped at 64."""
+    return max(1, min(os.cpu_count() or 1, 64))
 
 
 def reference_sample(budget_s):

@@ -171,7 +171,9 @@ __global__ void fill_uniform_kernel(void* __restrict__ dst, int prec, uint64_t l
     const uint64_t draw = (r0 + r) * full_cols + (c0 + c);
     const uint64_t x = avalanche64(seed + (draw + 1) * 0x9E3779B97F4A7C15ull);
     const double u = static_cast<double>(x >> 11) * 0x1.0p-53;
-    store_elem(dst, prec, r * ld + c, lo + (hi - lo) * u);
+    // Separate multiply and add (no FMA contraction), exactly like the
+    // reference's nextUniform built without -march.
+    store_elem(dst, prec, r * ld + c, __dadd_rn(lo, __dmul_rn(hi - lo, u)));
   }
 }
 

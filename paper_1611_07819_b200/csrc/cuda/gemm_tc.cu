@@ -63,8 +63,10 @@ struct TcCfg {
   static constexpr uint32_t kBytesB = kBytesBChunk * kChunks;
   static constexpr uint32_t kParts = kSplit ? 2 : 1;               // hi (+ lo)
   static constexpr uint32_t kStageBytes = kParts * (kBytesA + kBytesB);
-  static constexpr uint32_t kStages = (196u * 1024u) / kStageBytes;
-  static constexpr uint32_t kSmemBytes = kStages * kStageBytes + 1024 + 256;
+  static constexpr uint32_t kStages = (192u * 1024u) / kStageBytes;
+  // Epilogue staging for TMA stores: 4 warps x 2 buffers x (32 rows x 128 B).
+  static constexpr uint32_t kStagingBytes = 4u * 2u * 4096u;
+  static constexpr uint32_t kSmemBytes = kStages * kStageBytes + kStagingBytes + 1024 + 256;
   static constexpr uint32_t kClusterCtas = kCG * kPairs;
   static_assert(kAccStages * kChunks * kMmaN <= 512, "TMEM columns");
   static_assert(kPairs == 1 || kCG == 2, "A multicast across pairs needs 2-SM pairs");
@@ -84,6 +86,7 @@ struct TcParams {
   uint32_t hint_a, hint_b;              // L2 policy for A / B loads (0 normal, 1 evict_last, 2 evict_first)
   uint32_t* sync_ctr;                   // lockstep counter (zeroed per launch) or null
   uint32_t sync_every;                  // k-blocks per lockstep checkpoint
+  uint32_t tma_store;                   // C written by TMA stores (beta == 0, aligned C)
 };
 
 // Lockstep: persistent CTA pairs run ~100 tiles back to back and drift apart,
@@ -189,7 +192,8 @@ template <int kCG, int kElemBytes, int kSplit, int kChunks, int kPairs>
 __global__ void __launch_bounds__(kNumThreads, 1)
     tc_gemm_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid_constant__ CUtensorMap tm_b,
                    const __grid_constant__ CUtensorMap tm_a_lo,
-                   const __grid_constant__ CUtensorMap tm_b_lo, const TcParams p) {
+                   const __grid_constant__ CUtensorMap tm_b_lo,
+                   const __grid_constant__ CUtensorMap tm_c, const TcParams p) {
   using Cfg = TcCfg<kCG, kElemBytes, kSplit, kChunks, kPairs>;
   constexpr uint32_t kStages = Cfg::kStages;
   constexpr uint32_t kBlockK = Cfg::kBlockK;
@@ -200,7 +204,8 @@ __global__ void __launch_bounds__(kNumThreads, 1)
 
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + kStages * Cfg::kStageBytes);
+  uint8_t* staging = smem + kStages * Cfg::kStageBytes;  // 1024-aligned (stage bytes are KB multiples)
+  uint64_t* full_bar = reinterpret_cast<uint64_t*>(staging + Cfg::kStagingBytes);
   uint64_t* empty_bar = full_bar + kStages;
   uint64_t* tfull_bar = empty_bar + kStages;  // [kAcc]
   uint64_t* tempty_bar = tfull_bar + 2;       // [kAcc]
@@ -218,6 +223,7 @@ __global__ void __launch_bounds__(kNumThreads, 1)
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tm_a);
     tma_prefetch_desc(&tm_b);
+    if (p.tma_store) tma_prefetch_desc(&tm_c);
     if (kSplit) {
       tma_prefetch_desc(&tm_a_lo);
       tma_prefetch_desc(&tm_b_lo);
@@ -391,34 +397,100 @@ __global__ void __launch_bounds__(kNumThreads, 1)
   } else {
     // ------------------------------------------------------------ epilogue
     const uint32_t lane_grp = warp & 3;  // TMEM lanes [32*lane_grp, +32)
-    uint32_t acc = 0, acc_phase = 0;
+    const uint32_t ew = warp - 2;        // epilogue warp 0..3
+    uint8_t* stg = staging + ew * 2 * 4096;
+    const uint32_t cbytes = p.c_dtype == 2 ? 4 : 2;
+    uint32_t acc = 0, acc_phase = 0, iter = 0;
     for (uint32_t t = unit; t < num_tiles; t += num_units) {
       uint32_t mb, nbu;
       tile_coords(t, p, num_nbu, mb, nbu);
       const uint32_t nb = nbu * kPairs + pair;
       mbar_wait(&tfull_bar[acc], acc_phase);
       tc_fence_after();
-      const uint32_t row = mb * kBlockMcta * kCG + rank * kBlockMcta + lane_grp * 32 + lane;
+      const uint32_t row0 = mb * kBlockMcta * kCG + rank * kBlockMcta + lane_grp * 32;
+      const uint32_t row = row0 + lane;
       const uint32_t taddr = tmem_base + ((lane_grp * 32) << 16) + acc * kChunks * kMmaN;
+      if (p.tma_store) {
+        // TMEM -> registers -> swizzled smem (32 x 32 chunk) -> TMA store.
+        // The chunk buffer is reused two chunks later, after its store has
+        // finished reading shared memory.
 #pragma unroll 1
-      for (uint32_t c = 0; c < Cfg::kBlockN; c += 32) {
-        uint32_t v[32];
+        for (uint32_t c = 0; c < Cfg::kBlockN; c += 32, ++iter) {
+          uint32_t v[32];
+          __syncwarp();
+          tmem_ld_32x32b_x32(taddr + c, v);
+          tmem_wait_ld();
+          if (c + 32 == Cfg::kBlockN) {
+            // Accumulator fully read: release TMEM before the last stores.
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) {
+              if (kCG == 2 && !leader) mbar_arrive_cluster(&tempty_bar[acc], pair * kCG);
+              else mbar_arrive(&tempty_bar[acc]);
+            }
+          }
+          uint8_t* buf = stg + (iter & 1) * 4096;
+          if (lane == 0 && iter >= 2) bulk_wait_read<1>();
+          __syncwarp();
+          if (cbytes == 2) {
+            // 32 x 64 B rows, 64-byte swizzle: chunk j of row r at (j ^ ((r >> 1) & 3)).
+            uint32_t packed[16];
+#pragma unroll
+            for (int i = 0; i < 16; ++i) {
+              const float x0 = p.alpha * __uint_as_float(v[2 * i]), x1 = p.alpha * __uint_as_float(v[2 * i + 1]);
+              if (p.c_dtype == 1) {
+                __nv_bfloat162 h = __floats2bfloat162_rn(x0, x1);
+                packed[i] = *reinterpret_cast<uint32_t*>(&h);
+              } else {
+                __half2 h = __floats2half2_rn(x0, x1);
+                packed[i] = *reinterpret_cast<uint32_t*>(&h);
+              }
+            }
+#pragma unroll
+            for (uint32_t j = 0; j < 4; ++j) {
+              const uint32_t pj = j ^ ((lane >> 1) & 3);
+              *reinterpret_cast<uint4*>(buf + lane * 64 + pj * 16) =
+                  make_uint4(packed[4 * j], packed[4 * j + 1], packed[4 * j + 2], packed[4 * j + 3]);
+            }
+          } else {
+            // 32 x 128 B rows, 128-byte swizzle: chunk j of row r at (j ^ (r & 7)).
+#pragma unroll
+            for (uint32_t j = 0; j < 8; ++j) {
+              const uint32_t pj = j ^ (lane & 7);
+              *reinterpret_cast<float4*>(buf + lane * 128 + pj * 16) =
+                  make_float4(p.alpha * __uint_as_float(v[4 * j]), p.alpha * __uint_as_float(v[4 * j + 1]),
+                              p.alpha * __uint_as_float(v[4 * j + 2]), p.alpha * __uint_as_float(v[4 * j + 3]));
+            }
+          }
+          fence_proxy_async_smem();
+          __syncwarp();
+          if (lane == 0) {
+            tma_store_2d(&tm_c, buf, static_cast<int32_t>(nb * Cfg::kBlockN + c), static_cast<int32_t>(row0));
+            bulk_commit();
+          }
+        }
+      } else {
+#pragma unroll 1
+        for (uint32_t c = 0; c < Cfg::kBlockN; c += 32) {
+          uint32_t v[32];
+          __syncwarp();
+          tmem_ld_32x32b_x32(taddr + c, v);
+          tmem_wait_ld();
+          store_row32(p, row, nb * Cfg::kBlockN + c, v);
+        }
+        tc_fence_before();
         __syncwarp();
-        tmem_ld_32x32b_x32(taddr + c, v);
-        tmem_wait_ld();
-        store_row32(p, row, nb * Cfg::kBlockN + c, v);
-      }
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) {
-        if (kCG == 2 && !leader) mbar_arrive_cluster(&tempty_bar[acc], pair * kCG);
-        else mbar_arrive(&tempty_bar[acc]);
+        if (lane == 0) {
+          if (kCG == 2 && !leader) mbar_arrive_cluster(&tempty_bar[acc], pair * kCG);
+          else mbar_arrive(&tempty_bar[acc]);
+        }
       }
       if (++acc == kAcc) {
         acc = 0;
         acc_phase ^= 1;
       }
     }
+    if (p.tma_store && lane == 0) bulk_wait<0>();  // stores complete before smem goes away
   }
 
   __syncwarp();
@@ -453,7 +525,8 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 
 int make_map_2d(CUtensorMap* map, const void* ptr, CUtensorMapDataType dt, uint32_t esize,
                 uint64_t inner, uint64_t outer, uint64_t pitch_elems, uint32_t box_inner,
-                uint32_t box_outer, const char** err) {
+                uint32_t box_outer, const char** err,
+                CUtensorMapSwizzle swizzle = CU_TENSOR_MAP_SWIZZLE_128B) {
   auto fn = encode_fn();
   if (!fn) {
     *err = "cuTensorMapEncodeTiled unavailable";
@@ -472,7 +545,7 @@ int make_map_2d(CUtensorMap* map, const void* ptr, CUtensorMapDataType dt, uint3
                                     : promo == 128 ? CU_TENSOR_MAP_L2_PROMOTION_L2_128B
                                                    : CU_TENSOR_MAP_L2_PROMOTION_L2_256B;
   CUresult r = fn(map, dt, 2, const_cast<void*>(ptr), dims, strides, box, estr,
-                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, pr,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, swizzle, pr,
                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) {
     *err = "cuTensorMapEncodeTiled failed (alignment or stride)";
@@ -578,7 +651,20 @@ int launch(const TcOperand& a, const TcOperand& b, const TcOperand* a_lo, const 
     std::fprintf(stderr, "[gm] tc_gemm cg=%d elem=%d split=%d chunks=%d pairs=%d m=%u n=%u k=%u grid=%d resident=%d stages=%u smem=%u\n",
                  kCG, kElemBytes, kSplit, kChunks, kPairs, p.m, p.n, p.k, ctas, dev < 64 ? resident[dev] : -1,
                  Cfg::kStages, Cfg::kSmemBytes);
-  cudaError_t e = cudaLaunchKernelEx(&cfg, kern, ma, mb, mal, mbl, p);
+  CUtensorMap mc = ma;
+  {
+    const uint32_t cb = p.c_dtype == 2 ? 4 : 2;
+    p.tma_store = 0;
+    static const bool no_tma_store = std::getenv("GM_NO_TMA_STORE") != nullptr;
+    if (!no_tma_store && p.beta == 0.0f && (reinterpret_cast<uintptr_t>(p.c) % 16) == 0 && (p.ldc * cb) % 16 == 0) {
+      const char* e2 = nullptr;
+      if (make_map_2d(&mc, p.c, cb == 4 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_UINT16, cb, p.n,
+                      p.m, p.ldc, 32, 32, &e2,
+                      cb == 4 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B) == 0)
+        p.tma_store = 1;
+    }
+  }
+  cudaError_t e = cudaLaunchKernelEx(&cfg, kern, ma, mb, mal, mbl, mc, p);
   count_launch();
   if (e != cudaSuccess) {
     *err = cudaGetErrorString(e);
