@@ -437,7 +437,13 @@ DistMatrix Session::createMatrix(std::uint64_t rows, std::uint64_t cols, Precisi
   try {
     execCreate(op);
   } catch (...) {
+    // Roll back like the reference (session.cpp:208-216): a DestroyMatrix op
+    // removes the descriptor everywhere and frees whatever was allocated.
     try {
+      OpDescriptor rb;
+      rb.opcode = OpCode::DestroyMatrix;
+      rb.ids[0] = d.matrixId;
+      issue(rb);
       execDestroy(d.matrixId);
     } catch (...) {
     }

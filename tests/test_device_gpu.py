@@ -117,3 +117,22 @@ def test_get_data_roundtrip_all_layouts():
             s.setData(M, img.astype(np.float64) * 2)
             assert np.array_equal(s.getData(M), (img * 2).astype(np.float64))
             s.destroy(M)
+
+
+def test_worker_errors_aggregate_and_session_survives():
+    # Reference behaviour: worker failures become one Error ("op failed: worker r: ...",
+    # session.cpp:149-154); createMatrix rolls back (session.cpp:208-216).
+    with G.Session(workers=2) as s:
+        huge = 1 << 22  # 2^22 x 2^22 doubles = 128 TiB
+        with pytest.raises(G.GmError, match="op failed: worker"):
+            s.createMatrix(huge, huge, G.Precision.Double, G.makeRowBlockLayout(huge, huge, [0, 1]))
+        M = s.createMatrix(64, 64, G.Precision.Single, G.makeRowBlockLayout(64, 64, [0, 1]))
+        s.fillUniform(M, 1)
+        assert s.getDataRaw(M).shape == (64, 64)
+        s.verifyMetadataConsistency()
+        s.destroy(M)
+        with pytest.raises(G.GmError, match="unknown matrix id"):
+            s.getDataRaw(M)
+        with pytest.raises(G.GmError):
+            s.setDataRaw(s.createMatrix(4, 4, G.Precision.Single, G.makeSingleTileLayout(4, 4, 0)),
+                         np.zeros(3, dtype=np.float32))
