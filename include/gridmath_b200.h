@@ -229,6 +229,11 @@ int gm_matrix_get_local_raw(gm_session* s, uint64_t id, void* host, uint64_t byt
 int gm_matrix_local_bytes(gm_session* s, uint64_t id, uint64_t* bytes);
 int gm_matrix_set_local_packed(gm_session* s, uint64_t id, const void* host, uint64_t bytes);
 int gm_matrix_get_local_packed(gm_session* s, uint64_t id, void* host, uint64_t bytes);
+/* Redistribution (reference Session::reshape, session.cpp:310-325): new
+ * layout and/or storage precision (new_prec < 0 keeps it); version + 1,
+ * replicas reset; values converted like convertBuffer. */
+int gm_matrix_reshape(gm_session* s, uint64_t id, const gm_tile* tiles, uint32_t ntiles,
+                      int32_t new_prec);
 int gm_matrix_info(gm_session* s, uint64_t id, uint64_t* rows, uint64_t* cols, int32_t* prec,
                    uint64_t* version, uint64_t* replicated_version);
 

@@ -160,6 +160,14 @@ int gm_matrix_get_local_packed(gm_session* s, uint64_t id, void* host, uint64_t 
   return guard([&] { s->s->getLocalPacked(handle(s, id), host, bytes); });
 }
 
+int gm_matrix_reshape(gm_session* s, uint64_t id, const gm_tile* tiles, uint32_t ntiles, int32_t new_prec) {
+  return guard([&] {
+    std::optional<gridmath::Precision> p;
+    if (new_prec >= 0) p = gridmath::precisionFromTag(static_cast<uint8_t>(new_prec));
+    s->s->reshape(handle(s, id), toLayout(tiles, ntiles), p);
+  });
+}
+
 int gm_matrix_info(gm_session* s, uint64_t id, uint64_t* rows, uint64_t* cols, int32_t* prec,
                    uint64_t* version, uint64_t* replicated_version) {
   return guard([&] {

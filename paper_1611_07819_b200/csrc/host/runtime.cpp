@@ -83,6 +83,15 @@ void validateOp(const DescriptorTable& t, const OpDescriptor& op, std::uint32_t 
     case OpCode::ReplicateStart:
       (void)lookup(t, op.ids[0]);
       return;
+    case OpCode::Reshape: {
+      const MatrixDescriptor& old = lookup(t, op.ids[0]);
+      WireReader r(op.blob);
+      const MatrixDescriptor d = decodeDescriptor(r);
+      if (d.rows != old.rows || d.cols != old.cols) throw Error("reshape: shape must be preserved");
+      const LayoutReport rep = validateLayout(d.rows, d.cols, d.layout, workers);
+      if (!rep.ok()) throw Error("reshape: invalid layout: " + rep.detail);
+      return;
+    }
     case OpCode::Gemm: {
       const MatrixDescriptor& a = lookup(t, op.ids[0]);
       const MatrixDescriptor& b = lookup(t, op.ids[1]);
@@ -640,6 +649,125 @@ std::vector<double> Session::getData(DistMatrix m) {
   convertBuffer(raw.data(), d.precision, reinterpret_cast<std::uint8_t*>(out.data()),
                 Precision::Double, out.size());
   return out;
+}
+
+// ---------------------------------------------------------------- reshape
+
+void Session::reshape(DistMatrix m, const Layout& newLayout, std::optional<Precision> newPrecision) {
+  const MatrixDescriptor old = descriptor(m.id());  // copy: the table entry is replaced below
+  MatrixDescriptor nd = old;
+  nd.layout = newLayout;
+  nd.precision = newPrecision.value_or(old.precision);
+  nd.version = old.version + 1;
+  nd.replicatedVersion = ~0ull;
+  OpDescriptor op;
+  op.opcode = OpCode::Reshape;
+  op.ids[0] = m.id();
+  WireWriter ww;
+  encodeDescriptor(nd, ww);
+  op.blob = ww.take();
+  op.execId = nextExec_;
+  validateOp(table_, op, opts_.workers);
+
+  const std::uint64_t oldEb = bytesOf(old.precision), newEb = bytesOf(nd.precision);
+  const bool convert = old.precision != nd.precision;
+  const bool viaReplica = old.replicaFresh();
+  struct NewTile {
+    Worker* w;
+    DeviceTile tile;
+    void* staging;  // old-precision assembly buffer (dense), when converting
+  };
+  std::vector<NewTile> made;
+  std::vector<Xfer> xfers;
+  try {
+    for (const auto& t : nd.layout.tiles) {
+      const TileExtent& e = t.first;
+      Worker* w = local(t.second.rank);
+      NewTile ntile{w, {}, nullptr};
+      if (w) {
+        w->activate();
+        ntile.tile.extent = e;
+        ntile.tile.ld = paddedLd(e.colCount, newEb);
+        ntile.tile.ptr = w->arena.alloc(e.rowCount * ntile.tile.ld * newEb, w->compute);
+        if (convert) ntile.staging = w->arena.alloc(e.elements() * oldEb, w->compute);
+      }
+      // Destination of the old-precision bytes for this tile.
+      void* dst = w ? (convert ? ntile.staging : ntile.tile.ptr) : nullptr;
+      const std::uint64_t dstLd = convert ? e.colCount : ntile.tile.ld;
+      if (viaReplica) {
+        if (w) {
+          auto it = w->replicas.find(old.matrixId);
+          if (it == w->replicas.end() || it->second.version != old.version)
+            throw Error("reshape: replica of matrix " + std::to_string(old.matrixId) + " missing");
+          cudaCheck(cudaStreamWaitEvent(w->compute, it->second.ready, 0), "reshape: wait replica");
+          cudaCheck(cudaMemcpy2DAsync(dst, dstLd * oldEb,
+                                      static_cast<const std::uint8_t*>(it->second.full) +
+                                          (e.rowStart * it->second.ld + e.colStart) * oldEb,
+                                      it->second.ld * oldEb, e.colCount * oldEb, e.rowCount,
+                                      cudaMemcpyDeviceToDevice, w->compute),
+                    "reshape: from replica");
+        }
+      } else {
+        for (const auto& ot : old.layout.tiles) {
+          auto piece = intersectRect(Rect::ofExtent(e), Rect::ofExtent(ot.first));
+          if (!piece) continue;
+          Worker* sw = local(ot.second.rank);
+          if (!w && !sw) continue;
+          Xfer x;
+          x.src = ot.second.rank;
+          x.dst = t.second.rank;
+          x.rows = piece->rows();
+          x.cols = piece->cols();
+          x.eb = static_cast<std::uint32_t>(oldEb);
+          if (sw)
+            for (const DeviceTile& dt : sw->tiles.at(old.matrixId))
+              if (dt.extent == ot.first) {
+                x.srcPtr = static_cast<const std::uint8_t*>(dt.ptr) +
+                           ((piece->r0 - dt.extent.rowStart) * dt.ld + (piece->c0 - dt.extent.colStart)) * oldEb;
+                x.srcLd = dt.ld;
+              }
+          if (w) {
+            x.dstPtr = static_cast<std::uint8_t*>(dst) + ((piece->r0 - e.rowStart) * dstLd + (piece->c0 - e.colStart)) * oldEb;
+            x.dstLd = dstLd;
+          }
+          xfers.push_back(x);
+        }
+      }
+      if (w) made.push_back(ntile);
+    }
+    exchange(xfers, false);
+    for (NewTile& nt : made) {
+      if (!convert) continue;
+      nt.w->activate();
+      const TileExtent& e = nt.tile.extent;
+      cudaCheck(gmk::convert_rect(nt.staging, static_cast<int>(old.precision), e.colCount, nt.tile.ptr,
+                                  static_cast<int>(nd.precision), nt.tile.ld, e.rowCount, e.colCount, nt.w->compute),
+                "reshape: convert");
+      nt.w->arena.free(nt.staging, nt.w->compute);
+      nt.staging = nullptr;
+    }
+  } catch (...) {
+    for (NewTile& nt : made) {
+      if (nt.tile.ptr) nt.w->arena.free(nt.tile.ptr, nt.w->compute);
+      if (nt.staging) nt.w->arena.free(nt.staging, nt.w->compute);
+    }
+    throw;
+  }
+  // Metadata swap (version bump, replicas and cached panels of the old
+  // version die, WAR waits for the pieces just read), then retire old tiles.
+  issue(op);
+  forEachLocal([&](Worker& w) {
+    for (DeviceTile& t : w.tiles[old.matrixId]) w.arena.free(t.ptr, w.compute);
+    std::vector<DeviceTile> mine;
+    for (NewTile& nt : made)
+      if (nt.w == &w) mine.push_back(nt.tile);
+    w.tiles[old.matrixId] = std::move(mine);
+    w.residentBytes = 0;
+    for (auto& kv : w.tiles) {
+      const std::uint64_t eb = bytesOf(lookup(w.descs, kv.first).precision);
+      for (auto& t : kv.second) w.residentBytes += t.extent.elements() * eb;
+    }
+  });
 }
 
 // ---------------------------------------------------------------- data plane

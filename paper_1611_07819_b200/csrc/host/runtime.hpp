@@ -26,6 +26,7 @@
 #include <list>
 #include <map>
 #include <memory>
+#include <optional>
 #include <set>
 #include <string>
 #include <utility>
@@ -237,6 +238,9 @@ class Session {
   std::vector<double> getData(DistMatrix m);
   std::vector<std::uint8_t> getDataRaw(DistMatrix m);
   void getDataRawInto(DistMatrix m, void* image, std::uint64_t bytes, bool localOnly);
+  // Redistribution (reference Session::reshape, session.cpp:310-325, and
+  // execReshape, kernels.cpp:1083-1127): new layout and/or storage precision.
+  void reshape(DistMatrix m, const Layout& newLayout, std::optional<Precision> newPrecision = std::nullopt);
 
   ReplicationHandle replicateAsync(DistMatrix m);
   void replicateSync(DistMatrix m);

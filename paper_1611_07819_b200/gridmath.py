@@ -251,6 +251,11 @@ class Session:
             return (raw.astype(np.uint32) << 16).view(np.float32).astype(np.float64)
         return raw.astype(np.float64)
 
+    def reshape(self, m: DistMatrix, layout: Layout, prec: Optional[Precision] = None):
+        """Redistribute to `layout` (and storage `prec`); reference Session::reshape."""
+        check(_lib.load().gm_matrix_reshape(self._h, m.id, layout.as_c(), len(layout.tiles),
+                                            -1 if prec is None else int(prec)))
+
     # --- replication -------------------------------------------------------------
     def replicateAsync(self, m: DistMatrix) -> ReplicationHandle:
         v = ctypes.c_uint64()

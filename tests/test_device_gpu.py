@@ -136,3 +136,37 @@ def test_worker_errors_aggregate_and_session_survives():
         with pytest.raises(G.GmError):
             s.setDataRaw(s.createMatrix(4, 4, G.Precision.Single, G.makeSingleTileLayout(4, 4, 0)),
                          np.zeros(3, dtype=np.float32))
+
+
+def test_reshape_layouts_and_precisions():
+    # reference execReshape (kernels.cpp:1083-1127): pieces from old tiles (or
+    # the fresh replica) to the new owners, then convertBuffer to the new precision.
+    m, n, p = 150, 94, 4
+    g = G.makeWorkerGroup(p)
+    img = O.fill_uniform(m, n, 1, 77, -3.0, 3.0)
+    with G.Session(workers=p) as s:
+        M = s.createMatrix(m, n, G.Precision.Single, G.makeRowBlockLayout(m, n, g))
+        s.setDataRaw(M, img)
+        v0 = M.version()
+        s.reshape(M, G.makeColBlockLayout(m, n, g), G.Precision.Half)
+        assert M.version() == v0 + 1 and M.precision() == G.Precision.Half
+        want_h = _to_prec(img.astype(np.float64).ravel(), 0).reshape(m, n)  # Single -> Half (RNE)
+        assert np.array_equal(s.getDataRaw(M).view(np.uint16), want_h)
+        s.reshape(M, G.makeGridLayout(m, n, 2, 2, g), G.Precision.Single)
+        back = s.getDataRaw(M)
+        assert np.array_equal(back, want_h.view(np.float16).astype(np.float32))
+        # via the replica path, then a gemm on the reshaped operand
+        h = s.replicateAsync(M)
+        assert s.wait(h) == G.ReplState.Done
+        s.reshape(M, G.makeSingleTileLayout(m, n, 3), G.Precision.BF16)
+        assert M.info()[4] == 2 ** 64 - 1  # replicatedVersion reset with the new descriptor
+        want_b = _to_prec(back.astype(np.float64).ravel(), 3).reshape(m, n)
+        assert np.array_equal(s.getDataRaw(M).view(np.uint16), want_b)
+        B = s.createMatrix(n, 64, G.Precision.BF16, G.makeRowBlockLayout(n, 64, g))
+        C = s.createMatrix(m, 64, G.Precision.Single, G.makeGridLayout(m, 64, 2, 2, g))
+        s.fillUniform(B, 5)
+        G.gemm(s, M, B, C, 1.0, 0.0)
+        b = s.getDataRaw(B)
+        got = s.getDataRaw(C)
+    want = O.gemm_c(m, 64, n, want_b, 3, b, 3, np.zeros((m, 64), np.float32), 1, 1.0, 0.0, 0, 0)
+    assert O.rel_fro(got, want) <= 1e-5

@@ -76,6 +76,20 @@ with G.Session(workers=world, spmd_rank=rank, devices=[local], nccl_id=obj[0], p
     if rank == 0:
         print(f"[rank0] replication: rel_fro={e:.3e} repl_bytes={recv_repl} expect={expect} gemm_bytes={st2['bytes_received']-st1['bytes_received']}", flush=True)
     ok = ok and good
+    # reshape across ranks: grid -> row-block, Single -> BF16, then back
+    R = s.createMatrix(1000, 776, G.Precision.Single, G.makeGridLayout(1000, 776, pr, pc, g))
+    s.fillUniform(R, 9)
+    r0 = s.getDataRaw(R)
+    s.reshape(R, G.makeRowBlockLayout(1000, 776, g), G.Precision.BF16)
+    r1 = s.getDataRaw(R)
+    u = r0.view(np.uint32).astype(np.uint64)
+    want = ((u + 0x7FFF + ((u >> 16) & 1)) >> 16).astype(np.uint16)
+    s.reshape(R, G.makeColBlockLayout(1000, 776, g), G.Precision.Single)
+    r2 = s.getDataRaw(R)
+    good = np.array_equal(r1.view(np.uint16), want) and np.array_equal(r2, (want.astype(np.uint32) << 16).view(np.float32))
+    if rank == 0:
+        print(f"[rank0] reshape grid->row/bf16->col/f32 ok={good}", flush=True)
+    ok = ok and good
 t = torch.tensor([1 if ok else 0], device="cuda")
 dist.all_reduce(t, op=dist.ReduceOp.MIN)
 if rank == 0:
