@@ -270,6 +270,9 @@ int gm_session_local_workers(gm_session* s, uint32_t* ranks, uint32_t cap, uint3
 int gm_last_op_device_ms(gm_session* s, float* ms, uint32_t cap, uint32_t* n);
 /* Same, restricted to the local GEMM kernels of the last gemm (no exchange). */
 int gm_last_op_kernel_ms(gm_session* s, float* ms, uint32_t cap, uint32_t* n);
+/* Duration of the last gemm's panel exchange on each local worker's comm
+ * stream (0 when nothing moved). */
+int gm_last_op_comm_ms(gm_session* s, float* ms, uint32_t cap, uint32_t* n);
 
 /* Device timer over everything enqueued on the local workers' compute
  * streams between start and stop (CUDA events on those streams). stop

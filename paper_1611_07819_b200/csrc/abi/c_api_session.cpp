@@ -334,6 +334,14 @@ int gm_last_op_kernel_ms(gm_session* s, float* ms, uint32_t cap, uint32_t* n) {
   });
 }
 
+int gm_last_op_comm_ms(gm_session* s, float* ms, uint32_t cap, uint32_t* n) {
+  return guard([&] {
+    const auto v = s->s->lastOpCommMs();
+    *n = static_cast<uint32_t>(v.size());
+    for (uint32_t i = 0; i < v.size() && i < cap; ++i) ms[i] = v[i];
+  });
+}
+
 int gm_timer_start(gm_session* s) {
   return guard([&] { s->s->timerStart(); });
 }

@@ -50,8 +50,11 @@ void* DeviceArena::alloc(std::uint64_t bytes, cudaStream_t stream) {
   std::lock_guard<std::mutex> lock(mu_);
   auto& list = free_[cls];
   if (!list.empty()) {
-    Block b = list.back();
-    list.pop_back();
+    // FIFO: the block released longest ago (its release event has most
+    // likely completed), so back-to-back ops alternate between buffers
+    // instead of waiting for the previous op to finish with the newest one.
+    Block b = list.front();
+    list.erase(list.begin());
     if (b.released) {
       cudaCheck(cudaStreamWaitEvent(stream, b.released, 0), "arena: wait on release");
       eventPool_.push_back(b.released);

@@ -207,6 +207,8 @@ Worker::Worker(std::uint32_t r, int dev, std::uint64_t budget)
   cudaCheck(cudaEventCreate(&uStart), "worker: event");
   cudaCheck(cudaEventCreate(&uEnd), "worker: event");
   cudaCheck(cudaEventCreate(&kStart), "worker: event");
+  cudaCheck(cudaEventCreate(&cStart), "worker: event");
+  cudaCheck(cudaEventCreate(&cEnd), "worker: event");
 }
 
 Worker::~Worker() {
@@ -225,6 +227,8 @@ Worker::~Worker() {
   cudaEventDestroy(uStart);
   cudaEventDestroy(uEnd);
   cudaEventDestroy(kStart);
+  cudaEventDestroy(cStart);
+  cudaEventDestroy(cEnd);
   cudaStreamDestroy(compute);
   cudaStreamDestroy(comm);
 }
@@ -1040,6 +1044,7 @@ void Session::execGemm(const OpDescriptor& op) {
   std::vector<std::vector<Xfer>> groups(1 + S);
   std::vector<CacheEntry*> freshEntries;
   std::vector<Worker*> freshOwners;
+  std::vector<std::pair<Worker*, void*>> temps;  // uncached bands, freed after this op's GEMMs
 
   // m-chunk j of the interval [lo, hi): [lo + j*len/S, lo + (j+1)*len/S).
   auto chunkRange = [&](std::uint64_t lo, std::uint64_t hi, std::uint32_t j) {
@@ -1091,24 +1096,31 @@ void Session::execGemm(const OpDescriptor& op) {
         e.ld = paddedLd(nd.rect.cols(), eb);
         e.bytes = nd.rect.rows() * e.ld * eb;
         e.lastUse = tick_;
-        // Allocate before evicting so back-to-back ops double-buffer their
-        // bands (the next op's gather does not wait for this op's GEMM).
+        const std::uint64_t budget = w ? w->cacheBudget : localRef->cacheBudget;
+        // A band larger than the whole budget is not kept (same decision on
+        // every rank): it lives for this op only.
+        const bool keep = e.bytes <= budget;
         if (w) {
           w->activate();
           e.ptr = w->arena.alloc(e.bytes, w->comm);
         }
-        const std::uint64_t budget = w ? w->cacheBudget : localRef->cacheBudget;
-        for (CacheEntry& ev : dir.reserve(e.bytes, budget, tick_))
-          if (w && ev.ptr) {
-            w->arena.free(ev.ptr, w->compute);
-            w->recycle(ev.ready);
+        CacheEntry* slotp = nullptr;
+        if (keep) {
+          for (CacheEntry& ev : dir.reserve(e.bytes, budget, tick_))
+            if (w && ev.ptr) {
+              w->arena.free(ev.ptr, w->compute);
+              w->recycle(ev.ready);
+            }
+          slotp = &dir.insert(e);
+          if (w) {
+            freshEntries.push_back(slotp);
+            freshOwners.push_back(w);
           }
-        CacheEntry& slot = dir.insert(e);
-        if (w) {
-          freshEntries.push_back(&slot);
-          freshOwners.push_back(w);
-          view = {slot.ptr, slot.ld};
+        } else if (w) {
+          temps.push_back({w, e.ptr});
         }
+        const CacheEntry& slot = keep ? *slotp : e;
+        if (w) view = {slot.ptr, slot.ld};
         // Which group each piece belongs to: B whole; A split by m rows
         // (stored rows for A, stored columns for transposed A).
         for (const PieceRoute& pr : nd.pieces) {
@@ -1162,6 +1174,19 @@ void Session::execGemm(const OpDescriptor& op) {
 
   // Comm stream: B bands, then A chunks; an event per group per local worker.
   std::vector<std::vector<cudaEvent_t>> groupDone(1 + S);
+  bool anyXfer = false;
+  for (auto& gx : groups) anyXfer = anyXfer || !gx.empty();
+  forEachLocal([&](Worker& w) {
+    w.commTimed = anyXfer;
+    if (anyXfer) {
+      // The exchange starts once the comm stream has the producers' writes.
+      cudaEvent_t e = w.event();
+      cudaCheck(cudaEventRecord(e, w.compute), "gemm: timing");
+      cudaCheck(cudaStreamWaitEvent(w.comm, e, 0), "gemm: timing");
+      w.recycle(e);
+      cudaCheck(cudaEventRecord(w.cStart, w.comm), "gemm: comm timing");
+    }
+  });
   for (std::uint32_t gi = 0; gi <= S; ++gi) {
     if (groups[gi].empty()) continue;
     exchange(groups[gi], true);
@@ -1173,6 +1198,9 @@ void Session::execGemm(const OpDescriptor& op) {
       groupDone[gi].push_back(ev);
     }
   }
+  forEachLocal([&](Worker& w) {
+    if (w.commTimed) cudaCheck(cudaEventRecord(w.cEnd, w.comm), "gemm: comm timing");
+  });
   // Gathered bands become cache entries ready when the last group lands.
   for (std::size_t i = 0; i < freshEntries.size(); ++i) {
     Worker* w = freshOwners[i];
@@ -1249,6 +1277,10 @@ void Session::execGemm(const OpDescriptor& op) {
     }
     cudaCheck(cudaEventRecord(w.tEnd, w.compute), "gemm: timing");
   });
+  for (auto& tp : temps) {
+    tp.first->activate();
+    tp.first->arena.free(tp.second, tp.first->compute);
+  }
   // Group events go back to their pools (waits are already enqueued).
   for (auto& evs : groupDone) {
     std::size_t idx = 0;
@@ -1287,6 +1319,19 @@ std::vector<float> Session::lastOpKernelMs() {
     if (w.timed) {
       cudaCheck(cudaEventSynchronize(w.tEnd), "timing sync");
       cudaCheck(cudaEventElapsedTime(&ms, w.kStart, w.tEnd), "timing");
+    }
+    out.push_back(ms);
+  });
+  return out;
+}
+
+std::vector<float> Session::lastOpCommMs() {
+  std::vector<float> out;
+  forEachLocal([&](Worker& w) {
+    float ms = 0.0f;
+    if (w.commTimed) {
+      cudaCheck(cudaEventSynchronize(w.cEnd), "timing sync");
+      cudaCheck(cudaEventElapsedTime(&ms, w.cStart, w.cEnd), "timing");
     }
     out.push_back(ms);
   });

@@ -172,6 +172,8 @@ class Worker {
   std::uint64_t residentBytes = 0, bytesSent = 0, bytesReceived = 0;
   cudaEvent_t tStart = nullptr, tEnd = nullptr, uStart = nullptr, uEnd = nullptr;
   cudaEvent_t kStart = nullptr;  // compute phase of the last gemm (ends at tEnd)
+  cudaEvent_t cStart = nullptr, cEnd = nullptr;  // comm-stream exchange of the last gemm
+  bool commTimed = false;
   bool timed = false;
   ncclComm_t nccl = nullptr;
 
@@ -262,6 +264,7 @@ class Session {
   void synchronize();
   std::vector<float> lastOpDeviceMs();
   std::vector<float> lastOpKernelMs();
+  std::vector<float> lastOpCommMs();
   std::uint64_t localBytes(DistMatrix m) const;
   void setLocalPacked(DistMatrix m, const void* host, std::uint64_t bytes);
   void getLocalPacked(DistMatrix m, void* host, std::uint64_t bytes);

@@ -307,6 +307,12 @@ class Session:
         check(_lib.load().gm_last_op_kernel_ms(self._h, arr, 64, ctypes.byref(n)))
         return list(arr[: n.value])
 
+    def lastOpCommMs(self) -> List[float]:
+        arr = (ctypes.c_float * 64)()
+        n = ctypes.c_uint32()
+        check(_lib.load().gm_last_op_comm_ms(self._h, arr, 64, ctypes.byref(n)))
+        return list(arr[: n.value])
+
     def localBytes(self, m: DistMatrix) -> int:
         b = ctypes.c_uint64()
         check(_lib.load().gm_matrix_local_bytes(self._h, m.id, ctypes.byref(b)))

@@ -126,3 +126,33 @@ def test_destroy_frees_and_reuses():
         st = s.queryWorkerStats()
         assert all(r["reuses"] >= 4 for r in st)
         assert all(r["resident_bytes"] == 0 for r in st)
+
+
+def test_panel_cache_off_moves_panels_every_op():
+    # Budget smaller than a band: nothing is kept, every GEMM re-gathers its
+    # panels (what the benchmark measures); with the default budget the
+    # second identical GEMM hits the cache and moves nothing.
+    n, p = 512, 4
+    g = G.makeWorkerGroup(p)
+    moved = {}
+    for budget in (1, 0):
+        with G.Session(workers=p, panel_cache_bytes=budget) as s:
+            lay = G.makeGridLayout(n, n, 2, 2, g)
+            A = s.createMatrix(n, n, G.Precision.BF16, lay)
+            B = s.createMatrix(n, n, G.Precision.BF16, lay)
+            C = s.createMatrix(n, n, G.Precision.Single, lay)
+            s.fillUniform(A, 1)
+            s.fillUniform(B, 2)
+            per_op = []
+            for _ in range(3):
+                st0 = sum(r["bytes_received"] for r in s.queryWorkerStats())
+                G.gemm(s, A, B, C, 1.0, 0.0)
+                per_op.append(sum(r["bytes_received"] for r in s.queryWorkerStats()) - st0)
+            moved[budget] = per_op
+            a, b, c = s.getDataRaw(A), s.getDataRaw(B), s.getDataRaw(C)
+        want = O.gemm_c(n, n, n, a, 3, b, 3, np.zeros((n, n), np.float32), 1, 1.0, 0.0, 0, 0)
+        assert O.rel_fro(c, want) <= 1e-5
+    # 2x2 SUMMA: each worker receives (n/2 x n/2) of A and of B per op -> 4 workers x 2 x 2 B x n^2/4
+    expect = 4 * 2 * 2 * (n // 2) * (n // 2)
+    assert moved[1] == [expect] * 3
+    assert moved[0][0] == expect and moved[0][1] == 0 and moved[0][2] == 0
