@@ -233,7 +233,8 @@ def run_ours(args):
     # on every step after the first would skip the panel exchange. Each
     # timed step must move its panels.
     s = G.Session(workers=world, spmd_rank=rank if world > 1 else -1, devices=[local], nccl_id=nccl_id,
-                  gemm_max_ctas=args.gemm_max_ctas, panel_cache_bytes=1, pipeline_chunks=args.pipeline_chunks)
+                  gemm_max_ctas=args.gemm_max_ctas, panel_cache_bytes=1, pipeline_chunks=args.pipeline_chunks,
+                  transport=args.transport)
     n = args.n
     pr, pc = grid_for(world)
     lay = G.makeGridLayout(n, n, pr, pc, G.makeWorkerGroup(world))
@@ -289,7 +290,7 @@ def run_ours(args):
         recv_max = allreduce_max(dist, float(recv))
         barrier()
         peaks, _ = measured_peaks()
-        nvlink = {"bytes_received_per_gpu": int(recv_max), "exchange_ms": round(comm_ms_max, 4),
+        nvlink = {"plane": s.transport(), "bytes_received_per_gpu": int(recv_max), "exchange_ms": round(comm_ms_max, 4),
                   "achieved_gbs": round(recv_max / (comm_ms_max / 1e3) / 1e9, 1) if comm_ms_max > 0 else None,
                   "peak_gbs": 770.0, "peak_kind": "B200_PROFILING.md measured peer copy per direction (900 nominal)",
                   "note": "isolated op (exchange not overlapped); in the timed loop the exchange overlaps the previous GEMM",
@@ -475,6 +476,7 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--gemm-max-ctas", type=int, default=0)
     ap.add_argument("--pipeline-chunks", type=int, default=0)
+    ap.add_argument("--transport", type=int, default=0, help="0 auto (IPC copy engines), 1 NCCL")
     ap.add_argument("--no-cpu-baseline", dest="cpu_baseline", action="store_false")
     ap.add_argument("--no-c2", dest="c2", action="store_false")
     ap.add_argument("--config", default="c3", choices=["c3", "fc", "fp64"])

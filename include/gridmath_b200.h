@@ -193,7 +193,7 @@ typedef struct {
   uint8_t nccl_unique_id[128];
   uint64_t arena_slab_bytes;        /* 0 = default */
   int32_t gemm_max_ctas;            /* 0 = all SMs (cap leaves SMs for NCCL) */
-  int32_t transport;                /* 0 = auto, 1 = NCCL, 2 = copy-engine peer pulls */
+  int32_t transport;                /* 0 = auto, 1 = NCCL, 2 = copy engines (IPC pulls under SPMD) */
   uint64_t panel_cache_bytes;       /* per-worker panel cache budget; 0 = 1/4 of HBM, 1 = off */
   int32_t pipeline_chunks;          /* SUMMA overlap chunks per band (0 = auto, 1 = off) */
 } gm_session_options;
@@ -265,6 +265,13 @@ typedef struct {
 int gm_query_worker_stats(gm_session* s, gm_worker_stats* rows, uint32_t cap, uint32_t* n);
 int gm_verify_metadata(gm_session* s);
 int gm_session_local_workers(gm_session* s, uint32_t* ranks, uint32_t cap, uint32_t* n);
+/* Data plane the session chose: GM_TRANSPORT_PEER_COPY (one process, peer
+ * copies), GM_TRANSPORT_NCCL, GM_TRANSPORT_IPC (one process per GPU, copy
+ * engines pulling peer tiles over CUDA IPC, ordered by device-side flags). */
+#define GM_TRANSPORT_PEER_COPY 0
+#define GM_TRANSPORT_NCCL 1
+#define GM_TRANSPORT_IPC 2
+int gm_session_transport(gm_session* s, int32_t* kind);
 /* Device time of the last gm_gemm/gm_gemm_async per local worker (ms),
  * measured with CUDA events on the worker's compute stream. */
 int gm_last_op_device_ms(gm_session* s, float* ms, uint32_t cap, uint32_t* n);

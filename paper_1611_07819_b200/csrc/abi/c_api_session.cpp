@@ -242,6 +242,10 @@ int gm_session_local_workers(gm_session* s, uint32_t* ranks, uint32_t cap, uint3
   });
 }
 
+int gm_session_transport(gm_session* s, int32_t* kind) {
+  return guard([&] { *kind = s->s->transportKind(); });
+}
+
 int gm_last_op_device_ms(gm_session* s, float* ms, uint32_t cap, uint32_t* n) {
   return guard([&] {
     const auto v = s->s->lastOpDeviceMs();

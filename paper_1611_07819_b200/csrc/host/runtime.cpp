@@ -16,6 +16,8 @@
 // mode, reference kernels.hpp:19-22).
 #include "runtime.hpp"
 
+#include <cuda.h>  // types of the driver entry points (resolved at run time, no -lcuda)
+
 #include <algorithm>
 #include <cstdio>
 #include <cstdlib>
@@ -28,6 +30,51 @@ namespace gridmath {
 namespace {
 
 constexpr std::uint64_t kPitchAlign = 16;  // TMA row-stride rule
+
+// SPMD flag page: written[kSlots], readDone[2][kSlots] (comm, compute).
+constexpr std::uint32_t kSlots = 16384;
+constexpr std::size_t kFlagBytes = 3ull * kSlots * sizeof(std::uint32_t);
+
+// Stream memory operations and address-range lookup from the driver, via
+// the runtime's entry-point query (the library stays loadable without a
+// driver: CPU-only hosts load it for the pure-host helpers).
+struct DriverFns {
+  CUresult (*waitValue32)(CUstream, CUdeviceptr, cuuint32_t, unsigned int) = nullptr;
+  CUresult (*writeValue32)(CUstream, CUdeviceptr, cuuint32_t, unsigned int) = nullptr;
+  CUresult (*addressRange)(CUdeviceptr*, size_t*, CUdeviceptr) = nullptr;
+};
+
+const DriverFns& driver() {
+  static const DriverFns fns = [] {
+    DriverFns f;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuStreamWaitValue32", reinterpret_cast<void**>(&f.waitValue32),
+                                cudaEnableDefault, &q) != cudaSuccess || q != cudaDriverEntryPointSuccess)
+      f.waitValue32 = nullptr;
+    if (cudaGetDriverEntryPoint("cuStreamWriteValue32", reinterpret_cast<void**>(&f.writeValue32),
+                                cudaEnableDefault, &q) != cudaSuccess || q != cudaDriverEntryPointSuccess)
+      f.writeValue32 = nullptr;
+    if (cudaGetDriverEntryPoint("cuMemGetAddressRange", reinterpret_cast<void**>(&f.addressRange),
+                                cudaEnableDefault, &q) != cudaSuccess || q != cudaDriverEntryPointSuccess)
+      f.addressRange = nullptr;
+    cudaGetLastError();
+    return f;
+  }();
+  return fns;
+}
+
+// One record per tile (or per rank for the flag pages) in the IPC
+// registration all-reduce (max over uint8: the owner's bytes win, zeros
+// elsewhere; `failed` is an OR over ranks).
+struct IpcRecord {
+  cudaIpcMemHandle_t handle;
+  std::uint64_t base;    // allocation base in the exporter's address space
+  std::uint64_t offset;  // tile pointer - base
+  std::uint8_t valid;
+  std::uint8_t failed;
+  std::uint8_t pad[6];
+};
+static_assert(sizeof(IpcRecord) == 88, "ipc record layout");
 
 std::uint64_t paddedLd(std::uint64_t cols, std::uint64_t eb) {
   return ((cols * eb + kPitchAlign - 1) / kPitchAlign * kPitchAlign) / eb;
@@ -220,6 +267,8 @@ Worker::~Worker() {
     if (e.ready) cudaEventDestroy(e.ready);
   for (auto& kv : replicas)
     if (kv.second.ready) cudaEventDestroy(kv.second.ready);
+  for (auto& kv : lastWrite) cudaEventDestroy(kv.second);
+  if (flags) cudaFree(flags);
   if (nccl) ncclCommDestroy(nccl);
   for (cudaEvent_t e : pool_) cudaEventDestroy(e);
   cudaEventDestroy(tStart);
@@ -260,21 +309,232 @@ void* Worker::workspace(std::uint64_t bytes) {
 }
 
 void Worker::releaseReaders() {
-  for (auto& rd : readers_) rd.second->recycle(rd.first);
+  for (auto& kv : readers_)
+    for (auto& rd : kv.second) rd.second->recycle(rd.first);
   readers_.clear();
 }
 
-void Worker::beforeMutation() {
-  if (readers_.empty()) return;
+void Worker::beforeMutation(std::uint64_t matrix) {
+  auto it = readers_.find(matrix);
+  if (it == readers_.end()) return;
   activate();
-  for (auto& rd : readers_) {
+  for (auto& rd : it->second) {
     cudaCheck(cudaStreamWaitEvent(compute, rd.first, 0), "worker: wait reader");
     rd.second->recycle(rd.first);
   }
-  readers_.clear();
+  readers_.erase(it);
 }
 
 // ---------------------------------------------------------------- Session
+
+namespace {
+
+// Max-reduce a small host byte array over all SPMD ranks (control plane of
+// the IPC registration; blocking).
+void allreduceMaxBytes(Worker& w, void* host, std::size_t n) {
+  w.activate();
+  void* d = w.arena.alloc(std::max<std::size_t>(n, 256), w.compute);
+  cudaCheck(cudaMemcpyAsync(d, host, n, cudaMemcpyHostToDevice, w.compute), "ipc: upload records");
+  ncclCheck(ncclAllReduce(d, d, n, ncclUint8, ncclMax, w.nccl, w.compute), "ipc: allreduce records");
+  cudaCheck(cudaMemcpyAsync(host, d, n, cudaMemcpyDeviceToHost, w.compute), "ipc: download records");
+  cudaCheck(cudaStreamSynchronize(w.compute), "ipc: records sync");
+  w.arena.free(d, w.compute);
+}
+
+}  // namespace
+
+// SPMD copy-engine plane: every rank exports a flag page; every rank must
+// map every peer's page, or all ranks fall back to NCCL together.
+void Session::setupIpc() {
+  Worker& w = *local(static_cast<std::uint32_t>(opts_.spmdRank));
+  w.activate();
+  const DriverFns& drv = driver();
+  std::vector<IpcRecord> recs(opts_.workers);
+  std::memset(recs.data(), 0, recs.size() * sizeof(IpcRecord));
+  IpcRecord& mine = recs[opts_.spmdRank];
+  bool ok = drv.waitValue32 && drv.writeValue32 && drv.addressRange;
+  if (ok) {
+    void* f = nullptr;
+    ok = cudaMalloc(&f, kFlagBytes) == cudaSuccess;
+    if (ok) {
+      w.flags = static_cast<std::uint32_t*>(f);
+      ok = cudaMemset(f, 0, kFlagBytes) == cudaSuccess && cudaDeviceSynchronize() == cudaSuccess &&
+           cudaIpcGetMemHandle(&mine.handle, f) == cudaSuccess;
+      mine.base = reinterpret_cast<std::uint64_t>(f);
+      mine.valid = 1;
+    }
+  }
+  cudaGetLastError();
+  if (!ok) mine.failed = 1;
+  allreduceMaxBytes(w, recs.data(), recs.size() * sizeof(IpcRecord));
+  bool all = true;
+  for (const IpcRecord& r : recs) all = all && r.valid && !r.failed;
+  std::vector<std::uint32_t*> mapped(opts_.workers, nullptr);
+  for (std::uint32_t r = 0; all && r < opts_.workers; ++r) {
+    if (r == w.rank) continue;
+    void* p = nullptr;
+    if (cudaIpcOpenMemHandle(&p, recs[r].handle, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
+      cudaGetLastError();
+      all = false;
+      break;
+    }
+    ipcOpened_[{r, recs[r].base}] = p;
+    mapped[r] = static_cast<std::uint32_t*>(p);
+  }
+  std::uint8_t failed = all ? 0 : 1;
+  allreduceMaxBytes(w, &failed, 1);
+  if (failed) {
+    for (auto& kv : ipcOpened_) cudaIpcCloseMemHandle(kv.second);
+    ipcOpened_.clear();
+    if (w.flags) cudaFree(w.flags);
+    w.flags = nullptr;
+    cudaGetLastError();
+    if (opts_.transport == 2)
+      throw Error("session: copy-engine transport requested but peer GPU memory cannot be mapped (CUDA IPC)");
+    return;
+  }
+  mapped[w.rank] = w.flags;
+  peerFlags_ = std::move(mapped);
+  ipc_ = true;
+}
+
+// Exports this rank's tiles of matrix `id` and maps every peer's (one
+// collective per create/reshape). A local failure is carried through the
+// collective so every rank throws together.
+void Session::registerTiles(std::uint64_t id, const std::string& localError) {
+  const MatrixDescriptor& d = lookup(table_, id);
+  Worker& w = *local(static_cast<std::uint32_t>(opts_.spmdRank));
+  w.activate();
+  const DriverFns& drv = driver();
+  const std::size_t T = d.layout.tiles.size();
+  std::vector<IpcRecord> recs(T + 1);
+  std::memset(recs.data(), 0, recs.size() * sizeof(IpcRecord));
+  std::string err = localError;
+  if (err.empty()) {
+    auto tit = w.tiles.find(id);
+    std::size_t i = 0;
+    for (const auto& t : d.layout.tiles) {
+      if (t.second.rank == w.rank && tit != w.tiles.end())
+        for (const DeviceTile& dt : tit->second) {
+          if (!(dt.extent == t.first) || !err.empty()) continue;
+          CUdeviceptr base = 0;
+          size_t size = 0;
+          if (drv.addressRange(&base, &size, reinterpret_cast<CUdeviceptr>(dt.ptr)) != CUDA_SUCCESS) {
+            err = "ipc: cuMemGetAddressRange failed for a tile";
+          } else if (cudaIpcGetMemHandle(&recs[i].handle, reinterpret_cast<void*>(base)) != cudaSuccess) {
+            cudaGetLastError();
+            err = "ipc: cudaIpcGetMemHandle failed for a tile";
+          } else {
+            recs[i].base = base;
+            recs[i].offset = reinterpret_cast<std::uint64_t>(dt.ptr) - base;
+            recs[i].valid = 1;
+          }
+        }
+      ++i;
+    }
+  }
+  if (!err.empty()) recs[T].failed = 1;
+  allreduceMaxBytes(w, recs.data(), recs.size() * sizeof(IpcRecord));
+  if (recs[T].failed)
+    throw Error(err.empty() ? "op failed: a peer rank could not allocate or export its tiles" : err);
+  std::vector<void*> ptrs(T, nullptr);
+  std::size_t i = 0;
+  for (const auto& t : d.layout.tiles) {
+    if (t.second.rank != w.rank) {
+      const IpcRecord& r = recs[i];
+      if (!r.valid) throw Error("ipc: tile " + std::to_string(i) + " of matrix " + std::to_string(id) + " not exported");
+      const auto key = std::make_pair(t.second.rank, r.base);
+      auto it = ipcOpened_.find(key);
+      void* p = nullptr;
+      if (it == ipcOpened_.end()) {
+        cudaCheck(cudaIpcOpenMemHandle(&p, r.handle, cudaIpcMemLazyEnablePeerAccess), "ipc: map peer tile");
+        ipcOpened_[key] = p;
+      } else {
+        p = it->second;
+      }
+      ptrs[i] = static_cast<std::uint8_t*>(p) + r.offset;
+    }
+    ++i;
+  }
+  peerTiles_[id] = std::move(ptrs);
+}
+
+void Session::ipcWait(cudaStream_t s, const std::uint32_t* addr, std::uint64_t value) {
+  const CUresult r = driver().waitValue32(reinterpret_cast<CUstream>(s), reinterpret_cast<CUdeviceptr>(addr),
+                                          static_cast<cuuint32_t>(value), CU_STREAM_WAIT_VALUE_GEQ);
+  if (r != CUDA_SUCCESS) throw Error("ipc: cuStreamWaitValue32 failed (" + std::to_string(static_cast<int>(r)) + ")");
+}
+
+void Session::ipcWrite(cudaStream_t s, std::uint32_t* addr, std::uint64_t value) {
+  const CUresult r = driver().writeValue32(reinterpret_cast<CUstream>(s), reinterpret_cast<CUdeviceptr>(addr),
+                                           static_cast<cuuint32_t>(value), CU_STREAM_WRITE_VALUE_DEFAULT);
+  if (r != CUDA_SUCCESS) throw Error("ipc: cuStreamWriteValue32 failed (" + std::to_string(static_cast<int>(r)) + ")");
+}
+
+std::uint32_t Session::slotOf(std::uint64_t id) const {
+  auto it = slots_.find(id);
+  if (it == slots_.end()) throw Error("ipc: matrix " + std::to_string(id) + " has no flag slot");
+  return it->second;
+}
+
+BandView Session::srcView(const MatrixDescriptor& M, std::uint32_t src, const Rect& r) {
+  const std::uint64_t eb = bytesOf(M.precision);
+  if (Worker* sw = local(src)) {
+    for (const DeviceTile& dt : sw->tiles.at(M.matrixId))
+      if (r.inside(Rect::ofExtent(dt.extent)))
+        return offsetView(dt.ptr, dt.ld, r.r0 - dt.extent.rowStart, r.c0 - dt.extent.colStart, eb);
+    return {};
+  }
+  if (!ipc_) return {};
+  auto pit = peerTiles_.find(M.matrixId);
+  if (pit == peerTiles_.end()) return {};
+  std::size_t i = 0;
+  for (const auto& t : M.layout.tiles) {
+    if (t.second.rank == src && pit->second[i] && r.inside(Rect::ofExtent(t.first)))
+      return offsetView(pit->second[i], paddedLd(t.first.colCount, eb), r.r0 - t.first.rowStart,
+                        r.c0 - t.first.colStart, eb);
+    ++i;
+  }
+  return {};
+}
+
+// Publishes the previous op's mutations: per worker and matrix an event on
+// the compute stream (local readers on other streams wait on it) and, on the
+// SPMD copy-engine plane, written[slot] = exec id (peers' streams wait on it).
+void Session::flushWritten(std::uint64_t before) {
+  if (pendingWritten_.empty()) return;
+  // Only ops older than `before`: the current op's own mutation is published
+  // after its device work (at the next issue), never from inside the op.
+  std::vector<std::pair<std::uint64_t, std::uint64_t>> pend, keep;
+  for (const auto& pw : pendingWritten_) (pw.second < before ? pend : keep).push_back(pw);
+  pendingWritten_ = std::move(keep);
+  for (const auto& pw : pend) {
+    if (!table_.count(pw.first)) continue;
+    for (auto& wp : workers_) {
+      if (!wp) continue;
+      Worker& w = *wp;
+      auto tit = w.tiles.find(pw.first);
+      if (tit == w.tiles.end() || tit->second.empty()) continue;
+      w.activate();
+      cudaEvent_t& e = w.lastWrite[pw.first];
+      if (!e) cudaCheck(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "worker: write event");
+      cudaCheck(cudaEventRecord(e, w.compute), "worker: record write");
+      if (ipc_) ipcWrite(w.compute, w.flags + slotOf(pw.first), pw.second);
+    }
+  }
+}
+
+// Consumers publish readDone[stream][slot] = exec id once this op's pulls
+// from peer tiles are done (their producers wait on it before mutating).
+void Session::commitReads() {
+  for (const auto& pr : pendingReads_) {
+    Worker& d = *local(std::get<0>(pr));
+    const int si = std::get<2>(pr);
+    d.activate();
+    ipcWrite(si == 0 ? d.comm : d.compute, d.flags + kSlots * (1 + si) + slotOf(std::get<1>(pr)), curExec_);
+  }
+  pendingReads_.clear();
+}
 
 Session::Session(SessionOptions opts) : opts_(std::move(opts)) {
   if (opts_.workers == 0) throw Error("session: need at least one worker");
@@ -309,6 +569,7 @@ Session::Session(SessionOptions opts) : opts_(std::move(opts)) {
       nccl_ = true;
     }
     workers_[opts_.spmdRank] = std::move(w);
+    if (nccl_ && opts_.transport != 1) setupIpc();
   } else {
     for (std::uint32_t r = 0; r < opts_.workers; ++r) {
       const int dev = devs[r % devs.size()];
@@ -338,6 +599,18 @@ Session::~Session() {
   try {
     synchronize();
   } catch (...) {
+  }
+  if (ipc_) {
+    // Peers may still be pulling from this rank's tiles: every rank is
+    // idle before any mapping closes or any arena frees.
+    try {
+      std::uint8_t b = 0;
+      allreduceMaxBytes(*local(static_cast<std::uint32_t>(opts_.spmdRank)), &b, 1);
+    } catch (...) {
+    }
+    for (auto& kv : ipcOpened_) cudaIpcCloseMemHandle(kv.second);
+    ipcOpened_.clear();
+    cudaGetLastError();
   }
   // Reader events can belong to a peer's pool: return them all before any
   // worker goes away.
@@ -383,7 +656,9 @@ void Session::checkErrors(std::vector<std::string>& errs) {
 const MatrixDescriptor& Session::descriptor(std::uint64_t id) const { return lookup(table_, id); }
 
 std::uint64_t Session::issue(OpDescriptor& op) {
+  flushWritten(nextExec_);  // earlier ops' device work is enqueued: publish their writes
   op.execId = nextExec_++;
+  curExec_ = op.execId;
   validateOp(table_, op, opts_.workers);
   std::vector<std::pair<std::uint64_t, std::uint64_t>> moved;
   for (std::uint64_t id : mutatedMatrices(op)) {
@@ -396,6 +671,25 @@ std::uint64_t Session::issue(OpDescriptor& op) {
   for (auto& w : workers_)
     if (w) applyOpMetadata(OpDescriptor::decode(wire), w->descs);
   for (const auto& mv : moved) mutationHook(mv.first, mv.second);
+  // Flag slots follow the (replicated) op stream, so every rank agrees.
+  if (op.opcode == OpCode::CreateMatrix) {
+    std::uint32_t slot = kSlots;
+    if (!freeSlots_.empty()) {
+      slot = freeSlots_.front();
+      freeSlots_.erase(freeSlots_.begin());
+    } else if (nextSlot_ < kSlots) {
+      slot = nextSlot_++;
+    } else if (ipc_) {
+      throw Error("createMatrix: more than " + std::to_string(kSlots) + " live matrices");
+    }
+    if (slot < kSlots) slots_[op.ids[0]] = slot;
+    lastMut_[op.ids[0]] = op.execId;
+    pendingWritten_.push_back({op.ids[0], op.execId});  // the zero fill
+  }
+  for (const auto& mv : moved) {
+    lastMut_[mv.first] = op.execId;
+    pendingWritten_.push_back({mv.first, op.execId});
+  }
   if (opts_.checkMetadataEveryOp) verifyMetadataConsistency();
   return op.execId;
 }
@@ -424,8 +718,15 @@ void Session::mutationHook(std::uint64_t id, std::uint64_t oldVersion) {
       w.arena.free(e.ptr, w.compute);
       w.recycle(e.ready);
     }
-    w.beforeMutation();
+    w.beforeMutation(id);
+    // Peers that pulled from this worker's tiles of the matrix (SPMD
+    // copy-engine plane) must be done before it changes.
+    auto rr = remoteReaders_.find(id);
+    if (rr != remoteReaders_.end() && w.tiles.count(id))
+      for (const auto& rd : rr->second)
+        ipcWait(w.compute, peerFlags_[rd.first.first] + kSlots * (1 + rd.first.second) + slotOf(id), rd.second);
   }
+  remoteReaders_.erase(id);
   for (std::uint32_t r = 0; r < opts_.workers; ++r)
     if (!isLocal(r)) remoteCaches_[r].dropMatrix(id, true, newVersion);
 }
@@ -469,21 +770,27 @@ void Session::execCreate(const OpDescriptor& op) {
   WireReader r(op.blob);
   const MatrixDescriptor d = decodeDescriptor(r);
   const std::uint64_t eb = bytesOf(d.precision);
-  forEachLocal([&](Worker& w) {
-    std::vector<DeviceTile> mine;
-    for (const auto& t : d.layout.tiles) {
-      if (t.second.rank != w.rank) continue;
-      DeviceTile dt;
-      dt.extent = t.first;
-      dt.ld = paddedLd(t.first.colCount, eb);
-      const std::uint64_t bytes = t.first.rowCount * dt.ld * eb;
-      dt.ptr = w.arena.alloc(bytes, w.compute);
-      cudaCheck(cudaMemsetAsync(dt.ptr, 0, bytes, w.compute), "create: zero tile");
-      w.residentBytes += t.first.elements() * eb;
-      mine.push_back(dt);
-    }
-    w.tiles[d.matrixId] = std::move(mine);
-  });
+  std::string localError;
+  try {
+    forEachLocal([&](Worker& w) {
+      std::vector<DeviceTile>& mine = w.tiles[d.matrixId];  // partial on failure: destroy frees it
+      for (const auto& t : d.layout.tiles) {
+        if (t.second.rank != w.rank) continue;
+        DeviceTile dt;
+        dt.extent = t.first;
+        dt.ld = paddedLd(t.first.colCount, eb);
+        const std::uint64_t bytes = t.first.rowCount * dt.ld * eb;
+        dt.ptr = w.arena.alloc(bytes, w.compute);
+        mine.push_back(dt);
+        cudaCheck(cudaMemsetAsync(dt.ptr, 0, bytes, w.compute), "create: zero tile");
+        w.residentBytes += t.first.elements() * eb;
+      }
+    });
+  } catch (const std::exception& e) {
+    if (!ipc_) throw;
+    localError = e.what();
+  }
+  if (ipc_) registerTiles(d.matrixId, localError);  // collective: all ranks fail together
 }
 
 void Session::destroy(DistMatrix m) {
@@ -498,7 +805,12 @@ void Session::destroy(DistMatrix m) {
 
 void Session::execDestroy(std::uint64_t id) {
   forEachLocal([&](Worker& w) {
-    w.beforeMutation();
+    w.beforeMutation(id);
+    auto lw = w.lastWrite.find(id);
+    if (lw != w.lastWrite.end()) {
+      cudaEventDestroy(lw->second);
+      w.lastWrite.erase(lw);
+    }
     auto it = w.tiles.find(id);
     if (it != w.tiles.end()) {
       const std::uint64_t eb = 1;  // residentBytes tracked in bytes below
@@ -519,6 +831,14 @@ void Session::execDestroy(std::uint64_t id) {
     }
   });
   for (auto& c : remoteCaches_) c.dropMatrix(id, false, 0);
+  auto sl = slots_.find(id);
+  if (sl != slots_.end()) {
+    freeSlots_.push_back(sl->second);
+    slots_.erase(sl);
+  }
+  lastMut_.erase(id);
+  peerTiles_.erase(id);
+  remoteReaders_.erase(id);
   // resident bytes recomputed from the remaining tiles
   for (auto& w : workers_) {
     if (!w) continue;
@@ -672,6 +992,8 @@ void Session::reshape(DistMatrix m, const Layout& newLayout, std::optional<Preci
   op.blob = ww.take();
   op.execId = nextExec_;
   validateOp(table_, op, opts_.workers);
+  curExec_ = op.execId;  // pulls below are this op's reads (WAR bookkeeping)
+  flushWritten(curExec_);
 
   const std::uint64_t oldEb = bytesOf(old.precision), newEb = bytesOf(nd.precision);
   const bool convert = old.precision != nd.precision;
@@ -723,13 +1045,10 @@ void Session::reshape(DistMatrix m, const Layout& newLayout, std::optional<Preci
           x.rows = piece->rows();
           x.cols = piece->cols();
           x.eb = static_cast<std::uint32_t>(oldEb);
-          if (sw)
-            for (const DeviceTile& dt : sw->tiles.at(old.matrixId))
-              if (dt.extent == ot.first) {
-                x.srcPtr = static_cast<const std::uint8_t*>(dt.ptr) +
-                           ((piece->r0 - dt.extent.rowStart) * dt.ld + (piece->c0 - dt.extent.colStart)) * oldEb;
-                x.srcLd = dt.ld;
-              }
+          x.matrix = old.matrixId;
+          const BandView sv = srcView(old, ot.second.rank, *piece);
+          x.srcPtr = sv.ptr;
+          x.srcLd = sv.ld;
           if (w) {
             x.dstPtr = static_cast<std::uint8_t*>(dst) + ((piece->r0 - e.rowStart) * dstLd + (piece->c0 - e.colStart)) * oldEb;
             x.dstLd = dstLd;
@@ -772,65 +1091,94 @@ void Session::reshape(DistMatrix m, const Layout& newLayout, std::optional<Preci
       for (auto& t : kv.second) w.residentBytes += t.extent.elements() * eb;
     }
   });
+  if (ipc_) registerTiles(old.matrixId, "");
 }
 
 // ---------------------------------------------------------------- data plane
 
-// Copy-engine plane (single process): the consumer pulls every piece with a
-// 2D peer/D2D copy on its stream after waiting for the producer's prior
-// writes; the producer later waits for the consumer before mutating (WAR).
-// NCCL plane (SPMD): grouped ncclSend/ncclRecv, packing/unpacking strided
-// pieces through arena staging; stream order covers RAW and WAR.
-void Session::exchange(std::vector<Xfer>& xs, bool onComm) {
+// Copy-engine planes -- one process (peer copies between its workers) or
+// SPMD over CUDA IPC (a rank maps its peers' tiles): the consumer pulls each
+// piece with a 2D copy on its own stream. No SMs are used, so the pulls of
+// op i+1 overlap the persistent GEMM of op i. RAW: the consumer's stream
+// waits for the last write of the source matrix (a local event, or the
+// producer's written[slot] flag); WAR: the producer waits for the
+// consumer's completion (a reader event, or the consumer's readDone flag)
+// before it next mutates that matrix.
+// NCCL plane (SPMD fallback): grouped ncclSend/ncclRecv, packing/unpacking
+// strided pieces through arena staging.
+void Session::exchange(std::vector<Xfer>& xs, bool onComm, bool commit) {
+  flushWritten(curExec_);
   auto streamOf = [&](Worker& w) { return onComm ? w.comm : w.compute; };
-  if (!nccl_) {
-    std::map<std::pair<std::uint32_t, std::uint32_t>, bool> pairs;  // (src, dst)
-    for (const Xfer& x : xs)
-      if (x.src != x.dst || onComm) pairs[{x.src, x.dst}] = true;
-    // RAW: consumer waits for the producer's writes issued so far.
-    for (const auto& pr : pairs) {
-      Worker& s = *local(pr.first.first);
-      Worker& d = *local(pr.first.second);
-      s.activate();
-      cudaEvent_t e = s.event();
-      cudaCheck(cudaEventRecord(e, s.compute), "exchange: record");
-      d.activate();
-      cudaCheck(cudaStreamWaitEvent(streamOf(d), e, 0), "exchange: wait");
-      s.recycle(e);
-    }
+  const int sIdx = onComm ? 0 : 1;
+  if (!nccl_ || ipc_) {
+    std::set<std::tuple<std::uint32_t, std::uint32_t, std::uint64_t>> routes;  // (src, dst, matrix)
     for (const Xfer& x : xs) {
-      Worker& d = *local(x.dst);
-      d.activate();
-      cudaCheck(cudaMemcpy2DAsync(x.dstPtr, x.dstLd * x.eb, x.srcPtr, x.srcLd * x.eb, x.cols * x.eb,
-                                  x.rows, cudaMemcpyDefault, streamOf(d)),
-                "exchange: copy");
-      if (x.src != x.dst) {
-        d.bytesReceived += x.rows * x.cols * x.eb;
-        local(x.src)->bytesSent += x.rows * x.cols * x.eb;
+      const std::uint64_t bytes = x.rows * x.cols * x.eb;
+      if (bytes == 0) continue;
+      Worker* d = local(x.dst);
+      Worker* s = local(x.src);
+      if (!d) {
+        // Producer side of a peer's pull: remember the reader (WAR).
+        if (s) {
+          s->bytesSent += bytes;
+          std::uint64_t& last = remoteReaders_[x.matrix][{x.dst, sIdx}];
+          last = std::max(last, curExec_);
+        }
+        continue;
+      }
+      if (!routes.insert({x.src, x.dst, x.matrix}).second) continue;
+      d->activate();
+      if (s) {
+        auto it = s->lastWrite.find(x.matrix);
+        if (it != s->lastWrite.end() && (s != d || onComm))
+          cudaCheck(cudaStreamWaitEvent(streamOf(*d), it->second, 0), "exchange: wait writer");
+      } else {
+        ipcWait(streamOf(*d), peerFlags_[x.src] + slotOf(x.matrix), lastMut_.at(x.matrix));
       }
     }
-    // WAR: producer waits for the consumer's copies before its next mutation.
-    for (const auto& pr : pairs) {
-      Worker& s = *local(pr.first.first);
-      Worker& d = *local(pr.first.second);
-      if (&s == &d && !onComm) continue;
-      d.activate();
-      cudaEvent_t e = d.event();
-      cudaCheck(cudaEventRecord(e, streamOf(d)), "exchange: record done");
-      s.addReader(e, &d);
+    for (const Xfer& x : xs) {
+      const std::uint64_t bytes = x.rows * x.cols * x.eb;
+      Worker* d = local(x.dst);
+      if (!d || bytes == 0) continue;
+      if (!x.srcPtr)
+        throw Error("exchange: no mapping for a piece of matrix " + std::to_string(x.matrix) + " on worker " +
+                    std::to_string(x.src));
+      d->activate();
+      cudaCheck(cudaMemcpy2DAsync(x.dstPtr, x.dstLd * x.eb, x.srcPtr, x.srcLd * x.eb, x.cols * x.eb, x.rows,
+                                  cudaMemcpyDefault, streamOf(*d)),
+                "exchange: copy");
+      if (x.src != x.dst) {
+        d->bytesReceived += bytes;
+        if (Worker* s = local(x.src)) s->bytesSent += bytes;
+      }
     }
+    for (const auto& rt : routes) {
+      Worker& d = *local(std::get<1>(rt));
+      Worker* s = local(std::get<0>(rt));
+      if (s) {
+        if (s == &d && !onComm) continue;
+        d.activate();
+        cudaEvent_t e = d.event();
+        cudaCheck(cudaEventRecord(e, streamOf(d)), "exchange: record done");
+        s->addReader(std::get<2>(rt), e, &d);
+      } else {
+        pendingReads_.insert({std::get<1>(rt), std::get<2>(rt), sIdx});
+      }
+    }
+    if (commit) commitReads();
     return;
   }
-  // ---- NCCL
-  if (onComm) {
-    // The comm stream must see the compute stream's prior writes.
-    for (auto& wp : workers_) {
-      if (!wp) continue;
-      wp->activate();
-      cudaEvent_t e = wp->event();
-      cudaCheck(cudaEventRecord(e, wp->compute), "exchange: record");
-      cudaCheck(cudaStreamWaitEvent(wp->comm, e, 0), "exchange: wait");
-      wp->recycle(e);
+  // ---- NCCL: sending (and locally copying) streams wait for the last write
+  // of the matrices they read.
+  std::set<std::pair<std::uint32_t, std::uint64_t>> readSrc;  // (local src worker, matrix)
+  for (const Xfer& x : xs)
+    if (x.rows * x.cols != 0 && local(x.src)) readSrc.insert({x.src, x.matrix});
+  for (const auto& rs : readSrc) {
+    Worker& s = *local(rs.first);
+    auto it = s.lastWrite.find(rs.second);
+    if (onComm && it != s.lastWrite.end()) {
+      s.activate();
+      cudaCheck(cudaStreamWaitEvent(s.comm, it->second, 0), "exchange: wait writer");
     }
   }
   struct Staged {
@@ -907,12 +1255,12 @@ void Session::exchange(std::vector<Xfer>& xs, bool onComm) {
   }
   if (onComm) {
     // Sends read tiles on the comm stream: later mutations wait for them.
-    for (auto& wp : workers_) {
-      if (!wp) continue;
-      wp->activate();
-      cudaEvent_t e = wp->event();
-      cudaCheck(cudaEventRecord(e, wp->comm), "exchange: record");
-      wp->addReader(e, wp.get());
+    for (const auto& rs : readSrc) {
+      Worker& s = *local(rs.first);
+      s.activate();
+      cudaEvent_t e = s.event();
+      cudaCheck(cudaEventRecord(e, s.comm), "exchange: record");
+      s.addReader(rs.second, e, &s);
     }
   }
 }
@@ -1152,13 +1500,12 @@ void Session::execGemm(const OpDescriptor& op) {
             x.rows = r.rows();
             x.cols = r.cols();
             x.eb = static_cast<std::uint32_t>(eb);
-            if (sw)
-              for (const DeviceTile& dt : sw->tiles.at(M.matrixId))
-                if (r.inside(Rect::ofExtent(dt.extent))) {
-                  x.srcPtr = static_cast<const std::uint8_t*>(dt.ptr) +
-                             ((r.r0 - dt.extent.rowStart) * dt.ld + (r.c0 - dt.extent.colStart)) * eb;
-                  x.srcLd = dt.ld;
-                }
+            x.matrix = M.matrixId;
+            if (w || sw) {
+              const BandView sv = srcView(M, pr.src, r);
+              x.srcPtr = sv.ptr;
+              x.srcLd = sv.ld;
+            }
             if (w) {
               x.dstPtr = static_cast<std::uint8_t*>(slot.ptr) + ((r.r0 - nd.rect.r0) * slot.ld + (r.c0 - nd.rect.c0)) * eb;
               x.dstLd = slot.ld;
@@ -1176,20 +1523,17 @@ void Session::execGemm(const OpDescriptor& op) {
   std::vector<std::vector<cudaEvent_t>> groupDone(1 + S);
   bool anyXfer = false;
   for (auto& gx : groups) anyXfer = anyXfer || !gx.empty();
+  // No blanket wait on the compute stream: exchange() orders each pull after
+  // the last write of its source matrix only, so these pulls overlap the
+  // GEMM of the previous op.
+  flushWritten(curExec_);
   forEachLocal([&](Worker& w) {
     w.commTimed = anyXfer;
-    if (anyXfer) {
-      // The exchange starts once the comm stream has the producers' writes.
-      cudaEvent_t e = w.event();
-      cudaCheck(cudaEventRecord(e, w.compute), "gemm: timing");
-      cudaCheck(cudaStreamWaitEvent(w.comm, e, 0), "gemm: timing");
-      w.recycle(e);
-      cudaCheck(cudaEventRecord(w.cStart, w.comm), "gemm: comm timing");
-    }
+    if (anyXfer) cudaCheck(cudaEventRecord(w.cStart, w.comm), "gemm: comm timing");
   });
   for (std::uint32_t gi = 0; gi <= S; ++gi) {
     if (groups[gi].empty()) continue;
-    exchange(groups[gi], true);
+    exchange(groups[gi], true, false);
     for (auto& wp : workers_) {
       if (!wp) continue;
       wp->activate();
@@ -1198,6 +1542,7 @@ void Session::execGemm(const OpDescriptor& op) {
       groupDone[gi].push_back(ev);
     }
   }
+  commitReads();
   forEachLocal([&](Worker& w) {
     if (w.commTimed) cudaCheck(cudaEventRecord(w.cEnd, w.comm), "gemm: comm timing");
   });
@@ -1446,6 +1791,13 @@ void Session::execReplicate(std::uint64_t id) {
       w->activate();
       ReplicaEntry& e = w->replicas[id];
       const std::uint64_t ld = paddedLd(M.cols, eb);
+      if (e.full) {
+        // GEMMs on the compute stream may still read the previous version.
+        cudaEvent_t ev = w->event();
+        cudaCheck(cudaEventRecord(ev, w->compute), "replica: record readers");
+        cudaCheck(cudaStreamWaitEvent(w->comm, ev, 0), "replica: wait readers");
+        w->recycle(ev);
+      }
       if (!e.full || e.ld != ld) {
         if (e.full) w->arena.free(e.full, w->comm);
         e.full = w->arena.alloc(M.rows * ld * eb, w->comm);
@@ -1467,12 +1819,10 @@ void Session::execReplicate(std::uint64_t id) {
       x.rows = t.first.rowCount;
       x.cols = t.first.colCount;
       x.eb = static_cast<std::uint32_t>(eb);
-      if (sw)
-        for (const DeviceTile& dt : sw->tiles.at(id))
-          if (dt.extent == t.first) {
-            x.srcPtr = dt.ptr;
-            x.srcLd = dt.ld;
-          }
+      x.matrix = id;
+      const BandView sv = srcView(M, src, Rect::ofExtent(t.first));
+      x.srcPtr = sv.ptr;
+      x.srcLd = sv.ld;
       if (entry) {
         x.dstPtr = static_cast<std::uint8_t*>(entry->full) + (t.first.rowStart * entry->ld + t.first.colStart) * eb;
         x.dstLd = entry->ld;

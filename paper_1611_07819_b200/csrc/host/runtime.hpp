@@ -29,6 +29,7 @@
 #include <optional>
 #include <set>
 #include <string>
+#include <tuple>
 #include <utility>
 #include <vector>
 
@@ -75,7 +76,10 @@ struct SessionOptions {
   std::array<std::uint8_t, 128> ncclId{};
   int gemmMaxCtas = 0;                // cap the GEMM grid (0 = all SMs)
   std::uint64_t panelCacheBytes = 0;  // per worker; 0 = 1/4 of device memory
-  int transport = 0;                  // 0 auto, 1 NCCL, 2 copy engine
+  // Data plane. 0 auto: copy engines (single process: peer copies; SPMD:
+  // CUDA IPC pulls ordered by device-side flags) when every peer GPU is
+  // mappable, else NCCL. 1 forces NCCL point-to-point; 2 requires copy engines.
+  int transport = 0;
   int pipelineChunks = 0;             // SUMMA row chunks (0 = auto)
 };
 
@@ -153,12 +157,21 @@ class Worker {
   cudaEvent_t event();            // from a recycled pool
   void recycle(cudaEvent_t e);
   void* workspace(std::uint64_t bytes);
-  // Stream-ordered WAR guard: readers of this worker's tiles register their
-  // completion events; the compute stream waits on them before any mutation.
-  // `owner` is the worker whose pool the event came from (recycled there).
-  void addReader(cudaEvent_t e, Worker* owner) { readers_.push_back({e, owner}); }
-  void beforeMutation();
+  // Stream-ordered WAR guard, per matrix: readers of this worker's tiles of
+  // a matrix register their completion events; the compute stream waits on
+  // them before that matrix is mutated or freed. `owner` is the worker whose
+  // pool the event came from (recycled there).
+  void addReader(std::uint64_t matrix, cudaEvent_t e, Worker* owner) { readers_[matrix].push_back({e, owner}); }
+  void beforeMutation(std::uint64_t matrix);
   void releaseReaders();
+  // RAW: event on the compute stream after the last op that wrote this
+  // worker's tiles of a matrix; readers on other streams wait on it instead
+  // of on the whole compute stream (so the next op's panel pulls overlap
+  // the current GEMM).
+  std::map<std::uint64_t, cudaEvent_t> lastWrite;
+  // SPMD copy-engine plane: this rank's flag page (device memory, mapped by
+  // every peer): written[slot], then readDone[stream][slot].
+  std::uint32_t* flags = nullptr;
 
   std::uint32_t rank;
   int device;
@@ -179,7 +192,7 @@ class Worker {
 
  private:
   std::vector<cudaEvent_t> pool_;
-  std::vector<std::pair<cudaEvent_t, Worker*>> readers_;
+  std::map<std::uint64_t, std::vector<std::pair<cudaEvent_t, Worker*>>> readers_;
   void* ws_ = nullptr;
   std::uint64_t wsBytes_ = 0;
 };
@@ -194,6 +207,7 @@ struct Xfer {
   std::uint64_t dstLd = 0;
   std::uint64_t rows = 0, cols = 0;
   std::uint32_t eb = 0;
+  std::uint64_t matrix = 0;  // source matrix id (RAW/WAR tracking)
 };
 
 // Pure GEMM planning (no device state): merged C row/col intervals per
@@ -257,6 +271,8 @@ class Session {
   bool deterministic() const { return opts_.deterministic; }
   const SessionOptions& options() const { return opts_; }
   std::vector<std::uint32_t> localRanks() const;
+  // 0 = copy engine (one process), 1 = NCCL, 2 = CUDA IPC copy engine (SPMD).
+  int transportKind() const { return ipc_ ? 2 : (nccl_ ? 1 : 0); }
 
   // Issues a Gemm op (gemm() below wraps it). sync: wait for completion
   // like the reference's acked gemm(); otherwise stream-ordered only.
@@ -280,7 +296,18 @@ class Session {
   void execGemm(const OpDescriptor& op);
   void execReplicate(std::uint64_t id);
   void mutationHook(std::uint64_t id, std::uint64_t oldVersion);
-  void exchange(std::vector<Xfer>& xs, bool onComm);
+  void exchange(std::vector<Xfer>& xs, bool onComm, bool commit = true);
+  // --- RAW/WAR bookkeeping shared by the planes
+  void flushWritten(std::uint64_t before);  // publish mutations of ops with exec id < before
+  void commitReads();    // consumers publish readDone for this op's pulls
+  void setupIpc();
+  void registerTiles(std::uint64_t id, const std::string& localError);
+  void ipcWait(cudaStream_t s, const std::uint32_t* addr, std::uint64_t value);
+  void ipcWrite(cudaStream_t s, std::uint32_t* addr, std::uint64_t value);
+  std::uint32_t slotOf(std::uint64_t id) const;
+  // Source view of `r` (inside one tile of M owned by `src`): a local tile
+  // pointer, or the IPC mapping of a peer's tile. {nullptr, 0} if neither.
+  BandView srcView(const MatrixDescriptor& M, std::uint32_t src, const Rect& r);
   void forEachLocal(const std::function<void(Worker&)>& f);
   void checkErrors(std::vector<std::string>& errs);
 
@@ -294,6 +321,20 @@ class Session {
   std::uint64_t tick_ = 0;
   bool nccl_ = false;
   bool peerCopies_ = false;
+  bool ipc_ = false;
+  std::uint64_t curExec_ = 0;                              // exec id of the op being executed
+  std::map<std::uint64_t, std::uint64_t> lastMut_;         // matrix -> exec id of its last write
+  std::vector<std::pair<std::uint64_t, std::uint64_t>> pendingWritten_;  // (matrix, exec id)
+  std::map<std::uint64_t, std::uint32_t> slots_;           // matrix -> flag slot (same on all ranks)
+  std::vector<std::uint32_t> freeSlots_;
+  std::uint32_t nextSlot_ = 0;
+  // SPMD IPC plane
+  std::vector<std::uint32_t*> peerFlags_;                  // rank -> mapped flag page
+  std::map<std::pair<std::uint32_t, std::uint64_t>, void*> ipcOpened_;  // (rank, remote base) -> mapping
+  std::map<std::uint64_t, std::vector<void*>> peerTiles_;  // matrix -> per layout tile: mapped ptr
+  // producer side: matrix -> (consumer, stream) -> exec id of its last pull
+  std::map<std::uint64_t, std::map<std::pair<std::uint32_t, int>, std::uint64_t>> remoteReaders_;
+  std::set<std::tuple<std::uint32_t, std::uint64_t, int>> pendingReads_;  // (consumer, matrix, stream)
 };
 
 void gemm(Session& s, DistMatrix a, DistMatrix b, DistMatrix c, double alpha, double beta,

@@ -292,6 +292,13 @@ class Session:
         check(_lib.load().gm_session_local_workers(self._h, arr, 64, ctypes.byref(n)))
         return list(arr[: n.value])
 
+    def transport(self) -> str:
+        """Data plane in use: "peer_copy" (one process), "nccl", or "ipc"
+        (one process per GPU, copy-engine pulls over CUDA IPC)."""
+        k = ctypes.c_int32()
+        check(_lib.load().gm_session_transport(self._h, ctypes.byref(k)))
+        return {0: "peer_copy", 1: "nccl", 2: "ipc"}[k.value]
+
     def synchronize(self):
         check(_lib.load().gm_session_synchronize(self._h))
 
