@@ -44,17 +44,18 @@ std::uint64_t DeviceArena::sizeClass(std::uint64_t bytes) {
   return p * 2;
 }
 
-void* DeviceArena::alloc(std::uint64_t bytes, cudaStream_t stream) {
+void* DeviceArena::alloc(std::uint64_t bytes, cudaStream_t stream, std::uint64_t epoch, std::uint64_t minAge) {
   if (bytes == 0) throw Error("arena: zero-byte allocation");
   const std::uint64_t cls = sizeClass(bytes);
   std::lock_guard<std::mutex> lock(mu_);
   auto& list = free_[cls];
-  if (!list.empty()) {
-    // FIFO: the block released longest ago (its release event has most
-    // likely completed), so back-to-back ops alternate between buffers
-    // instead of waiting for the previous op to finish with the newest one.
-    Block b = list.front();
-    list.erase(list.begin());
+  // FIFO: the block released longest ago (its release event has most likely
+  // completed); with minAge, skip blocks released too recently.
+  auto pick = list.begin();
+  while (pick != list.end() && minAge && pick->epoch + minAge > epoch) ++pick;
+  if (pick != list.end()) {
+    Block b = *pick;
+    list.erase(pick);
     if (b.released) {
       cudaCheck(cudaStreamWaitEvent(stream, b.released, 0), "arena: wait on release");
       eventPool_.push_back(b.released);
@@ -78,7 +79,7 @@ void* DeviceArena::alloc(std::uint64_t bytes, cudaStream_t stream) {
   return p;
 }
 
-void DeviceArena::free(void* p, cudaStream_t stream) {
+void DeviceArena::free(void* p, cudaStream_t stream, std::uint64_t epoch) {
   if (!p) return;
   std::lock_guard<std::mutex> lock(mu_);
   auto it = live_.find(p);
@@ -93,7 +94,7 @@ void DeviceArena::free(void* p, cudaStream_t stream) {
     cudaCheck(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming), "arena: event");
   }
   cudaCheck(cudaEventRecord(ev, stream), "arena: record release");
-  free_[cls].push_back(Block{p, ev});
+  free_[cls].push_back(Block{p, ev, epoch});
   stats_.frees += 1;
   stats_.held_bytes += cls;
 }

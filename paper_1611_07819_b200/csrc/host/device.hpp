@@ -33,10 +33,13 @@ class DeviceArena {
   DeviceArena& operator=(const DeviceArena&) = delete;
 
   // `stream`: the stream that will first touch the block (waits on the
-  // block's release event if it was recycled).
-  void* alloc(std::uint64_t bytes, cudaStream_t stream);
+  // block's release event if it was recycled). With minAge > 0 only blocks
+  // freed at least `minAge` epochs before `epoch` are reused (else a new
+  // block is allocated): per-op temporaries double-buffer, so the next op
+  // can fill its buffer while the current op still reads its own.
+  void* alloc(std::uint64_t bytes, cudaStream_t stream, std::uint64_t epoch = 0, std::uint64_t minAge = 0);
   // `stream`: the stream whose pending work last used the block.
-  void free(void* p, cudaStream_t stream);
+  void free(void* p, cudaStream_t stream, std::uint64_t epoch = 0);
   gm_arena_stats stats() const;
   static std::uint64_t sizeClass(std::uint64_t bytes);
   int device() const { return device_; }
@@ -45,6 +48,7 @@ class DeviceArena {
   struct Block {
     void* ptr;
     cudaEvent_t released;
+    std::uint64_t epoch;
   };
   int device_;
   mutable std::mutex mu_;

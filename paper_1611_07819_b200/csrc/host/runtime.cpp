@@ -1355,6 +1355,7 @@ void Session::execGemm(const OpDescriptor& op) {
   const MatrixDescriptor& C = lookup(table_, op.ids[2]);
   const std::uint32_t P = opts_.workers;
   ++tick_;
+  ++gemmEpoch_;
   Worker* localRef = nullptr;
   for (auto& wp : workers_)
     if (wp) localRef = wp.get();
@@ -1450,7 +1451,8 @@ void Session::execGemm(const OpDescriptor& op) {
         const bool keep = e.bytes <= budget;
         if (w) {
           w->activate();
-          e.ptr = w->arena.alloc(e.bytes, w->comm);
+          // Uncached bands double-buffer across GEMMs (see DeviceArena::alloc).
+          e.ptr = keep ? w->arena.alloc(e.bytes, w->comm) : w->arena.alloc(e.bytes, w->comm, gemmEpoch_, 2);
         }
         CacheEntry* slotp = nullptr;
         if (keep) {
@@ -1624,7 +1626,7 @@ void Session::execGemm(const OpDescriptor& op) {
   });
   for (auto& tp : temps) {
     tp.first->activate();
-    tp.first->arena.free(tp.second, tp.first->compute);
+    tp.first->arena.free(tp.second, tp.first->compute, gemmEpoch_);
   }
   // Group events go back to their pools (waits are already enqueued).
   for (auto& evs : groupDone) {

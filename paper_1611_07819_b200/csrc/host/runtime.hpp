@@ -319,6 +319,7 @@ class Session {
   std::uint64_t nextMatrixId_ = 1;
   std::uint64_t nextExec_ = 1;
   std::uint64_t tick_ = 0;
+  std::uint64_t gemmEpoch_ = 0;  // arena epoch of band temporaries (one per GEMM)
   bool nccl_ = false;
   bool peerCopies_ = false;
   bool ipc_ = false;
