@@ -23,6 +23,14 @@
  * order (every element still accumulates k = 0..K-1 in order), so the
  * restatement is a plain triple loop. Compiled with -ffp-contract=off.
  *
+ * FC-layer neighbours of the GEMM, same conventions:
+ *   runElementwise<T>     src/kernels.cpp:741-815   relu / mulScalar / add /
+ *                         sub / axpy / reluGrad / copy / biasAdd, T from
+ *                         execElementwise :817-829
+ *   runRowColSumDet<T>    src/kernels.cpp:570-614   ascending-index sums,
+ *                         acc = acc + alpha * sum
+ *   execSetConst          src/kernels.cpp:435-443   storeScalar<double>
+ *
  * Precision tags: 0 half, 1 single, 2 double, 3 bf16 (bf16 is not a
  * reference type; it is widened exactly like half and stored RNE via float).
  */
@@ -208,4 +216,98 @@ uint32_t oracle_split(uint64_t n, uint64_t parts, uint64_t* starts, uint64_t* le
     ++cnt;
   }
   return cnt;
+}
+
+/* ---- FC-layer neighbours ---------------------------------------------- */
+
+static void store_f(void* base, int prec, size_t i, float v) { store_d(base, prec, i, (double)v); }
+
+/* Elementwise op over full row-major images (kernels.cpp:741-815).
+ * unary: kind 0 Relu, 1 MulScalar (y unused). binary: kind 0 Add, 1 Sub,
+ * 2 Axpy (alpha*x + y), 3 ReluGrad (x > 0 ? y : 0), 4 Copy, 5 BiasAdd
+ * (x + y[0, j], y is 1 x cols). Compute type: Double iff any of x, y (binary
+ * only), dst is Double (:817-829). dst may alias x or y (elementwise). */
+void oracle_elementwise(int unary, int kind, double alpha, uint64_t rows, uint64_t cols,
+                        const void* x, int xp, const void* y, int yp, void* dst, int dp) {
+  const int dbl = xp == 2 || dp == 2 || (!unary && yp == 2);
+  for (uint64_t i = 0; i < rows; ++i)
+    for (uint64_t j = 0; j < cols; ++j) {
+      const size_t e = (size_t)(i * cols + j);
+      const size_t ye = (!unary && kind == 5) ? (size_t)j : e;
+      if (dbl) {
+        const double xv = load_d(x, xp, e);
+        double out;
+        if (unary) {
+          out = kind == 0 ? (xv > 0.0 ? xv : 0.0) : alpha * xv;
+        } else {
+          const double yv = kind == 4 ? 0.0 : load_d(y, yp, ye);
+          switch (kind) {
+            case 0: out = xv + yv; break;
+            case 1: out = xv - yv; break;
+            case 2: { const double ax = alpha * xv; out = ax + yv; break; }
+            case 3: out = xv > 0.0 ? yv : 0.0; break;
+            case 5: out = xv + yv; break;
+            default: out = xv; break;
+          }
+        }
+        store_d(dst, dp, e, out);
+      } else {
+        const float al = (float)alpha;
+        const float xv = load_f(x, xp, e);
+        float out;
+        if (unary) {
+          out = kind == 0 ? (xv > 0.0f ? xv : 0.0f) : al * xv;
+        } else {
+          const float yv = kind == 4 ? 0.0f : load_f(y, yp, ye);
+          switch (kind) {
+            case 0: out = xv + yv; break;
+            case 1: out = xv - yv; break;
+            case 2: { const float ax = al * xv; out = ax + yv; break; }
+            case 3: out = xv > 0.0f ? yv : 0.0f; break;
+            case 5: out = xv + yv; break;
+            default: out = xv; break;
+          }
+        }
+        store_f(dst, dp, e, out);
+      }
+    }
+}
+
+/* Deterministic addRowColSum (kernels.cpp:570-614): racc[i] += alpha *
+ * sum_j a[i][j], then cacc[j] += alpha * sum_i a[i][j], each sum in
+ * ascending index order in T. racc is rows x 1, cacc is 1 x cols. */
+void oracle_row_col_sum(double alpha, uint64_t rows, uint64_t cols, const void* a, int ap,
+                        void* racc, int rp, void* cacc, int cp) {
+  const int dbl = ap == 2 || rp == 2 || cp == 2;
+  for (uint64_t i = 0; i < rows; ++i) {
+    if (dbl) {
+      double sum = 0.0;
+      for (uint64_t j = 0; j < cols; ++j) sum += load_d(a, ap, (size_t)(i * cols + j));
+      const double cur = load_d(racc, rp, (size_t)i), add = alpha * sum;
+      store_d(racc, rp, (size_t)i, cur + add);
+    } else {
+      float sum = 0.0f;
+      for (uint64_t j = 0; j < cols; ++j) sum += load_f(a, ap, (size_t)(i * cols + j));
+      const float cur = load_f(racc, rp, (size_t)i), add = (float)alpha * sum;
+      store_f(racc, rp, (size_t)i, cur + add);
+    }
+  }
+  for (uint64_t j = 0; j < cols; ++j) {
+    if (dbl) {
+      double sum = 0.0;
+      for (uint64_t i = 0; i < rows; ++i) sum += load_d(a, ap, (size_t)(i * cols + j));
+      const double cur = load_d(cacc, cp, (size_t)j), add = alpha * sum;
+      store_d(cacc, cp, (size_t)j, cur + add);
+    } else {
+      float sum = 0.0f;
+      for (uint64_t i = 0; i < rows; ++i) sum += load_f(a, ap, (size_t)(i * cols + j));
+      const float cur = load_f(cacc, cp, (size_t)j), add = (float)alpha * sum;
+      store_f(cacc, cp, (size_t)j, cur + add);
+    }
+  }
+}
+
+/* execSetConst (kernels.cpp:435-443): storeScalar<double>(value). */
+void oracle_set_const(void* dst, int prec, uint64_t n, double value) {
+  for (uint64_t i = 0; i < n; ++i) store_d(dst, prec, (size_t)i, value);
 }

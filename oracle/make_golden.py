@@ -107,6 +107,82 @@ def build_cases():
     case("c1_like_256", 256, 256, 256, S, S, S, 4, "grid", "grid", "grid")
 
 
+FC_CASES = []
+
+
+def fc_case(name, op, sub, p, shape, xp, lx, yp=None, ly=None, dp=None, ld=None, alpha=0.0, repl=0,
+            special=None):
+    FC_CASES.append(dict(name=name, op=op, sub=sub, p=p, rows=shape[0], cols=shape[1], xp=xp, lx=lx, yp=yp,
+                         ly=ly, dp=dp, ld=ld, alpha=alpha, repl=repl, special=special))
+
+
+def build_fc_cases():
+    # FC-layer neighbours (reference session.cpp:547-609).
+    sh = (67, 45)
+    fc_case("relu_f32_grid_to_row", 0, 0, 4, sh, S, "grid", dp=S, ld="row", special="specials")
+    fc_case("relu_half_p2", 0, 0, 2, sh, H, "row", dp=H, ld="row")
+    fc_case("relu_f64_irregular", 0, 0, 3, sh, D, "irregular", dp=D, ld="col")
+    fc_case("mulscalar_f32", 0, 1, 4, sh, S, "grid", alpha=0.3)
+    fc_case("mulscalar_half", 0, 1, 2, sh, H, "col", alpha=-1.7)
+    fc_case("add_f32_mixed_layouts", 1, 0, 4, sh, S, "grid", S, "row", S, "col")
+    fc_case("sub_half_single_to_half", 1, 1, 3, sh, H, "irregular", S, "grid", H, "row")
+    fc_case("add_f64", 1, 0, 2, sh, D, "row", S, "col", D, "grid")
+    fc_case("axpy_f32", 1, 2, 4, sh, S, "grid", S, "grid", alpha=-0.01)
+    fc_case("axpy_f64_mixed", 1, 2, 3, sh, S, "row", D, "col", alpha=0.125)
+    fc_case("relugrad_f32", 1, 3, 4, sh, S, "grid", S, "grid", special="specials")
+    fc_case("relugrad_half", 1, 3, 2, sh, H, "row", H, "col")
+    fc_case("copy_single_to_half", 1, 4, 4, sh, S, "grid", dp=H, ld="row")
+    fc_case("copy_double_to_single", 1, 4, 2, sh, D, "col", dp=S, ld="grid")
+    fc_case("copy_half_to_double", 1, 4, 3, sh, H, "row", dp=D, ld="irregular")
+    fc_case("biasadd_f32_row", 1, 5, 4, sh, S, "row", S, "col")
+    fc_case("biasadd_f32_replicated", 1, 5, 4, sh, S, "row", S, "col", repl=2)
+    fc_case("biasadd_half_bias_grid_x", 1, 5, 4, sh, S, "grid", H, "single")
+    fc_case("rowcolsum_det_f32", 2, 1, 4, sh, S, "grid", S, "row", S, "col", alpha=1.0)
+    fc_case("rowcolsum_det_f64", 2, 1, 3, sh, D, "irregular", D, "row", S, "col", alpha=-0.5)
+    fc_case("rowcolsum_det_half", 2, 1, 2, sh, H, "row", S, "row", H, "col", alpha=0.25)
+    fc_case("rowcolsum_fast_f32", 2, 0, 4, sh, S, "grid", S, "row", S, "col", alpha=1.0)
+    fc_case("setconst_f32_zero", 3, 0, 4, sh, S, "grid", alpha=0.0)
+    fc_case("setconst_half_overflow", 3, 0, 2, sh, H, "row", alpha=65520.0)
+    fc_case("setconst_f64_pi", 3, 0, 3, sh, D, "irregular", alpha=3.141592653589793)
+    fc_case("setconst_bf16_via_single", 3, 0, 4, sh, S, "col", alpha=1.0 / 3.0)
+
+
+def run_fc_case(c):
+    rows, cols = c["rows"], c["cols"]
+    op, sub = c["op"], c["sub"]
+    x = O.fill_uniform(rows, cols, c["xp"], 11)
+    if c["special"] == "specials":
+        flat = x.reshape(-1)
+        flat[:6] = np.array([np.nan, np.inf, -np.inf, -0.0, 0.0, -1e-30], dtype=flat.dtype)
+    xt = layouts_for(c["lx"], rows, cols, c["p"])
+    y = d = None
+    yt = dt = []
+    if op == 1 and sub == 5:
+        y = O.fill_uniform(1, cols, c["yp"], 12)
+        yt = layouts_for(c["ly"], 1, cols, c["p"])
+    elif op == 2:
+        y = O.fill_uniform(rows, 1, c["yp"], 12)
+        yt = layouts_for(c["ly"], rows, 1, c["p"])
+        d = O.fill_uniform(1, cols, c["dp"], 13)
+        dt = layouts_for(c["ld"], 1, cols, c["p"])
+    elif c["yp"] is not None:
+        y = O.fill_uniform(rows, cols, c["yp"], 12)
+        yt = layouts_for(c["ly"], rows, cols, c["p"])
+    if op in (0, 1) and c["dp"] is not None:
+        d = O.fill_uniform(rows, cols, c["dp"], 13)
+        dt = layouts_for(c["ld"], rows, cols, c["p"])
+    yp = 1 if c["yp"] is None else c["yp"]
+    dp = 1 if c["dp"] is None else c["dp"]
+    res = O.fcop_ref(c["p"], op, sub, c["alpha"], x, c["xp"], xt, y, yp, yt, d, dp, dt, c["repl"])
+    out0, out1 = res if op == 2 else (res, np.zeros(1))
+    arr = dict(x=x, out0=out0, out1=out1, xt=np.array(xt, dtype=np.uint64))
+    if y is not None:
+        arr.update(y=y, yt=np.array(yt, dtype=np.uint64))
+    if d is not None:
+        arr.update(d=d, dt=np.array(dt, dtype=np.uint64))
+    return arr
+
+
 def run_case(c):
     m, n, k = c["m"], c["n"], c["k"]
     ar, ac = (k, m) if c["ta"] else (m, k)
@@ -142,6 +218,12 @@ def main():
         np.savez_compressed(os.path.join(OUT, c["name"] + ".npz"), **arrays)
         index.append({k: v for k, v in c.items()})
         print("golden", c["name"])
+    build_fc_cases()
+    fc_index = []
+    for c in FC_CASES:
+        np.savez_compressed(os.path.join(OUT, "fc_" + c["name"] + ".npz"), **run_fc_case(c))
+        fc_index.append(dict(c))
+        print("golden fc", c["name"])
     # Layout vectors from the reference constructors (layout.cpp:13-75).
     lay = []
     for kind in (0, 1):
@@ -179,9 +261,10 @@ def main():
     O.reflib().gmref_half_to_float(allh.ctypes.data, back.ctypes.data, allh.size)
     np.savez_compressed(os.path.join(OUT, "fp16_codec.npz"), f=f, h=h, all_h=allh, all_f=back)
     with open(os.path.join(OUT, "index.json"), "w") as fh:
-        json.dump(dict(cases=index, layouts=lay, descriptors=desc,
+        json.dump(dict(cases=index, fc_cases=fc_index, layouts=lay, descriptors=desc,
                        generator="oracle/make_golden.py over oracle/_ref/libgmref.so"), fh, indent=1)
-    print("wrote", len(index), "gemm cases,", len(lay), "layouts,", len(desc), "descriptors")
+    print("wrote", len(index), "gemm cases,", len(fc_index), "fc cases,", len(lay), "layouts,", len(desc),
+          "descriptors")
 
 
 if __name__ == "__main__":

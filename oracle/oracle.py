@@ -12,9 +12,10 @@ Two CPU implementations of the reference's GEMM path:
   Session / createMatrix / setData / gemm / getDataRaw API
   (oracle/ref_harness.cpp).
 * ``CLib`` -- oracle/gemm_oracle.c, the plain-C restatement of runGemm<T>
-  (reference src/kernels.cpp:445-558) and of the fp16 codec
-  (include/gridmath/precision.hpp:42-100). Pinned bit-for-bit against the
-  reference by tests/test_oracle.py and tests/golden/.
+  (reference src/kernels.cpp:445-558), of the FC-layer neighbours
+  (runElementwise :741-815, runRowColSumDet :570-614, execSetConst :435-443)
+  and of the fp16 codec (include/gridmath/precision.hpp:42-100). Pinned
+  bit-for-bit against the reference by tests/test_oracle.py and tests/golden/.
 """
 from __future__ import annotations
 
@@ -64,6 +65,11 @@ def clib():
                                             c_double, c_double]
         lib.oracle_split.argtypes = [c_uint64, c_uint64, POINTER(c_uint64), POINTER(c_uint64)]
         lib.oracle_split.restype = c_uint32
+        lib.oracle_elementwise.argtypes = [c_int32, c_int32, c_double, c_uint64, c_uint64, c_void_p,
+                                           c_int32, c_void_p, c_int32, c_void_p, c_int32]
+        lib.oracle_row_col_sum.argtypes = [c_double, c_uint64, c_uint64, c_void_p, c_int32, c_void_p,
+                                           c_int32, c_void_p, c_int32]
+        lib.oracle_set_const.argtypes = [c_void_p, c_int32, c_uint64, c_double]
         _c = lib
     return _c
 
@@ -92,6 +98,11 @@ def reflib():
         lib.gmref_encode_descriptor.argtypes = [c_uint64, c_uint64, c_uint64, c_int32, c_uint64, T,
                                                 c_uint32, POINTER(ctypes.c_uint8), c_uint32,
                                                 POINTER(c_uint32)]
+        lib.gmref_fcop.argtypes = [c_uint32, c_int32, c_int32, c_double,
+                                   c_uint64, c_uint64, c_int32, T, c_uint32, c_void_p,
+                                   c_uint64, c_uint64, c_int32, T, c_uint32, c_void_p,
+                                   c_uint64, c_uint64, c_int32, T, c_uint32, c_void_p,
+                                   c_int32, c_void_p, c_void_p, c_char_p, c_size_t]
         lib.gmref_float_to_half.argtypes = [c_void_p, c_void_p, c_uint64]
         lib.gmref_half_to_float.argtypes = [c_void_p, c_void_p, c_uint64]
         _ref = lib
@@ -149,6 +160,68 @@ def gemm_ref(workers, a, pa, a_tiles, b, pb, b_tiles, c, pc, c_tiles, alpha, bet
     if rc:
         raise RuntimeError("reference gemm failed: " + err.value.decode())
     return out, secs.value
+
+
+# ---------------------------------------------------------------- FC-layer neighbours
+# op codes shared with oracle/ref_harness.cpp gmref_fcop: 0 EwUnary (kind 0 relu,
+# 1 mulScalar), 1 EwBinary (0 add, 1 sub, 2 axpy, 3 reluGrad, 4 copy, 5 biasAdd),
+# 2 addRowColSum, 3 setConst.
+
+def ew_c(unary, kind, alpha, x, xp, y, yp, dst, dp):
+    """C restatement of one elementwise op; returns the new dst image (dst is
+    only used for its shape/precision; aliasing is the caller's choice of x/y)."""
+    x = np.ascontiguousarray(x)
+    y = np.ascontiguousarray(y) if y is not None else None
+    out = np.ascontiguousarray(dst).copy()
+    clib().oracle_elementwise(1 if unary else 0, kind, alpha, out.shape[0], out.shape[1], x.ctypes.data, xp,
+                              y.ctypes.data if y is not None else None, yp if y is not None else 1,
+                              out.ctypes.data, dp)
+    return out
+
+
+def rowcolsum_c(alpha, a, ap, racc, rp, cacc, cp):
+    a = np.ascontiguousarray(a)
+    r = np.ascontiguousarray(racc).copy()
+    c = np.ascontiguousarray(cacc).copy()
+    clib().oracle_row_col_sum(alpha, a.shape[0], a.shape[1], a.ctypes.data, ap, r.ctypes.data, rp,
+                              c.ctypes.data, cp)
+    return r, c
+
+
+def set_const_c(shape, prec, value):
+    out = np.empty(shape, dtype=NP_DTYPE[prec])
+    clib().oracle_set_const(out.ctypes.data, prec, out.size, value)
+    return out
+
+
+def fcop_ref(workers, op, sub, alpha, x, xp, x_tiles, y=None, yp=1, y_tiles=(), d=None, dp=1, d_tiles=(),
+             replicate_mask=0):
+    """Runs one FC-layer neighbour through the unmodified reference Session.
+    Returns the result image (op 2: (rowAcc, colAcc))."""
+    lib = reflib()
+    x = np.ascontiguousarray(x)
+    y = np.ascontiguousarray(y) if y is not None else None
+    d = np.ascontiguousarray(d) if d is not None else None
+    if op == 0:
+        out0 = np.empty_like(d if sub == 0 else x)
+    elif op == 1:
+        out0 = np.empty_like({2: y, 3: y, 5: x}.get(sub, d))
+    elif op == 2:
+        out0 = np.empty_like(y)
+    else:
+        out0 = np.empty_like(x)
+    out1 = np.empty_like(d) if op == 2 else np.empty(1, np.uint8)
+    err = ctypes.create_string_buffer(512)
+    yr, yc = (y.shape if y is not None else (0, 0))
+    dr, dc = (d.shape if d is not None else (0, 0))
+    rc = lib.gmref_fcop(workers, op, sub, alpha,
+                        x.shape[0], x.shape[1], xp, tiles_array(x_tiles), len(x_tiles), x.ctypes.data,
+                        yr, yc, yp, tiles_array(list(y_tiles)), len(y_tiles), y.ctypes.data if y is not None else None,
+                        dr, dc, dp, tiles_array(list(d_tiles)), len(d_tiles), d.ctypes.data if d is not None else None,
+                        replicate_mask, out0.ctypes.data, out1.ctypes.data, err, 512)
+    if rc:
+        raise RuntimeError("reference op failed: " + err.value.decode())
+    return (out0, out1) if op == 2 else out0
 
 
 def plan_remote_bytes(workers, a_shape, pa, a_tiles, b_shape, pb, b_tiles, c_shape, pc, c_tiles,

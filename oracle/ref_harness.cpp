@@ -10,6 +10,8 @@
 //   setData(m, vector<double>)                             session.hpp:72
 //   gemm(s, A, B, C, alpha, beta, transA, transB)          session.hpp:161
 //   replicateSync / getDataRaw                             session.hpp:75,82
+//   relu / mulScalar / add / sub / axpy / reluGrad / biasAdd /
+//   copyMatrix / setConst / addRowColSum                   session.hpp:163-177
 // and calls fabric().closeAll() before the Session dies (its destructor
 // otherwise deadlocks, session.cpp:57-63 vs worker.cpp:56).
 //
@@ -120,6 +122,75 @@ int gmref_gemm(uint32_t workers, int32_t deterministic, uint64_t ar, uint64_t ac
       if (gemm_seconds) *gemm_seconds = std::chrono::duration<double>(t1 - t0).count();
       const std::vector<uint8_t> raw = s.getDataRaw(C);
       std::memcpy(c_out, raw.data(), raw.size());
+    } catch (const std::exception& e) {
+      setErr(err, errcap, e.what());
+      rc = 1;
+    }
+    s.fabric().closeAll();
+    return rc;
+  } catch (const std::exception& e) {
+    setErr(err, errcap, e.what());
+    return 1;
+  }
+}
+
+// One FC-layer neighbour op through the reference Session (public free
+// functions, session.cpp:547-609). op: 0 EwUnary (sub: 0 relu(x, d),
+// 1 mulScalar(x, alpha) in place), 1 EwBinary (sub: 0 add(x, y, d),
+// 1 sub(x, y, d), 2 axpy(alpha, x, y) -> y, 3 reluGrad(x, y) -> y,
+// 4 copyMatrix(x, d), 5 biasAdd(x, y) -> x), 2 addRowColSum(x, y = rowAcc,
+// d = colAcc, alpha, sub = deterministic), 3 setConst(x, alpha).
+// Matrices with rows == 0 are not created. out0 = result image (op 2: rowAcc),
+// out1 = colAcc (op 2 only). replicate_mask bit0/bit1: replicateSync(x)/(y).
+int gmref_fcop(uint32_t workers, int32_t op, int32_t sub, double alpha, uint64_t xr, uint64_t xc,
+               int32_t xp, const HTile* xt, uint32_t xn, const void* x, uint64_t yr, uint64_t yc,
+               int32_t yp, const HTile* yt, uint32_t yn, const void* y, uint64_t dr, uint64_t dc,
+               int32_t dp, const HTile* dt, uint32_t dn, const void* d, int32_t replicate_mask,
+               void* out0, void* out1, char* err, size_t errcap) {
+  try {
+    SessionOptions opts;
+    opts.workers = workers;
+    Session s(opts);
+    int rc = 0;
+    try {
+      auto make = [&](uint64_t r, uint64_t c, int32_t p, const HTile* t, uint32_t n, const void* img) {
+        const Precision pp = precisionFromTag(static_cast<uint8_t>(p));
+        DistMatrix m = s.createMatrix(r, c, pp, toLayout(t, n));
+        s.setData(m, rawToDouble(img, pp, r * c));
+        return m;
+      };
+      DistMatrix X = make(xr, xc, xp, xt, xn, x);
+      DistMatrix Y, D;
+      if (yr) Y = make(yr, yc, yp, yt, yn, y);
+      if (dr) D = make(dr, dc, dp, dt, dn, d);
+      if (replicate_mask & 1) s.replicateSync(X);
+      if ((replicate_mask & 2) && yr) s.replicateSync(Y);
+      DistMatrix out = X, out2;
+      if (op == 0) {
+        if (sub == 0) { relu(s, X, D); out = D; }
+        else mulScalar(s, X, alpha);
+      } else if (op == 1) {
+        switch (sub) {
+          case 0: addMatrices(s, X, Y, D); out = D; break;
+          case 1: subMatrices(s, X, Y, D); out = D; break;
+          case 2: axpy(s, alpha, X, Y); out = Y; break;
+          case 3: reluGrad(s, X, Y); out = Y; break;
+          case 4: copyMatrix(s, X, D); out = D; break;
+          default: biasAdd(s, X, Y); out = X; break;
+        }
+      } else if (op == 2) {
+        addRowColSum(s, X, Y, D, alpha, sub != 0);
+        out = Y;
+        out2 = D;
+      } else {
+        setConst(s, X, alpha);
+      }
+      const std::vector<uint8_t> raw = s.getDataRaw(out);
+      std::memcpy(out0, raw.data(), raw.size());
+      if (op == 2) {
+        const std::vector<uint8_t> raw2 = s.getDataRaw(out2);
+        std::memcpy(out1, raw2.data(), raw2.size());
+      }
     } catch (const std::exception& e) {
       setErr(err, errcap, e.what());
       rc = 1;
