@@ -250,6 +250,37 @@ int gm_gemm_async(gm_session* s, uint64_t a, uint64_t b, uint64_t c, double alph
                   int32_t trans_a, int32_t trans_b);
 int gm_session_synchronize(gm_session* s);
 
+/* FC-layer neighbours of the GEMM (reference session.hpp:163-174; SURVEY
+ * 8(f)2), synchronous like gm_gemm. The owner of each destination tile
+ * computes it on its GPU; operands in other layouts are gathered like GEMM
+ * panels (replica, own tile, panel cache, else copy-engine pulls). Compute
+ * type: double iff any operand is Double, else float (kernels.cpp:136-140);
+ * results are bit-for-bit the reference's (except subnormal Half inputs,
+ * which the device widens IEEE-exactly). */
+int gm_set_const(gm_session* s, uint64_t m, double value);                     /* session.cpp:603-608 */
+int gm_add_row_col_sum(gm_session* s, uint64_t a, uint64_t row_acc, uint64_t col_acc,
+                       double alpha, int32_t deterministic);                   /* session.cpp:547-556 */
+int gm_relu(gm_session* s, uint64_t x, uint64_t dst);                          /* session.cpp:580 */
+int gm_mul_scalar(gm_session* s, uint64_t x, double alpha);                    /* session.cpp:581-583 */
+int gm_add_matrices(gm_session* s, uint64_t x, uint64_t y, uint64_t dst);      /* session.cpp:584-586 */
+int gm_sub_matrices(gm_session* s, uint64_t x, uint64_t y, uint64_t dst);      /* session.cpp:587-589 */
+int gm_axpy(gm_session* s, double alpha, uint64_t x, uint64_t y);              /* session.cpp:590-592 */
+int gm_relu_grad(gm_session* s, uint64_t preact, uint64_t grad);               /* session.cpp:593-595 */
+int gm_bias_add(gm_session* s, uint64_t x, uint64_t bias);                     /* session.cpp:596-598 */
+int gm_copy_matrix(gm_session* s, uint64_t src, uint64_t dst);                 /* session.cpp:599-601 */
+int gm_cast_precision(gm_session* s, uint64_t src, uint64_t dst);              /* session.cpp:602 */
+/* Issue one wire op (reference OpDescriptor, ops.hpp:47-60: opcode numbering
+ * of OpCode, ids[4], s0, s1, flags[4]) for the device-path opcodes Gemm,
+ * SetConst, EwUnary, EwBinary, AddRowColSum. sync = 0: stream-ordered only
+ * (pair with gm_session_synchronize). */
+#define GM_OP_SET_CONST 5
+#define GM_OP_GEMM 6
+#define GM_OP_ADD_ROW_COL_SUM 7
+#define GM_OP_EW_UNARY 8
+#define GM_OP_EW_BINARY 9
+int gm_op_issue(gm_session* s, int32_t opcode, const uint64_t ids[4], double s0, double s1,
+                const uint8_t flags[4], int32_t sync);
+
 /* Replication (session.hpp:81-84). */
 int gm_replicate_async(gm_session* s, uint64_t id, uint64_t* version);
 int gm_replicate_sync(gm_session* s, uint64_t id);

@@ -18,6 +18,7 @@ LIB_PATH = os.path.join(_HERE, "libgridmath_b200.so")
 GM_HALF, GM_SINGLE, GM_DOUBLE, GM_BF16 = 0, 1, 2, 3
 GM_MATH_DEFAULT, GM_MATH_TF32 = 0, 1
 GM_REPL_IN_FLIGHT, GM_REPL_DONE, GM_REPL_FAILED = 0, 1, 2
+GM_OP_SET_CONST, GM_OP_GEMM, GM_OP_ADD_ROW_COL_SUM, GM_OP_EW_UNARY, GM_OP_EW_BINARY = 5, 6, 7, 8, 9
 
 
 class GmError(RuntimeError):
@@ -124,6 +125,18 @@ _SIGNATURES = {
                     c_int32, c_int32], c_int32),
     "gm_gemm_async": ([c_void_p, c_uint64, c_uint64, c_uint64, c_double, c_double, c_int32,
                        c_int32], c_int32),
+    "gm_set_const": ([c_void_p, c_uint64, c_double], c_int32),
+    "gm_add_row_col_sum": ([c_void_p, c_uint64, c_uint64, c_uint64, c_double, c_int32], c_int32),
+    "gm_relu": ([c_void_p, c_uint64, c_uint64], c_int32),
+    "gm_mul_scalar": ([c_void_p, c_uint64, c_double], c_int32),
+    "gm_add_matrices": ([c_void_p, c_uint64, c_uint64, c_uint64], c_int32),
+    "gm_sub_matrices": ([c_void_p, c_uint64, c_uint64, c_uint64], c_int32),
+    "gm_axpy": ([c_void_p, c_double, c_uint64, c_uint64], c_int32),
+    "gm_relu_grad": ([c_void_p, c_uint64, c_uint64], c_int32),
+    "gm_bias_add": ([c_void_p, c_uint64, c_uint64], c_int32),
+    "gm_copy_matrix": ([c_void_p, c_uint64, c_uint64], c_int32),
+    "gm_cast_precision": ([c_void_p, c_uint64, c_uint64], c_int32),
+    "gm_op_issue": ([c_void_p, c_int32, _P(c_uint64), c_double, c_double, _P(c_uint8), c_int32], c_int32),
     "gm_session_synchronize": ([c_void_p], c_int32),
     "gm_replicate_async": ([c_void_p, c_uint64, _P(c_uint64)], c_int32),
     "gm_replicate_sync": ([c_void_p, c_uint64], c_int32),

@@ -185,6 +185,76 @@ int gm_gemm(gm_session* s, uint64_t a, uint64_t b, uint64_t c, double alpha, dou
   return guard([&] { s->s->runGemm(gemmOp(s, a, b, c, alpha, beta, trans_a, trans_b, 0), true); });
 }
 
+// FC-layer neighbours (reference session.hpp:163-174 / session.cpp:547-609).
+int gm_set_const(gm_session* s, uint64_t m, double value) {
+  return guard([&] { gridmath::setConst(*s->s, handle(s, m), value); });
+}
+
+int gm_add_row_col_sum(gm_session* s, uint64_t a, uint64_t row_acc, uint64_t col_acc, double alpha,
+                       int32_t deterministic) {
+  return guard([&] {
+    gridmath::addRowColSum(*s->s, handle(s, a), handle(s, row_acc), handle(s, col_acc), alpha, deterministic != 0);
+  });
+}
+
+int gm_relu(gm_session* s, uint64_t x, uint64_t dst) {
+  return guard([&] { gridmath::relu(*s->s, handle(s, x), handle(s, dst)); });
+}
+
+int gm_mul_scalar(gm_session* s, uint64_t x, double alpha) {
+  return guard([&] { gridmath::mulScalar(*s->s, handle(s, x), alpha); });
+}
+
+int gm_add_matrices(gm_session* s, uint64_t x, uint64_t y, uint64_t dst) {
+  return guard([&] { gridmath::addMatrices(*s->s, handle(s, x), handle(s, y), handle(s, dst)); });
+}
+
+int gm_sub_matrices(gm_session* s, uint64_t x, uint64_t y, uint64_t dst) {
+  return guard([&] { gridmath::subMatrices(*s->s, handle(s, x), handle(s, y), handle(s, dst)); });
+}
+
+int gm_axpy(gm_session* s, double alpha, uint64_t x, uint64_t y) {
+  return guard([&] { gridmath::axpy(*s->s, alpha, handle(s, x), handle(s, y)); });
+}
+
+int gm_relu_grad(gm_session* s, uint64_t preact, uint64_t grad) {
+  return guard([&] { gridmath::reluGrad(*s->s, handle(s, preact), handle(s, grad)); });
+}
+
+int gm_bias_add(gm_session* s, uint64_t x, uint64_t bias) {
+  return guard([&] { gridmath::biasAdd(*s->s, handle(s, x), handle(s, bias)); });
+}
+
+int gm_copy_matrix(gm_session* s, uint64_t src, uint64_t dst) {
+  return guard([&] { gridmath::copyMatrix(*s->s, handle(s, src), handle(s, dst)); });
+}
+
+int gm_cast_precision(gm_session* s, uint64_t src, uint64_t dst) {
+  return guard([&] { gridmath::castPrecision(*s->s, handle(s, src), handle(s, dst)); });
+}
+
+int gm_op_issue(gm_session* s, int32_t opcode, const uint64_t ids[4], double s0, double s1,
+                const uint8_t flags[4], int32_t sync) {
+  return guard([&] {
+    gridmath::OpDescriptor op;
+    op.opcode = static_cast<gridmath::OpCode>(opcode);
+    for (int i = 0; i < 4; ++i) {
+      op.ids[i] = ids ? ids[i] : 0;
+      op.flags[i] = flags ? flags[i] : 0;
+    }
+    op.s0 = s0;
+    op.s1 = s1;
+    switch (op.opcode) {
+      case gridmath::OpCode::Gemm: s->s->runGemm(op, sync != 0); break;
+      case gridmath::OpCode::SetConst:
+      case gridmath::OpCode::EwUnary:
+      case gridmath::OpCode::EwBinary:
+      case gridmath::OpCode::AddRowColSum: s->s->runPointwise(op, sync != 0); break;
+      default: throw gridmath::Error("gm_op_issue: opcode " + std::to_string(opcode) + " not on the device path");
+    }
+  });
+}
+
 int gm_gemm_ex(gm_session* s, uint64_t a, uint64_t b, uint64_t c, double alpha, double beta,
                int32_t trans_a, int32_t trans_b, int32_t math) {
   return guard([&] { s->s->runGemm(gemmOp(s, a, b, c, alpha, beta, trans_a, trans_b, math), true); });

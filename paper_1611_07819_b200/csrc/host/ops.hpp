@@ -41,6 +41,10 @@ enum class OpCode : std::uint32_t {
   Shutdown,
 };
 
+// Elementwise kinds in flags[0] (reference ops.hpp:41-42).
+enum class UnaryKind : std::uint8_t { Relu = 0, MulScalar = 1 };
+enum class BinaryKind : std::uint8_t { Add = 0, Sub = 1, Axpy = 2, ReluGrad = 3, Copy = 4, BiasAdd = 5 };
+
 struct OpDescriptor {
   std::uint64_t execId = 0;
   std::uint64_t recordPipeline = 0;

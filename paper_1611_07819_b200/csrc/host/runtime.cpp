@@ -24,12 +24,11 @@
 #include <cstring>
 
 #include "../cuda/convert.h"
+#include "internal.hpp"
 
 namespace gridmath {
 
 namespace {
-
-constexpr std::uint64_t kPitchAlign = 16;  // TMA row-stride rule
 
 // SPMD flag page: written[kSlots], readDone[2][kSlots] (comm, compute).
 constexpr std::uint32_t kSlots = 16384;
@@ -76,10 +75,6 @@ struct IpcRecord {
 };
 static_assert(sizeof(IpcRecord) == 88, "ipc record layout");
 
-std::uint64_t paddedLd(std::uint64_t cols, std::uint64_t eb) {
-  return ((cols * eb + kPitchAlign - 1) / kPitchAlign * kPitchAlign) / eb;
-}
-
 void ncclCheck(ncclResult_t r, const char* what) {
   if (r != ncclSuccess) throw Error(std::string(what) + ": " + ncclGetErrorString(r));
 }
@@ -100,17 +95,13 @@ std::vector<Interval> mergeIntervals(std::vector<Interval> v) {
   return out;
 }
 
-const MatrixDescriptor& lookup(const DescriptorTable& t, std::uint64_t id) {
-  auto it = t.find(id);
-  if (it == t.end()) throw Error("unknown matrix id " + std::to_string(id));
-  return it->second;
-}
-
 void requireDistinct(const OpDescriptor& op, std::initializer_list<int> slots) {
   for (int i : slots)
     for (int j : slots)
       if (i != j && op.ids[i] == op.ids[j]) throw Error("operands must be distinct matrices");
 }
+
+}  // namespace
 
 // Master-side checks before anything is issued (reference kernels.cpp:265-379).
 void validateOp(const DescriptorTable& t, const OpDescriptor& op, std::uint32_t workers) {
@@ -154,6 +145,38 @@ void validateOp(const DescriptorTable& t, const OpDescriptor& op, std::uint32_t 
                     std::to_string(c.rows) + "x" + std::to_string(c.cols) + ")");
       return;
     }
+    case OpCode::SetConst:
+      (void)lookup(t, op.ids[0]);
+      return;
+    case OpCode::AddRowColSum: {
+      const MatrixDescriptor& a = lookup(t, op.ids[0]);
+      const MatrixDescriptor& row = lookup(t, op.ids[1]);
+      const MatrixDescriptor& col = lookup(t, op.ids[2]);
+      requireDistinct(op, {0, 1, 2});
+      if (row.rows != a.rows || row.cols != 1) throw Error("addRowColSum: rowAcc must be rows x 1");
+      if (col.rows != 1 || col.cols != a.cols) throw Error("addRowColSum: colAcc must be 1 x cols");
+      return;
+    }
+    case OpCode::EwUnary: {
+      const MatrixDescriptor& x = lookup(t, op.ids[0]);
+      const MatrixDescriptor& d = lookup(t, op.ids[1]);
+      if (x.rows != d.rows || x.cols != d.cols) throw Error("elementwise: shape mismatch");
+      return;
+    }
+    case OpCode::EwBinary: {
+      const MatrixDescriptor& x = lookup(t, op.ids[0]);
+      const MatrixDescriptor& y = lookup(t, op.ids[1]);
+      const MatrixDescriptor& d = lookup(t, op.ids[2]);
+      const auto kind = static_cast<BinaryKind>(op.flags[0]);
+      if (op.flags[0] > static_cast<std::uint8_t>(BinaryKind::BiasAdd)) throw Error("bad elementwise kind");
+      if (kind == BinaryKind::BiasAdd) {
+        if (y.rows != 1 || y.cols != x.cols) throw Error("biasAdd: bias must be 1 x cols");
+      } else if (kind != BinaryKind::Copy && (x.rows != y.rows || x.cols != y.cols)) {
+        throw Error("elementwise: shape mismatch");
+      }
+      if (x.rows != d.rows || x.cols != d.cols) throw Error("elementwise: shape mismatch");
+      return;
+    }
     case OpCode::MetaChecksum:
     case OpCode::QueryStats:
       return;
@@ -162,10 +185,7 @@ void validateOp(const DescriptorTable& t, const OpDescriptor& op, std::uint32_t 
   }
 }
 
-BandView offsetView(const void* base, std::uint64_t ld, std::uint64_t r, std::uint64_t c,
-                    std::uint64_t eb) {
-  return {static_cast<const std::uint8_t*>(base) + (r * ld + c) * eb, ld};
-}
+namespace {
 
 }  // namespace
 

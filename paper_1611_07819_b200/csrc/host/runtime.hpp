@@ -277,6 +277,10 @@ class Session {
   // Issues a Gemm op (gemm() below wraps it). sync: wait for completion
   // like the reference's acked gemm(); otherwise stream-ordered only.
   void runGemm(const OpDescriptor& op, bool sync);
+  // FC-layer neighbours on device (reference session.cpp:547-609,
+  // kernels.cpp:435-815): SetConst, EwUnary, EwBinary, AddRowColSum.
+  // Same sync contract as runGemm.
+  void runPointwise(const OpDescriptor& op, bool sync);
   void synchronize();
   std::vector<float> lastOpDeviceMs();
   std::vector<float> lastOpKernelMs();
@@ -295,6 +299,18 @@ class Session {
   void execDestroy(std::uint64_t id);
   void execGemm(const OpDescriptor& op);
   void execReplicate(std::uint64_t id);
+  void execSetConst(const OpDescriptor& op);
+  // A read of `rect` of a matrix by `worker` (reference NeedPlanner::addNeed
+  // with allowReplica, pieces.cpp:14-30): resolved to the local replica, a
+  // containing local tile, a cached panel, or a gather into a dense temp.
+  struct ReadNeed {
+    std::uint32_t worker = 0;
+    std::uint64_t matrix = 0;
+    Rect rect;
+    BandView view;  // filled for local workers
+  };
+  void resolveReads(std::vector<ReadNeed>& needs, std::uint64_t mutated, std::vector<Xfer>& xs,
+                    std::vector<std::pair<Worker*, void*>>& temps);
   void mutationHook(std::uint64_t id, std::uint64_t oldVersion);
   void exchange(std::vector<Xfer>& xs, bool onComm, bool commit = true);
   // --- RAW/WAR bookkeeping shared by the planes
@@ -340,5 +356,18 @@ class Session {
 
 void gemm(Session& s, DistMatrix a, DistMatrix b, DistMatrix c, double alpha, double beta,
           bool transA = false, bool transB = false);
+// FC-layer neighbours (reference session.hpp:163-174, same signatures).
+void addRowColSum(Session& s, DistMatrix a, DistMatrix rowAcc, DistMatrix colAcc, double alpha,
+                  bool deterministic);
+void relu(Session& s, DistMatrix x, DistMatrix dst);
+void mulScalar(Session& s, DistMatrix x, double alpha);
+void addMatrices(Session& s, DistMatrix x, DistMatrix y, DistMatrix dst);
+void subMatrices(Session& s, DistMatrix x, DistMatrix y, DistMatrix dst);
+void axpy(Session& s, double alpha, DistMatrix x, DistMatrix y);
+void reluGrad(Session& s, DistMatrix preact, DistMatrix grad);
+void biasAdd(Session& s, DistMatrix x, DistMatrix bias);
+void copyMatrix(Session& s, DistMatrix src, DistMatrix dst);
+void castPrecision(Session& s, DistMatrix src, DistMatrix dst);
+void setConst(Session& s, DistMatrix m, double value);
 
 }  // namespace gridmath

@@ -343,6 +343,12 @@ class Session:
                   transA=False, transB=False):
         check(_lib.load().gm_gemm_async(self._h, a.id, b.id, c.id, alpha, beta, int(transA), int(transB)))
 
+    def opIssue(self, opcode: int, ids, s0: float = 0.0, s1: float = 0.0, flags=(0, 0, 0, 0), sync: bool = False):
+        """Issue one wire op (reference OpDescriptor) on the device path."""
+        ids4 = (ctypes.c_uint64 * 4)(*(list(ids) + [0] * (4 - len(ids))))
+        fl4 = (ctypes.c_uint8 * 4)(*(list(flags) + [0] * (4 - len(flags))))
+        check(_lib.load().gm_op_issue(self._h, opcode, ids4, s0, s1, fl4, int(sync)))
+
 
 def kernel_launches() -> int:
     n = ctypes.c_uint64()
@@ -354,3 +360,50 @@ def gemm(s: Session, a: DistMatrix, b: DistMatrix, c: DistMatrix, alpha: float, 
          transA: bool = False, transB: bool = False, math: int = _lib.GM_MATH_DEFAULT):
     """gridmath::gemm (session.hpp:161-162): C = alpha*op(A)*op(B) + beta*C."""
     check(_lib.load().gm_gemm_ex(s._h, a.id, b.id, c.id, alpha, beta, int(transA), int(transB), math))
+
+
+# --- FC-layer neighbours (reference session.hpp:163-174, same names) ----------
+
+def addRowColSum(s: Session, a: DistMatrix, rowAcc: DistMatrix, colAcc: DistMatrix, alpha: float,
+                 deterministic: bool):
+    check(_lib.load().gm_add_row_col_sum(s._h, a.id, rowAcc.id, colAcc.id, alpha, int(deterministic)))
+
+
+def relu(s: Session, x: DistMatrix, dst: DistMatrix):
+    check(_lib.load().gm_relu(s._h, x.id, dst.id))
+
+
+def mulScalar(s: Session, x: DistMatrix, alpha: float):
+    check(_lib.load().gm_mul_scalar(s._h, x.id, alpha))
+
+
+def addMatrices(s: Session, x: DistMatrix, y: DistMatrix, dst: DistMatrix):
+    check(_lib.load().gm_add_matrices(s._h, x.id, y.id, dst.id))
+
+
+def subMatrices(s: Session, x: DistMatrix, y: DistMatrix, dst: DistMatrix):
+    check(_lib.load().gm_sub_matrices(s._h, x.id, y.id, dst.id))
+
+
+def axpy(s: Session, alpha: float, x: DistMatrix, y: DistMatrix):
+    check(_lib.load().gm_axpy(s._h, alpha, x.id, y.id))
+
+
+def reluGrad(s: Session, preact: DistMatrix, grad: DistMatrix):
+    check(_lib.load().gm_relu_grad(s._h, preact.id, grad.id))
+
+
+def biasAdd(s: Session, x: DistMatrix, bias: DistMatrix):
+    check(_lib.load().gm_bias_add(s._h, x.id, bias.id))
+
+
+def copyMatrix(s: Session, src: DistMatrix, dst: DistMatrix):
+    check(_lib.load().gm_copy_matrix(s._h, src.id, dst.id))
+
+
+def castPrecision(s: Session, src: DistMatrix, dst: DistMatrix):
+    check(_lib.load().gm_cast_precision(s._h, src.id, dst.id))
+
+
+def setConst(s: Session, m: DistMatrix, value: float):
+    check(_lib.load().gm_set_const(s._h, m.id, value))
