@@ -411,26 +411,53 @@ def run_extra_config(args):
     g = G.makeWorkerGroup(world)
     s = G.Session(workers=world, spmd_rank=rank if world > 1 else -1, devices=[local], nccl_id=nccl_id)
     if args.config == "fc":
+        # One hidden FC layer of the reference Trainer (dnn.cpp:87-194), every
+        # op on the device path: forward (gemm reads the W replica, biasAdd,
+        # relu), backward (reluGrad, dW = X^T.delta, db = colsum(delta) served
+        # from the panel cache of the dW gather, dX = delta.W^T from the
+        # replica), SGD update (axpy on W and b) and the re-replication of the
+        # new W and b that the next step's forward reads.
         batch, fi, fo = 4096, 9216, 4096
-        X = s.createMatrix(batch, fi, G.Precision.BF16, G.makeRowBlockLayout(batch, fi, g))
-        W = s.createMatrix(fi, fo, G.Precision.BF16, G.makeColBlockLayout(fi, fo, g))
-        Y = s.createMatrix(batch, fo, G.Precision.BF16, G.makeRowBlockLayout(batch, fo, g))
-        D = s.createMatrix(batch, fo, G.Precision.BF16, G.makeRowBlockLayout(batch, fo, g))
-        dW = s.createMatrix(fi, fo, G.Precision.BF16, G.makeColBlockLayout(fi, fo, g))
-        dX = s.createMatrix(batch, fi, G.Precision.BF16, G.makeRowBlockLayout(batch, fi, g))
-        s.fillUniform(X, 1)
-        s.fillUniform(D, 3)
+        P = G.Precision.BF16
+        X = s.createMatrix(batch, fi, P, G.makeRowBlockLayout(batch, fi, g))
+        W = s.createMatrix(fi, fo, P, G.makeColBlockLayout(fi, fo, g))
+        Bv = s.createMatrix(1, fo, P, G.makeColBlockLayout(1, fo, g))
+        Z = s.createMatrix(batch, fo, P, G.makeRowBlockLayout(batch, fo, g))
+        ACT = s.createMatrix(batch, fo, P, G.makeRowBlockLayout(batch, fo, g))
+        DL = s.createMatrix(batch, fo, P, G.makeRowBlockLayout(batch, fo, g))
+        dW = s.createMatrix(fi, fo, P, G.makeColBlockLayout(fi, fo, g))
+        dB = s.createMatrix(1, fo, P, G.makeColBlockLayout(1, fo, g))
+        ROW = s.createMatrix(batch, 1, P, G.makeRowBlockLayout(batch, 1, g))
+        dX = s.createMatrix(batch, fi, P, G.makeRowBlockLayout(batch, fi, g))
         bound = 1.0 / math.sqrt(fi)
+        s.fillUniform(X, 1)
+        s.fillUniform(W, 2, -bound, bound)
+        s.fillUniform(Bv, 3, -0.1, 0.1)
+        s.replicateAsync(W)
+        s.replicateAsync(Bv)
+        lr = 1e-3
+        SC, GE, RCS, EU, EB = 5, 6, 7, 8, 9
 
         def step(i):
-            s.fillUniform(W, 100 + i, -bound, bound)  # stand-in for the SGD update (new W version)
-            s.replicateAsync(W)                       # W replicated to every worker (async)
-            s.gemmAsync(X, W, Y)                      # forward reads the replica
-            s.gemmAsync(X, D, dW, 1.0, 0.0, True, False)   # dW = X^T dY (gathers X)
-            s.gemmAsync(D, W, dX, 1.0, 0.0, False, True)   # dX = dY W^T (replica again)
+            s.fillUniform(DL, 1000 + i)                           # upstream gradient dAct (synthetic)
+            s.gemmAsync(X, W, Z)                                   # z = x.W (W replica)
+            s.opIssue(EB, [Z.id, Bv.id, Z.id], flags=(5,))         # biasAdd (bias replica)
+            s.opIssue(EU, [Z.id, ACT.id], flags=(0,))              # act = relu(z)
+            s.opIssue(EB, [Z.id, DL.id, DL.id], flags=(3,))        # delta = reluGrad(z, dAct)
+            s.gemmAsync(X, DL, dW, 1.0, 0.0, True, False)          # dW = x^T.delta (gathers delta bands)
+            s.opIssue(SC, [ROW.id], 0.0)
+            s.opIssue(SC, [dB.id], 0.0)
+            s.opIssue(RCS, [DL.id, ROW.id, dB.id], 1.0, flags=(1,))  # db: same bands (panel cache)
+            s.gemmAsync(DL, W, dX, 1.0, 0.0, False, True)          # dX = delta.W^T (W replica)
+            s.opIssue(EB, [dW.id, W.id, W.id], -lr, flags=(2,))    # W -= lr dW
+            s.opIssue(EB, [dB.id, Bv.id, Bv.id], -lr, flags=(2,))  # b -= lr db
+            s.replicateAsync(W)                                    # next step's forward reads these
+            s.replicateAsync(Bv)
 
         flops = 3 * 2.0 * batch * fi * fo
-        workload = f"FC fwd+bwd bf16 batch {batch}, {fi}->{fo}, W col-block + replicated, X/Y row-block"
+        workload = (f"FC train step bf16 batch {batch}, {fi}->{fo}: fwd (gemm, biasAdd, relu), bwd (reluGrad, "
+                    "dW gemm, addRowColSum, dX gemm), SGD axpy, W/b re-replication; W col-block + replicated, "
+                    "X row-block; value counts the 3 GEMMs' flops")
     else:
         n = 16384 if args.n == 32768 else args.n
         pr, pc = grid_for(world)
