@@ -201,6 +201,14 @@ typedef struct {
 void gm_session_options_default(gm_session_options* o);
 int gm_session_create(const gm_session_options* opts, gm_session** out);
 int gm_session_destroy(gm_session* s);
+/* Checkpoint-restart (reference Session::checkpoint / restore,
+ * session.cpp:413-480) in the reference's DMCK file format: files written by
+ * either implementation restore in the other. checkpoint fails while a
+ * replication is in flight; under SPMD rank 0 writes (collective). restore
+ * creates a session from `opts` (root seed taken from the file) holding every
+ * saved matrix with its id and version + 1. */
+int gm_session_checkpoint(gm_session* s, const char* path);
+int gm_session_restore(const char* path, const gm_session_options* opts, gm_session** out);
 /* SPMD only: the NCCL unique id rank 0 must broadcast before create. */
 int gm_nccl_unique_id(uint8_t out[128]);
 

@@ -103,6 +103,11 @@ def reflib():
                                    c_uint64, c_uint64, c_int32, T, c_uint32, c_void_p,
                                    c_uint64, c_uint64, c_int32, T, c_uint32, c_void_p,
                                    c_int32, c_void_p, c_void_p, c_char_p, c_size_t]
+        lib.gmref_ckpt_write.argtypes = [c_uint32, c_uint32, POINTER(c_uint64), POINTER(c_uint64), POINTER(c_int32),
+                                         POINTER(T), POINTER(c_uint32), POINTER(c_void_p), c_double, c_char_p,
+                                         c_char_p, c_size_t]
+        lib.gmref_ckpt_read.argtypes = [c_char_p, c_uint32, c_uint32, POINTER(c_uint64), POINTER(c_void_p),
+                                        POINTER(c_uint64), c_char_p, c_size_t]
         lib.gmref_float_to_half.argtypes = [c_void_p, c_void_p, c_uint64]
         lib.gmref_half_to_float.argtypes = [c_void_p, c_void_p, c_uint64]
         _ref = lib
@@ -277,3 +282,36 @@ def rel_fro(got: np.ndarray, want: np.ndarray) -> float:
     w = np.asarray(want, dtype=np.float64)
     den = np.linalg.norm(w)
     return float(np.linalg.norm(g - w) / (den if den else 1.0))
+
+
+def ckpt_write_ref(workers, mats, path, alpha=1.0):
+    """The reference writes a DMCK checkpoint of `mats` = [(image2d, prec,
+    tiles)] (ids 1..n; mulScalar(alpha) on matrix 1 first when alpha != 1)."""
+    lib = reflib()
+    n = len(mats)
+    imgs = [np.ascontiguousarray(m[0]) for m in mats]
+    tarrs = [tiles_array(list(m[2])) for m in mats]
+    rows = (c_uint64 * n)(*[i.shape[0] for i in imgs])
+    cols = (c_uint64 * n)(*[i.shape[1] for i in imgs])
+    precs = (c_int32 * n)(*[m[1] for m in mats])
+    tp = (POINTER(HTile) * n)(*[ctypes.cast(t, POINTER(HTile)) for t in tarrs])
+    nt = (c_uint32 * n)(*[len(m[2]) for m in mats])
+    ip = (c_void_p * n)(*[i.ctypes.data for i in imgs])
+    err = ctypes.create_string_buffer(512)
+    if lib.gmref_ckpt_write(workers, n, rows, cols, precs, tp, nt, ip, alpha, os.fsencode(path), err, 512):
+        raise RuntimeError("reference checkpoint failed: " + err.value.decode())
+
+
+def ckpt_read_ref(path, workers, shapes):
+    """The reference restores `path` and returns [(image, version)] for ids
+    1..len(shapes); shapes = [(rows, cols, prec)]."""
+    lib = reflib()
+    n = len(shapes)
+    outs = [np.empty((r, c), dtype=NP_DTYPE[p]) for (r, c, p) in shapes]
+    ids = (c_uint64 * n)(*range(1, n + 1))
+    op = (c_void_p * n)(*[o.ctypes.data for o in outs])
+    vers = (c_uint64 * n)()
+    err = ctypes.create_string_buffer(512)
+    if lib.gmref_ckpt_read(os.fsencode(path), workers, n, ids, op, vers, err, 512):
+        raise RuntimeError("reference restore failed: " + err.value.decode())
+    return [(outs[i], vers[i]) for i in range(n)]

@@ -12,6 +12,7 @@
 //   replicateSync / getDataRaw                             session.hpp:75,82
 //   relu / mulScalar / add / sub / axpy / reluGrad / biasAdd /
 //   copyMatrix / setConst / addRowColSum                   session.hpp:163-177
+//   checkpoint / restore (DMCK files)                      session.hpp:95-96
 // and calls fabric().closeAll() before the Session dies (its destructor
 // otherwise deadlocks, session.cpp:57-63 vs worker.cpp:56).
 //
@@ -21,6 +22,7 @@
 #include <cmath>
 #include <cstdint>
 #include <cstring>
+#include <memory>
 #include <string>
 #include <vector>
 
@@ -297,3 +299,65 @@ void gmref_half_to_float(const uint16_t* in, float* out, uint64_t n) {
 }
 
 }  // extern "C"
+
+// Checkpoint through the reference: creates n matrices (ids 1..n) from the
+// images, applies mulScalar(alpha) to matrix 1 when alpha != 1 (a version
+// bump), then Session::checkpoint(path) (session.cpp:413-442).
+extern "C" int gmref_ckpt_write(uint32_t workers, uint32_t n, const uint64_t* rows, const uint64_t* cols,
+                                const int32_t* precs, const HTile* const* tiles, const uint32_t* ntiles,
+                                const void* const* images, double alpha, const char* path, char* err,
+                                size_t errcap) {
+  try {
+    SessionOptions opts;
+    opts.workers = workers;
+    Session s(opts);
+    int rc = 0;
+    try {
+      std::vector<DistMatrix> ms;
+      for (uint32_t i = 0; i < n; ++i) {
+        const Precision pp = precisionFromTag(static_cast<uint8_t>(precs[i]));
+        DistMatrix m = s.createMatrix(rows[i], cols[i], pp, toLayout(tiles[i], ntiles[i]));
+        s.setData(m, rawToDouble(images[i], pp, rows[i] * cols[i]));
+        ms.push_back(m);
+      }
+      if (alpha != 1.0 && n > 0) mulScalar(s, ms[0], alpha);
+      s.checkpoint(path);
+    } catch (const std::exception& e) {
+      setErr(err, errcap, e.what());
+      rc = 1;
+    }
+    s.fabric().closeAll();
+    return rc;
+  } catch (const std::exception& e) {
+    setErr(err, errcap, e.what());
+    return 1;
+  }
+}
+
+// Restore through the reference (session.cpp:446-480) and read back the
+// matrices `ids` (raw images + versions).
+extern "C" int gmref_ckpt_read(const char* path, uint32_t workers, uint32_t n, const uint64_t* ids,
+                               void* const* out, uint64_t* versions, char* err, size_t errcap) {
+  try {
+    SessionOptions opts;
+    opts.workers = workers;
+    std::unique_ptr<Session> s = Session::restore(path, opts);
+    int rc = 0;
+    try {
+      for (uint32_t i = 0; i < n; ++i) {
+        const DistMatrix m(s.get(), ids[i]);
+        const std::vector<uint8_t> raw = s->getDataRaw(m);
+        std::memcpy(out[i], raw.data(), raw.size());
+        versions[i] = s->descriptor(ids[i]).version;
+      }
+    } catch (const std::exception& e) {
+      setErr(err, errcap, e.what());
+      rc = 1;
+    }
+    s->fabric().closeAll();
+    return rc;
+  } catch (const std::exception& e) {
+    setErr(err, errcap, e.what());
+    return 1;
+  }
+}

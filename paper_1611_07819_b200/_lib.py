@@ -103,6 +103,8 @@ _SIGNATURES = {
     "gm_session_options_default": ([_P(gm_session_options)], None),
     "gm_session_create": ([_P(gm_session_options), _P(c_void_p)], c_int32),
     "gm_session_destroy": ([c_void_p], c_int32),
+    "gm_session_checkpoint": ([c_void_p, c_char_p], c_int32),
+    "gm_session_restore": ([c_char_p, _P(gm_session_options), _P(c_void_p)], c_int32),
     "gm_nccl_unique_id": ([_P(c_uint8 * 128)], c_int32),
     "gm_matrix_create": ([c_void_p, c_uint64, c_uint64, c_int32, _P(gm_tile), c_uint32,
                           _P(c_uint64)], c_int32),

@@ -78,29 +78,42 @@ int gm_nccl_unique_id(uint8_t out[128]) {
   });
 }
 
+namespace {
+gridmath::SessionOptions toOptions(const gm_session_options* o) {
+  gridmath::SessionOptions opts;
+  opts.workers = o->workers;
+  opts.deterministic = o->deterministic != 0;
+  opts.replicationChunkBytes = o->replication_chunk_bytes;
+  opts.rootSeed = o->root_seed;
+  opts.checkMetadataEveryOp = o->check_metadata_every_op != 0;
+  opts.spmdRank = o->spmd_rank;
+  for (int i = 0; i < o->num_devices && i < 16; ++i) opts.devices.push_back(o->devices[i]);
+  std::memcpy(opts.ncclId.data(), o->nccl_unique_id, 128);
+  opts.gemmMaxCtas = o->gemm_max_ctas;
+  opts.transport = o->transport;
+  opts.panelCacheBytes = o->panel_cache_bytes;
+  opts.pipelineChunks = o->pipeline_chunks;
+  return opts;
+}
+}  // namespace
+
 int gm_session_create(const gm_session_options* o, gm_session** out) {
   return guard([&] {
-    gridmath::SessionOptions opts;
-    opts.workers = o->workers;
-    opts.deterministic = o->deterministic != 0;
-    opts.replicationChunkBytes = o->replication_chunk_bytes;
-    opts.rootSeed = o->root_seed;
-    opts.checkMetadataEveryOp = o->check_metadata_every_op != 0;
-    opts.spmdRank = o->spmd_rank;
-    for (int i = 0; i < o->num_devices && i < 16; ++i) opts.devices.push_back(o->devices[i]);
-    std::memcpy(opts.ncclId.data(), o->nccl_unique_id, 128);
-    opts.gemmMaxCtas = o->gemm_max_ctas;
-    opts.transport = o->transport;
-    opts.panelCacheBytes = o->panel_cache_bytes;
-    opts.pipelineChunks = o->pipeline_chunks;
-    auto* s = new gm_session;
-    try {
-      s->s = std::make_unique<gridmath::Session>(opts);
-    } catch (...) {
-      delete s;
-      throw;
-    }
-    *out = s;
+    auto s = std::make_unique<gm_session>();
+    s->s = std::make_unique<gridmath::Session>(toOptions(o));
+    *out = s.release();
+  });
+}
+
+int gm_session_checkpoint(gm_session* s, const char* path) {
+  return guard([&] { s->s->checkpoint(path); });
+}
+
+int gm_session_restore(const char* path, const gm_session_options* o, gm_session** out) {
+  return guard([&] {
+    auto s = std::make_unique<gm_session>();
+    s->s = gridmath::Session::restore(path, toOptions(o));
+    *out = s.release();
   });
 }
 

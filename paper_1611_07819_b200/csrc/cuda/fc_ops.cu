@@ -33,9 +33,9 @@ __device__ __forceinline__ T ew_eval(int kind, T xv, const EwView& y, uint64_t y
   }
 }
 
-// blockIdx.y strides rows, threads stride columns: every warp touches one
-// contiguous row segment of each operand (coalesced); the kind and precision
-// switches are uniform across the grid.
+// Generic path (operands of different storage precisions): blockIdx.y
+// strides rows, threads stride columns, so every warp touches one contiguous
+// row segment of each operand; the kind and precision switches are uniform.
 template <typename T>
 __global__ void ew_kernel(EwView x, EwView y, int ybc, void* __restrict__ d, uint64_t dld, int dprec,
                           uint64_t rows, uint64_t cols, int kind, T alpha) {
@@ -49,6 +49,92 @@ __global__ void ew_kernel(EwView x, EwView y, int ybc, void* __restrict__ d, uin
   }
 }
 
+// Storage element of precision tag P and its conversions to / from the
+// compute type (same rules as load_elem* / store_elem*).
+template <int P> struct Stor { using type = uint16_t; };
+template <> struct Stor<1> { using type = float; };
+template <> struct Stor<2> { using type = double; };
+
+template <int P, typename T>
+__device__ __forceinline__ T widen(typename Stor<P>::type v) {
+  if constexpr (P == 0) return static_cast<T>(half_bits_to_f32(v));
+  else if constexpr (P == 3) return static_cast<T>(__uint_as_float(static_cast<uint32_t>(v) << 16));
+  else return static_cast<T>(v);
+}
+template <int P, typename T>
+__device__ __forceinline__ typename Stor<P>::type narrow(T v) {
+  if constexpr (P == 2) return static_cast<double>(v);
+  else {
+    const float f = static_cast<float>(v);  // T is float unless P == 2
+    if constexpr (P == 0) return f32_to_half_bits(f);
+    else if constexpr (P == 3) return f32_to_bf16_bits(f);
+    else return f;
+  }
+}
+
+// Same-precision fast path: one 16-byte vector per thread per step (8 half /
+// bf16, 4 single or 2 double elements), every operand 16-byte aligned with
+// a 16-byte-multiple pitch (checked at launch). HBM-bound.
+template <typename T, int P>
+__global__ void ew_vec_kernel(EwView x, EwView y, int ybc, void* __restrict__ d, uint64_t dld, uint64_t rows,
+                              uint64_t cols, int kind, T alpha) {
+  using S = typename Stor<P>::type;
+  constexpr int N = 16 / sizeof(S);
+  union V {
+    uint4 u;
+    S e[N];
+  };
+  const uint64_t nvec = (cols + N - 1) / N;
+  const bool useY = kind >= kEwAdd && kind != kEwCopy;
+  for (uint64_t r = blockIdx.y; r < rows; r += gridDim.y) {
+    const S* xr = static_cast<const S*>(x.ptr) + r * x.ld;
+    const S* yr = static_cast<const S*>(y.ptr) + (ybc ? 0 : r * y.ld);
+    S* dr = static_cast<S*>(d) + r * dld;
+    for (uint64_t v = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; v < nvec;
+         v += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+      const uint64_t c0 = v * N;
+      if (c0 + N <= cols) {
+        V xv, yv, out;
+        xv.u = __ldg(reinterpret_cast<const uint4*>(xr + c0));
+        if (useY) yv.u = __ldg(reinterpret_cast<const uint4*>(yr + c0));
+#pragma unroll
+        for (int k = 0; k < N; ++k) {
+          const T a = widen<P, T>(xv.e[k]);
+          T o;
+          switch (kind) {
+            case kEwRelu: o = a > T(0) ? a : T(0); break;
+            case kEwMulScalar: o = mul_rn(alpha, a); break;
+            case kEwAdd:
+            case kEwBiasAdd: o = add_rn(a, widen<P, T>(yv.e[k])); break;
+            case kEwSub: o = sub_rn(a, widen<P, T>(yv.e[k])); break;
+            case kEwAxpy: o = add_rn(mul_rn(alpha, a), widen<P, T>(yv.e[k])); break;
+            case kEwReluGrad: o = a > T(0) ? widen<P, T>(yv.e[k]) : T(0); break;
+            default: o = a; break;
+          }
+          out.e[k] = narrow<P, T>(o);
+        }
+        *reinterpret_cast<uint4*>(dr + c0) = out.u;
+      } else {
+        for (uint64_t c = c0; c < cols; ++c) {
+          const T a = widen<P, T>(xr[c]);
+          T o;
+          switch (kind) {
+            case kEwRelu: o = a > T(0) ? a : T(0); break;
+            case kEwMulScalar: o = mul_rn(alpha, a); break;
+            case kEwAdd:
+            case kEwBiasAdd: o = add_rn(a, widen<P, T>(yr[c])); break;
+            case kEwSub: o = sub_rn(a, widen<P, T>(yr[c])); break;
+            case kEwAxpy: o = add_rn(mul_rn(alpha, a), widen<P, T>(yr[c])); break;
+            case kEwReluGrad: o = a > T(0) ? widen<P, T>(yr[c]) : T(0); break;
+            default: o = a; break;
+          }
+          dr[c] = narrow<P, T>(o);
+        }
+      }
+    }
+  }
+}
+
 __global__ void set_const_kernel(void* __restrict__ d, uint64_t ld, int prec, uint64_t rows, uint64_t cols,
                                  double v) {
   for (uint64_t r = blockIdx.y; r < rows; r += gridDim.y)
@@ -57,54 +143,197 @@ __global__ void set_const_kernel(void* __restrict__ d, uint64_t ld, int prec, ui
       store_elem(d, prec, r * ld + c, v);
 }
 
-// Line sums with the reference's sequential chain: 32 outputs per CTA; the
-// whole CTA stages 32 x 64 chunks of the band through shared memory
-// (coalesced along rows, double-buffered), and warp 0's lane o folds its
-// line's 64 values in ascending index order. One chain per output, so the
-// sum is bitwise the serial ascending-index sum.
-constexpr int kOut = 32, kStep = 64, kLsThreads = 256;
+// Line sums with the reference's sequential chain: 32 outputs per CTA. The
+// whole CTA streams the band in 32 x 256 chunks (coalesced along rows),
+// prefetching chunk i+1 into registers while warp 0 folds chunk i out of
+// shared memory (double-buffered); lane o adds its line's values in
+// ascending index order. One chain per output, so each sum is bitwise the
+// serial ascending-index sum, independent of layout and tiling.
+constexpr int kOut = 32, kStep = 256, kLsThreads = 256, kPer = kOut * kStep / kLsThreads;
 
 template <typename T>
 __global__ void __launch_bounds__(kLsThreads) line_sums_kernel(EwView a, uint64_t rows, uint64_t cols,
                                                                 int by_rows, void* __restrict__ acc,
                                                                 uint64_t acc_stride, int acc_prec, T alpha) {
-  __shared__ T st[2][kOut][kStep + 1];
+  extern __shared__ __align__(16) unsigned char ls_smem[];
+  T(*st)[kOut][kStep + 1] = reinterpret_cast<T(*)[kOut][kStep + 1]>(ls_smem);
   const uint64_t outs = by_rows ? rows : cols;  // number of sums
   const uint64_t len = by_rows ? cols : rows;   // length of each chain
   const uint64_t o0 = static_cast<uint64_t>(blockIdx.x) * kOut;
   const int tid = threadIdx.x;
-  T sum = T(0);
-  int buf = 0;
-  for (uint64_t s0 = 0; s0 < len; s0 += kStep, buf ^= 1) {
-    for (int i = tid; i < kOut * kStep; i += kLsThreads) {
+  T pre[kPer];
+  auto coords = [&](int i, uint64_t s0, int& o, int& s, uint64_t& r, uint64_t& c) {
+    if (by_rows) {  // consecutive i -> consecutive columns of one row
+      o = i / kStep;
+      s = i % kStep;
+      r = o0 + o;
+      c = s0 + s;
+    } else {  // consecutive i -> consecutive columns (outputs) of one row
+      s = i / kOut;
+      o = i % kOut;
+      r = s0 + s;
+      c = o0 + o;
+    }
+  };
+  auto fetch = [&](uint64_t s0) {
+#pragma unroll
+    for (int j = 0; j < kPer; ++j) {
       int o, s;
       uint64_t r, c;
-      if (by_rows) {  // consecutive i -> consecutive columns of one row
-        o = i / kStep;
-        s = i % kStep;
-        r = o0 + o;
-        c = s0 + s;
-      } else {  // consecutive i -> consecutive columns (outputs) of one row
-        s = i / kOut;
-        o = i % kOut;
-        r = s0 + s;
-        c = o0 + o;
-      }
-      st[buf][o][s] = (r < rows && c < cols) ? load_as<T>(a.ptr, a.prec, r * a.ld + c) : T(0);
+      coords(tid + j * kLsThreads, s0, o, s, r, c);
+      pre[j] = (r < rows && c < cols) ? load_as<T>(a.ptr, a.prec, r * a.ld + c) : T(0);
+    }
+  };
+  T sum = T(0);
+  int buf = 0;
+  fetch(0);
+  for (uint64_t s0 = 0; s0 < len; s0 += kStep, buf ^= 1) {
+#pragma unroll
+    for (int j = 0; j < kPer; ++j) {
+      int o, s;
+      uint64_t r, c;
+      coords(tid + j * kLsThreads, s0, o, s, r, c);
+      st[buf][o][s] = pre[j];
     }
     __syncthreads();
+    if (s0 + kStep < len) fetch(s0 + kStep);  // in flight while warp 0 sums
     if (tid < kOut) {
       const int n = static_cast<int>(len - s0 < kStep ? len - s0 : kStep);
       for (int s = 0; s < n; ++s) sum = add_rn(sum, st[buf][tid][s]);
     }
-    // The next chunk goes to the other buffer; the one after that reuses this
-    // buffer only after the barrier that warp 0 reaches once it is done here.
+    // Buffer buf is rewritten two iterations later, after the barrier that
+    // warp 0 reaches only once it has finished here.
   }
   if (tid < kOut && o0 + tid < outs) {
     const uint64_t idx = (o0 + tid) * acc_stride;
     const T cur = load_as<T>(acc, acc_prec, idx);
     store_as(acc, acc_prec, idx, add_rn(cur, mul_rn(alpha, sum)));
   }
+}
+
+// Line sums, aligned fast path: the same ascending chains, fed by a 4-stage
+// cp.async ring of raw storage in shared memory (16-byte copies, zero-filled
+// past the band's edge), so ~3 stages (384 elements per chain) are in flight
+// while warp 0 folds the current one. A CTA owns 32 outputs:
+//   by rows: stage = 32 rows x 128 elements, row pitch 128*E + 16 bytes, so
+//            lane o's 16-byte LDS of its row are bank-conflict-free;
+//   by cols: stage = 128 rows x 32 elements (lane o reads column o).
+// Zero padding is exact: a chain that starts at +0 never holds -0, so adding
+// +0 leaves it unchanged.
+constexpr int kAsStep = 128, kAsStages = 4, kAsThreads = 128;
+
+__device__ __forceinline__ void cp_async16(uint32_t saddr, const void* g, uint32_t bytes) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(saddr), "l"(g), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
+}
+
+template <typename T, int P>
+__global__ void __launch_bounds__(kAsThreads) line_sums_async_kernel(const void* __restrict__ a, uint64_t lda,
+                                                                      uint64_t rows, uint64_t cols, int by_rows,
+                                                                      void* __restrict__ acc, uint64_t acc_stride,
+                                                                      int acc_prec, T alpha) {
+  using S = typename Stor<P>::type;
+  constexpr int E = sizeof(S), VE = 16 / E;
+  constexpr int kPitchR = kAsStep * E + 16, kStageR = 32 * kPitchR;
+  constexpr int kPitchC = 32 * E, kStageC = kAsStep * kPitchC;
+  constexpr int kStage = kStageR > kStageC ? kStageR : kStageC;
+  extern __shared__ __align__(128) unsigned char ring[];
+  const uint32_t ring_s = static_cast<uint32_t>(__cvta_generic_to_shared(ring));
+  const uint64_t outs = by_rows ? rows : cols;
+  const uint64_t len = by_rows ? cols : rows;
+  const uint64_t o0 = static_cast<uint64_t>(blockIdx.x) * 32;
+  const uint64_t nchunks = (len + kAsStep - 1) / kAsStep;
+  const unsigned char* ab = static_cast<const unsigned char*>(a);
+  const int tid = threadIdx.x;
+
+  auto issue = [&](uint64_t chunk) {
+    const uint32_t st = ring_s + static_cast<uint32_t>((chunk % kAsStages) * kStage);
+    const uint64_t s0 = chunk * kAsStep;
+    constexpr int kVecs = 32 * kAsStep / VE;  // 16-byte copies per stage
+    for (int q = tid; q < kVecs; q += kAsThreads) {
+      uint64_t r, c;
+      uint32_t soff;
+      if (by_rows) {
+        constexpr int per = kAsStep / VE;
+        const int o = q / per, v = q % per;
+        r = o0 + o;
+        c = s0 + static_cast<uint64_t>(v) * VE;
+        soff = static_cast<uint32_t>(o * kPitchR + v * 16);
+      } else {
+        constexpr int per = 32 / VE;
+        const int sr = q / per, v = q % per;
+        r = s0 + sr;
+        c = o0 + static_cast<uint64_t>(v) * VE;
+        soff = static_cast<uint32_t>(sr * kPitchC + v * 16);
+      }
+      uint32_t bytes = 0;
+      const unsigned char* g = ab;
+      if (r < rows && c < cols) {
+        const uint64_t left = (cols - c) * E;
+        bytes = left < 16 ? static_cast<uint32_t>(left) : 16u;
+        g = ab + (r * lda + c) * E;
+      }
+      cp_async16(st + soff, g, bytes);
+    }
+  };
+
+  for (int i = 0; i < kAsStages - 1; ++i) {
+    if (static_cast<uint64_t>(i) < nchunks) issue(i);
+    cp_async_commit();
+  }
+  T sum = T(0);
+  for (uint64_t i = 0; i < nchunks; ++i) {
+    cp_async_wait<kAsStages - 2>();
+    __syncthreads();
+    if (i + kAsStages - 1 < nchunks) issue(i + kAsStages - 1);
+    cp_async_commit();
+    if (tid < 32) {
+      const unsigned char* st = ring + (i % kAsStages) * kStage;
+      if (by_rows) {
+        const unsigned char* row = st + tid * kPitchR;
+#pragma unroll 4
+        for (int v = 0; v < kAsStep / VE; ++v) {
+          union {
+            uint4 u;
+            S e[VE];
+          } w;
+          w.u = *reinterpret_cast<const uint4*>(row + v * 16);
+#pragma unroll
+          for (int k = 0; k < VE; ++k) sum = add_rn(sum, widen<P, T>(w.e[k]));
+        }
+      } else {
+        const S* col = reinterpret_cast<const S*>(st) + tid;
+#pragma unroll 16
+        for (int sr = 0; sr < kAsStep; ++sr) sum = add_rn(sum, widen<P, T>(col[sr * 32]));
+      }
+    }
+  }
+  cp_async_wait<0>();
+  if (tid < 32 && o0 + tid < outs) {
+    const uint64_t idx = (o0 + tid) * acc_stride;
+    const T cur = load_as<T>(acc, acc_prec, idx);
+    store_as(acc, acc_prec, idx, add_rn(cur, mul_rn(alpha, sum)));
+  }
+}
+
+template <typename T, int P>
+cudaError_t launch_sums_async(EwView band, uint64_t rows, uint64_t cols, int by_rows, void* acc,
+                              uint64_t acc_stride, int acc_prec, T alpha, cudaStream_t s) {
+  using S = typename Stor<P>::type;
+  constexpr int E = sizeof(S);
+  constexpr int kStageR = 32 * (kAsStep * E + 16), kStageC = kAsStep * 32 * E;
+  constexpr size_t smem = static_cast<size_t>(kAsStages) * (kStageR > kStageC ? kStageR : kStageC);
+  static const cudaError_t attr = cudaFuncSetAttribute(line_sums_async_kernel<T, P>,
+                                                       cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (attr != cudaSuccess) return attr;
+  const uint64_t outs = by_rows ? rows : cols;
+  line_sums_async_kernel<T, P><<<static_cast<unsigned>((outs + 31) / 32), kAsThreads, smem, s>>>(
+      band.ptr, band.ld, rows, cols, by_rows, acc, acc_stride, acc_prec, alpha);
+  return cudaSuccess;
 }
 
 dim3 rect_grid(uint64_t rows, uint64_t cols, unsigned threads) {
@@ -118,17 +347,43 @@ dim3 rect_grid(uint64_t rows, uint64_t cols, unsigned threads) {
   return dim3(static_cast<unsigned>(gx), static_cast<unsigned>(gy));
 }
 
+bool vec_ok(const void* p, uint64_t ld, int eb) {
+  return (reinterpret_cast<uintptr_t>(p) % 16 == 0) && ((ld * eb) % 16 == 0);
+}
+
+template <typename T, int P>
+void launch_vec(EwView x, EwView y, int ybc, void* dst, uint64_t dld, uint64_t rows, uint64_t cols, int kind,
+                T alpha, cudaStream_t s) {
+  constexpr int N = 16 / sizeof(typename Stor<P>::type);
+  const dim3 g = rect_grid(rows, (cols + N - 1) / N, 256);
+  ew_vec_kernel<T, P><<<g, 256, 0, s>>>(x, y, ybc, dst, dld, rows, cols, kind, alpha);
+}
+
 }  // namespace
 
 cudaError_t ew_apply(EwView x, EwView y, int y_row_bcast, void* dst, uint64_t dld, int dprec, uint64_t rows,
                      uint64_t cols, int kind, double alpha, int double_compute, cudaStream_t s) {
   if (rows == 0 || cols == 0) return cudaSuccess;
-  const dim3 g = rect_grid(rows, cols, 256);
-  if (double_compute)
-    ew_kernel<double><<<g, 256, 0, s>>>(x, y, y_row_bcast, dst, dld, dprec, rows, cols, kind, alpha);
-  else
-    ew_kernel<float><<<g, 256, 0, s>>>(x, y, y_row_bcast, dst, dld, dprec, rows, cols, kind,
-                                       static_cast<float>(alpha));
+  const bool useY = kind >= kEwAdd && kind != kEwCopy;
+  const int eb = dprec == 2 ? 8 : (dprec == 1 ? 4 : 2);
+  const bool same = x.prec == dprec && (!useY || y.prec == dprec);
+  const bool aligned = vec_ok(x.ptr, x.ld, eb) && vec_ok(dst, dld, eb) && (!useY || vec_ok(y.ptr, y.ld, eb));
+  if (same && aligned) {
+    const float af = static_cast<float>(alpha);
+    switch (dprec) {
+      case 0: launch_vec<float, 0>(x, y, y_row_bcast, dst, dld, rows, cols, kind, af, s); break;
+      case 1: launch_vec<float, 1>(x, y, y_row_bcast, dst, dld, rows, cols, kind, af, s); break;
+      case 2: launch_vec<double, 2>(x, y, y_row_bcast, dst, dld, rows, cols, kind, alpha, s); break;
+      default: launch_vec<float, 3>(x, y, y_row_bcast, dst, dld, rows, cols, kind, af, s); break;
+    }
+  } else {
+    const dim3 g = rect_grid(rows, cols, 256);
+    if (double_compute)
+      ew_kernel<double><<<g, 256, 0, s>>>(x, y, y_row_bcast, dst, dld, dprec, rows, cols, kind, alpha);
+    else
+      ew_kernel<float><<<g, 256, 0, s>>>(x, y, y_row_bcast, dst, dld, dprec, rows, cols, kind,
+                                         static_cast<float>(alpha));
+  }
   count_launch();
   return cudaGetLastError();
 }
@@ -145,13 +400,38 @@ cudaError_t line_sums(EwView band, uint64_t rows, uint64_t cols, int by_rows, vo
                       int acc_prec, double alpha, int double_compute, cudaStream_t s) {
   const uint64_t outs = by_rows ? rows : cols;
   if (outs == 0) return cudaSuccess;
+  const int eb = band.prec == 2 ? 8 : (band.prec == 1 ? 4 : 2);
+  // Fast path: 16-byte aligned band rows; the chain type follows the
+  // reference (double iff any operand is Double).
+  if (vec_ok(band.ptr, band.ld, eb) && (double_compute ? band.prec == 2 : band.prec != 2)) {
+    cudaError_t e;
+    const float af = static_cast<float>(alpha);
+    switch (band.prec) {
+      case 0: e = launch_sums_async<float, 0>(band, rows, cols, by_rows, acc, acc_stride, acc_prec, af, s); break;
+      case 1: e = launch_sums_async<float, 1>(band, rows, cols, by_rows, acc, acc_stride, acc_prec, af, s); break;
+      case 2: e = launch_sums_async<double, 2>(band, rows, cols, by_rows, acc, acc_stride, acc_prec, alpha, s); break;
+      default: e = launch_sums_async<float, 3>(band, rows, cols, by_rows, acc, acc_stride, acc_prec, af, s); break;
+    }
+    if (e != cudaSuccess) return e;
+    count_launch();
+    return cudaGetLastError();
+  }
   const unsigned grid = static_cast<unsigned>((outs + kOut - 1) / kOut);
-  if (double_compute)
-    line_sums_kernel<double><<<grid, kLsThreads, 0, s>>>(band, rows, cols, by_rows, acc, acc_stride, acc_prec,
-                                                         alpha);
-  else
-    line_sums_kernel<float><<<grid, kLsThreads, 0, s>>>(band, rows, cols, by_rows, acc, acc_stride, acc_prec,
-                                                        static_cast<float>(alpha));
+  if (double_compute) {
+    const size_t smem = 2 * kOut * (kStep + 1) * sizeof(double);
+    static const cudaError_t attr =
+        cudaFuncSetAttribute(line_sums_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (attr != cudaSuccess) return attr;
+    line_sums_kernel<double><<<grid, kLsThreads, smem, s>>>(band, rows, cols, by_rows, acc, acc_stride, acc_prec,
+                                                            alpha);
+  } else {
+    const size_t smem = 2 * kOut * (kStep + 1) * sizeof(float);
+    static const cudaError_t attr =
+        cudaFuncSetAttribute(line_sums_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (attr != cudaSuccess) return attr;
+    line_sums_kernel<float><<<grid, kLsThreads, smem, s>>>(band, rows, cols, by_rows, acc, acc_stride, acc_prec,
+                                                           static_cast<float>(alpha));
+  }
   count_launch();
   return cudaGetLastError();
 }

@@ -109,6 +109,13 @@ class WireReader {
     if (n) std::memcpy(dst, p_ + pos_, n);
     pos_ += n;
   }
+  // Borrow the next n bytes (valid while the underlying buffer lives).
+  const std::uint8_t* raw(std::size_t n) {
+    need(n);
+    const std::uint8_t* p = p_ + pos_;
+    pos_ += n;
+    return p;
+  }
   std::size_t remaining() const { return n_ - pos_; }
   bool done() const { return pos_ == n_; }
 

@@ -761,6 +761,11 @@ DistMatrix Session::createMatrix(std::uint64_t rows, std::uint64_t cols, Precisi
   d.cols = cols;
   d.precision = p;
   d.layout = layout;
+  return createWithDescriptor(d);
+}
+
+DistMatrix Session::createWithDescriptor(const MatrixDescriptor& d) {
+  nextMatrixId_ = std::max(nextMatrixId_, d.matrixId + 1);
   OpDescriptor op;
   op.opcode = OpCode::CreateMatrix;
   op.ids[0] = d.matrixId;

@@ -246,6 +246,9 @@ class Session {
   Session& operator=(const Session&) = delete;
 
   DistMatrix createMatrix(std::uint64_t rows, std::uint64_t cols, Precision p, const Layout& layout);
+  // Creates a matrix with a caller-chosen descriptor (id, version, layout);
+  // reference Session::createWithDescriptor (session.cpp:200-218).
+  DistMatrix createWithDescriptor(const MatrixDescriptor& d);
   void destroy(DistMatrix m);
   void setData(DistMatrix m, const std::vector<double>& rowMajor);
   void setDataF32(DistMatrix m, const std::vector<float>& rowMajor);
@@ -257,6 +260,15 @@ class Session {
   // Redistribution (reference Session::reshape, session.cpp:310-325, and
   // execReshape, kernels.cpp:1083-1127): new layout and/or storage precision.
   void reshape(DistMatrix m, const Layout& newLayout, std::optional<Precision> newPrecision = std::nullopt);
+
+  // Checkpoint-restart in the reference's DMCK format (session.cpp:413-480):
+  // "DMCK", u32 version 1, u64 root seed, u32 count, per matrix (ascending
+  // id) its descriptor and full row-major image, then the zlib CRC-32 of
+  // everything after the magic. Files are interchangeable with the
+  // reference's. Under SPMD every rank gathers, rank 0 writes; restore is
+  // collective (every rank reads the file).
+  void checkpoint(const std::string& path);
+  static std::unique_ptr<Session> restore(const std::string& path, SessionOptions opts);
 
   ReplicationHandle replicateAsync(DistMatrix m);
   void replicateSync(DistMatrix m);

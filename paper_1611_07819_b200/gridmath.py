@@ -18,6 +18,7 @@ gridmath::Error).
 from __future__ import annotations
 
 import ctypes
+import os
 import enum
 from dataclasses import dataclass
 from typing import List, Optional, Sequence
@@ -166,7 +167,7 @@ class Session:
     def __init__(self, workers: int = 1, deterministic: bool = True, devices: Optional[Sequence[int]] = None,
                  spmd_rank: int = -1, nccl_id: Optional[bytes] = None, gemm_max_ctas: int = 0,
                  transport: int = 0, check_metadata_every_op: bool = False, panel_cache_bytes: int = 0,
-                 pipeline_chunks: int = 0):
+                 pipeline_chunks: int = 0, _restore_from: Optional[str] = None):
         lib = _lib.load()
         o = _lib.gm_session_options()
         lib.gm_session_options_default(ctypes.byref(o))
@@ -185,9 +186,26 @@ class Session:
         o.panel_cache_bytes = panel_cache_bytes
         o.pipeline_chunks = pipeline_chunks
         self._h = ctypes.c_void_p()
-        check(lib.gm_session_create(ctypes.byref(o), ctypes.byref(self._h)))
+        if _restore_from is None:
+            check(lib.gm_session_create(ctypes.byref(o), ctypes.byref(self._h)))
+        else:
+            check(lib.gm_session_restore(os.fsencode(_restore_from), ctypes.byref(o), ctypes.byref(self._h)))
         self.workers = workers
         self.deterministic = deterministic
+
+    @classmethod
+    def restore(cls, path: str, workers: int = 1, **kw) -> "Session":
+        """Session::restore (session.cpp:446-480): a new session holding every
+        matrix of a DMCK checkpoint (ours or the reference's)."""
+        return cls(workers=workers, _restore_from=path, **kw)
+
+    def checkpoint(self, path: str):
+        """Session::checkpoint (session.cpp:413-442), DMCK format."""
+        check(_lib.load().gm_session_checkpoint(self._h, os.fsencode(path)))
+
+    def matrix(self, mid: int) -> "DistMatrix":
+        """Handle of an existing matrix id (e.g. after restore)."""
+        return DistMatrix(self, mid)
 
     def close(self):
         if self._h:

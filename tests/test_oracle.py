@@ -148,3 +148,16 @@ def test_fc_restatement_matches_reference_golden(golden_index):
                 assert np.array_equal(got.view(np.uint8), want.view(np.uint8)), c["name"]
             else:
                 assert np.allclose(got, want, rtol=1e-5, atol=1e-5), c["name"]
+
+
+def test_reference_checkpoint_round_trip(tmp_path):
+    """The checker for the DMCK parity tests: the reference restores what it
+    wrote (session.cpp:413-480), with version + 1 from restore's setData."""
+    img = O.fill_uniform(20, 30, 1, 3).reshape(20, 30)
+    path = str(tmp_path / "r.dmck")
+    O.ckpt_write_ref(2, [(img, 1, O.row_block_tiles(20, 30, 2))], path, alpha=2.0)
+    raw = open(path, "rb").read()
+    assert raw[:4] == b"DMCK" and int.from_bytes(raw[4:8], "little") == 1
+    (got, ver), = O.ckpt_read_ref(path, 3, [(20, 30, 1)])
+    assert ver == 3
+    assert np.array_equal(got, (img * np.float32(2.0)).astype(np.float32))
