@@ -289,6 +289,18 @@ int gm_cast_precision(gm_session* s, uint64_t src, uint64_t dst);              /
 int gm_op_issue(gm_session* s, int32_t opcode, const uint64_t ids[4], double s0, double s1,
                 const uint8_t flags[4], int32_t sync);
 
+/* Pipeline recording (reference Session::beginRecord / endRecord / replay,
+ * session.cpp:385-409). Between begin and end, only recordable ops may be
+ * issued (SetConst, Gemm, AddRowColSum, EwUnary, EwBinary, ReplicateStart;
+ * anything else fails with "op not recordable inside an open pipeline
+ * recording"); they execute normally and are remembered. gm_replay re-issues
+ * the steps with fresh exec ids and returns when the device work is done;
+ * gm_replay_async only enqueues it. */
+int gm_begin_record(gm_session* s, uint64_t* pipeline_id);
+int gm_end_record(gm_session* s);
+int gm_replay(gm_session* s, uint64_t pipeline_id);
+int gm_replay_async(gm_session* s, uint64_t pipeline_id);
+
 /* Replication (session.hpp:81-84). */
 int gm_replicate_async(gm_session* s, uint64_t id, uint64_t* version);
 int gm_replicate_sync(gm_session* s, uint64_t id);

@@ -138,6 +138,10 @@ _SIGNATURES = {
     "gm_bias_add": ([c_void_p, c_uint64, c_uint64], c_int32),
     "gm_copy_matrix": ([c_void_p, c_uint64, c_uint64], c_int32),
     "gm_cast_precision": ([c_void_p, c_uint64, c_uint64], c_int32),
+    "gm_begin_record": ([c_void_p, _P(c_uint64)], c_int32),
+    "gm_end_record": ([c_void_p], c_int32),
+    "gm_replay": ([c_void_p, c_uint64], c_int32),
+    "gm_replay_async": ([c_void_p, c_uint64], c_int32),
     "gm_op_issue": ([c_void_p, c_int32, _P(c_uint64), c_double, c_double, _P(c_uint8), c_int32], c_int32),
     "gm_session_synchronize": ([c_void_p], c_int32),
     "gm_replicate_async": ([c_void_p, c_uint64, _P(c_uint64)], c_int32),

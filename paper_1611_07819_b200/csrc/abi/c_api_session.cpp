@@ -246,6 +246,23 @@ int gm_cast_precision(gm_session* s, uint64_t src, uint64_t dst) {
   return guard([&] { gridmath::castPrecision(*s->s, handle(s, src), handle(s, dst)); });
 }
 
+// Pipeline recording (reference session.hpp:89-92).
+int gm_begin_record(gm_session* s, uint64_t* pipeline_id) {
+  return guard([&] { *pipeline_id = s->s->beginRecord(); });
+}
+
+int gm_end_record(gm_session* s) {
+  return guard([&] { s->s->endRecord(); });
+}
+
+int gm_replay(gm_session* s, uint64_t pipeline_id) {
+  return guard([&] { s->s->replay(pipeline_id, true); });
+}
+
+int gm_replay_async(gm_session* s, uint64_t pipeline_id) {
+  return guard([&] { s->s->replay(pipeline_id, false); });
+}
+
 int gm_op_issue(gm_session* s, int32_t opcode, const uint64_t ids[4], double s0, double s1,
                 const uint8_t flags[4], int32_t sync) {
   return guard([&] {

@@ -675,11 +675,39 @@ void Session::checkErrors(std::vector<std::string>& errs) {
 
 const MatrixDescriptor& Session::descriptor(std::uint64_t id) const { return lookup(table_, id); }
 
+namespace {
+// Reference session.cpp:16-30.
+bool recordable(OpCode c) {
+  switch (c) {
+    case OpCode::SetConst:
+    case OpCode::Gemm:
+    case OpCode::AddRowColSum:
+    case OpCode::EwUnary:
+    case OpCode::EwBinary:
+    case OpCode::SoftmaxRows:
+    case OpCode::SubtractOneHot:
+    case OpCode::ReplicateStart:
+      return true;
+    default:
+      return false;
+  }
+}
+}  // namespace
+
+void Session::requireRecordable(OpCode c) const {
+  if (recording_ != 0 && !recordable(c)) throw Error("op not recordable inside an open pipeline recording");
+}
+
 std::uint64_t Session::issue(OpDescriptor& op) {
+  requireRecordable(op.opcode);
   flushWritten(nextExec_);  // earlier ops' device work is enqueued: publish their writes
   op.execId = nextExec_++;
   curExec_ = op.execId;
   validateOp(table_, op, opts_.workers);
+  if (recording_ != 0) {
+    op.recordPipeline = recording_;
+    pipelines_[recording_].push_back(op);
+  }
   std::vector<std::pair<std::uint64_t, std::uint64_t>> moved;
   for (std::uint64_t id : mutatedMatrices(op)) {
     auto it = table_.find(id);
@@ -1003,6 +1031,7 @@ std::vector<double> Session::getData(DistMatrix m) {
 // ---------------------------------------------------------------- reshape
 
 void Session::reshape(DistMatrix m, const Layout& newLayout, std::optional<Precision> newPrecision) {
+  requireRecordable(OpCode::Reshape);
   const MatrixDescriptor old = descriptor(m.id());  // copy: the table entry is replaced below
   MatrixDescriptor nd = old;
   nd.layout = newLayout;
@@ -1789,6 +1818,49 @@ float Session::timerStop() {
     best = std::max(best, ms);
   });
   return best;
+}
+
+// ---------------------------------------------------------------- record / replay
+
+std::uint64_t Session::beginRecord() {
+  if (recording_ != 0) throw Error("beginRecord: a recording is already open");
+  recording_ = nextPipelineId_++;
+  pipelines_[recording_] = {};
+  return recording_;
+}
+
+void Session::endRecord() {
+  if (recording_ == 0) throw Error("endRecord: no open recording");
+  closedPipelines_.insert(recording_);
+  recording_ = 0;
+}
+
+void Session::replay(std::uint64_t pipelineId, bool sync) {
+  if (recording_ != 0) throw Error("replay: recording still open");
+  if (!closedPipelines_.count(pipelineId))
+    throw Error("replay: unknown or unfinished pipeline " + std::to_string(pipelineId));
+  for (const OpDescriptor& recorded : pipelines_.at(pipelineId)) {
+    OpDescriptor step = recorded;
+    step.execId = 0;
+    step.recordPipeline = 0;
+    switch (step.opcode) {
+      case OpCode::Gemm:
+        runGemm(step, false);
+        break;
+      case OpCode::SetConst:
+      case OpCode::EwUnary:
+      case OpCode::EwBinary:
+      case OpCode::AddRowColSum:
+        runPointwise(step, false);
+        break;
+      case OpCode::ReplicateStart:
+        replicateAsync(DistMatrix(this, step.ids[0]));
+        break;
+      default:
+        throw Error("replay: op not supported on the B200 GEMM path");
+    }
+  }
+  if (sync) synchronize();
 }
 
 // ---------------------------------------------------------------- replication

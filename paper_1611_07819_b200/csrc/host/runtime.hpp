@@ -270,6 +270,16 @@ class Session {
   void checkpoint(const std::string& path);
   static std::unique_ptr<Session> restore(const std::string& path, SessionOptions opts);
 
+  // Pipeline recording (reference session.cpp:385-409): recordable ops
+  // (SetConst, Gemm, AddRowColSum, EwUnary, EwBinary, ReplicateStart) issued
+  // between beginRecord and endRecord execute normally and are remembered;
+  // replay re-issues the steps with fresh exec ids (same metadata walk).
+  // replay is synchronous like the reference's; sync = false leaves the
+  // device work stream-ordered.
+  std::uint64_t beginRecord();
+  void endRecord();
+  void replay(std::uint64_t pipelineId, bool sync = true);
+
   ReplicationHandle replicateAsync(DistMatrix m);
   void replicateSync(DistMatrix m);
   ReplState wait(const ReplicationHandle& h);
@@ -305,6 +315,7 @@ class Session {
 
  private:
   std::uint64_t issue(OpDescriptor& op);  // validate + metadata + per-worker mirror
+  void requireRecordable(OpCode c) const;
   Worker* local(std::uint32_t rank) const;
   bool isLocal(std::uint32_t rank) const;
   void execCreate(const OpDescriptor& op);
@@ -345,6 +356,9 @@ class Session {
   std::vector<PanelCache> remoteCaches_;          // directory for non-local workers (SPMD)
   std::map<std::pair<std::uint64_t, std::uint64_t>, bool> replFailed_;
   std::uint64_t nextMatrixId_ = 1;
+  std::uint64_t recording_ = 0, nextPipelineId_ = 1;
+  std::map<std::uint64_t, std::vector<OpDescriptor>> pipelines_;
+  std::set<std::uint64_t> closedPipelines_;
   std::uint64_t nextExec_ = 1;
   std::uint64_t tick_ = 0;
   std::uint64_t gemmEpoch_ = 0;  // arena epoch of band temporaries (one per GEMM)

@@ -361,6 +361,19 @@ class Session:
                   transA=False, transB=False):
         check(_lib.load().gm_gemm_async(self._h, a.id, b.id, c.id, alpha, beta, int(transA), int(transB)))
 
+    # --- pipeline recording (session.hpp:89-92) ---------------------------------
+    def beginRecord(self) -> int:
+        pid = ctypes.c_uint64()
+        check(_lib.load().gm_begin_record(self._h, ctypes.byref(pid)))
+        return pid.value
+
+    def endRecord(self):
+        check(_lib.load().gm_end_record(self._h))
+
+    def replay(self, pipeline_id: int, sync: bool = True):
+        fn = _lib.load().gm_replay if sync else _lib.load().gm_replay_async
+        check(fn(self._h, pipeline_id))
+
     def opIssue(self, opcode: int, ids, s0: float = 0.0, s1: float = 0.0, flags=(0, 0, 0, 0), sync: bool = False):
         """Issue one wire op (reference OpDescriptor) on the device path."""
         ids4 = (ctypes.c_uint64 * 4)(*(list(ids) + [0] * (4 - len(ids))))
