@@ -237,6 +237,15 @@ int gm_matrix_get_local_raw(gm_session* s, uint64_t id, void* host, uint64_t byt
 int gm_matrix_local_bytes(gm_session* s, uint64_t id, uint64_t* bytes);
 int gm_matrix_set_local_packed(gm_session* s, uint64_t id, const void* host, uint64_t bytes);
 int gm_matrix_get_local_packed(gm_session* s, uint64_t id, void* host, uint64_t bytes);
+/* Asynchronous packed local I/O (stream-ordered; `host` must stay valid and
+ * unmodified until gm_session_synchronize; pin it for real overlap).
+ * Uploads move in row chunks of ~chunk_bytes (0 = 256 MiB) on a side stream;
+ * the next gm_gemm* reading the tile in place starts each of its row chunks
+ * as soon as the rows it needs have landed, and a download of its C drains
+ * behind the GEMM's row chunks. Version bumps as for the synchronous calls. */
+int gm_matrix_set_local_packed_async(gm_session* s, uint64_t id, const void* host, uint64_t bytes,
+                                     uint64_t chunk_bytes);
+int gm_matrix_get_local_packed_async(gm_session* s, uint64_t id, void* host, uint64_t bytes);
 /* Redistribution (reference Session::reshape, session.cpp:310-325): new
  * layout and/or storage precision (new_prec < 0 keeps it); version + 1,
  * replicas reset; values converted like convertBuffer. */

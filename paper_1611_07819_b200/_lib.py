@@ -118,6 +118,8 @@ _SIGNATURES = {
     "gm_matrix_local_bytes": ([c_void_p, c_uint64, _P(c_uint64)], c_int32),
     "gm_matrix_set_local_packed": ([c_void_p, c_uint64, c_void_p, c_uint64], c_int32),
     "gm_matrix_get_local_packed": ([c_void_p, c_uint64, c_void_p, c_uint64], c_int32),
+    "gm_matrix_set_local_packed_async": ([c_void_p, c_uint64, c_void_p, c_uint64, c_uint64], c_int32),
+    "gm_matrix_get_local_packed_async": ([c_void_p, c_uint64, c_void_p, c_uint64], c_int32),
     "gm_matrix_reshape": ([c_void_p, c_uint64, _P(gm_tile), c_uint32, c_int32], c_int32),
     "gm_matrix_info": ([c_void_p, c_uint64, _P(c_uint64), _P(c_uint64), _P(c_int32),
                         _P(c_uint64), _P(c_uint64)], c_int32),

@@ -173,6 +173,15 @@ int gm_matrix_get_local_packed(gm_session* s, uint64_t id, void* host, uint64_t 
   return guard([&] { s->s->getLocalPacked(handle(s, id), host, bytes); });
 }
 
+int gm_matrix_set_local_packed_async(gm_session* s, uint64_t id, const void* host, uint64_t bytes,
+                                     uint64_t chunk_bytes) {
+  return guard([&] { s->s->setLocalPackedAsync(handle(s, id), host, bytes, chunk_bytes); });
+}
+
+int gm_matrix_get_local_packed_async(gm_session* s, uint64_t id, void* host, uint64_t bytes) {
+  return guard([&] { s->s->getLocalPackedAsync(handle(s, id), host, bytes); });
+}
+
 int gm_matrix_reshape(gm_session* s, uint64_t id, const gm_tile* tiles, uint32_t ntiles, int32_t new_prec) {
   return guard([&] {
     std::optional<gridmath::Precision> p;

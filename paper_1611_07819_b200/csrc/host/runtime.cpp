@@ -269,6 +269,8 @@ Worker::Worker(std::uint32_t r, int dev, std::uint64_t budget)
   int lo = 0, hi = 0;
   cudaDeviceGetStreamPriorityRange(&lo, &hi);
   cudaCheck(cudaStreamCreateWithPriority(&comm, cudaStreamNonBlocking, hi), "worker: comm stream");
+  cudaCheck(cudaStreamCreateWithFlags(&h2d, cudaStreamNonBlocking), "worker: h2d stream");
+  cudaCheck(cudaStreamCreateWithFlags(&d2h, cudaStreamNonBlocking), "worker: d2h stream");
   cudaCheck(cudaEventCreate(&tStart), "worker: event");
   cudaCheck(cudaEventCreate(&tEnd), "worker: event");
   cudaCheck(cudaEventCreate(&uStart), "worker: event");
@@ -282,6 +284,14 @@ Worker::~Worker() {
   activate();
   cudaStreamSynchronize(compute);
   cudaStreamSynchronize(comm);
+  cudaStreamSynchronize(h2d);
+  cudaStreamSynchronize(d2h);
+  for (auto& kv : uploads) {
+    for (auto& c : kv.second.chunks) cudaEventDestroy(c.done);
+    cudaEventDestroy(kv.second.done);
+  }
+  for (auto& kv : chunkDone)
+    for (auto& c : kv.second) cudaEventDestroy(c.done);
   releaseReaders();
   for (CacheEntry& e : cache.dropAll())
     if (e.ready) cudaEventDestroy(e.ready);
@@ -300,6 +310,25 @@ Worker::~Worker() {
   cudaEventDestroy(cEnd);
   cudaStreamDestroy(compute);
   cudaStreamDestroy(comm);
+  cudaStreamDestroy(h2d);
+  cudaStreamDestroy(d2h);
+}
+
+void Worker::joinUpload(std::uint64_t matrix) {
+  auto it = uploads.find(matrix);
+  if (it == uploads.end()) return;
+  activate();
+  cudaCheck(cudaStreamWaitEvent(compute, it->second.done, 0), "upload: join");
+  for (auto& c : it->second.chunks) recycle(c.done);
+  recycle(it->second.done);
+  uploads.erase(it);
+}
+
+void Worker::dropChunkDone(std::uint64_t matrix) {
+  auto it = chunkDone.find(matrix);
+  if (it == chunkDone.end()) return;
+  for (auto& c : it->second) recycle(c.done);
+  chunkDone.erase(it);
 }
 
 void Worker::activate() const { cudaCheck(cudaSetDevice(device), "cudaSetDevice"); }
@@ -538,8 +567,11 @@ void Session::flushWritten(std::uint64_t before) {
       w.activate();
       cudaEvent_t& e = w.lastWrite[pw.first];
       if (!e) cudaCheck(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "worker: write event");
-      cudaCheck(cudaEventRecord(e, w.compute), "worker: record write");
-      if (ipc_) ipcWrite(w.compute, w.flags + slotOf(pw.first), pw.second);
+      // A pending chunked upload is the write being published: from the h2d
+      // stream, after its last chunk (the compute stream has not joined it).
+      cudaStream_t ws = w.uploads.count(pw.first) ? w.h2d : w.compute;
+      cudaCheck(cudaEventRecord(e, ws), "worker: record write");
+      if (ipc_) ipcWrite(ws, w.flags + slotOf(pw.first), pw.second);
     }
   }
 }
@@ -694,12 +726,36 @@ bool recordable(OpCode c) {
 }
 }  // namespace
 
+// Matrices an op reads or writes in place on their owners' compute streams
+// wait for pending chunked uploads first. The GEMM joins only C: it waits on
+// the row chunks of A and B itself (execGemm).
+void Session::joinUploads(const OpDescriptor& op) {
+  int n = 1;
+  switch (op.opcode) {
+    case OpCode::Gemm: {
+      forEachLocal([&](Worker& w) { w.joinUpload(op.ids[2]); });
+      return;
+    }
+    case OpCode::EwBinary:
+    case OpCode::AddRowColSum: n = 3; break;
+    case OpCode::EwUnary: n = 2; break;
+    case OpCode::CreateMatrix:
+    case OpCode::QueryStats:
+    case OpCode::MetaChecksum: return;
+    default: n = 1; break;
+  }
+  forEachLocal([&](Worker& w) {
+    for (int i = 0; i < n; ++i) w.joinUpload(op.ids[i]);
+  });
+}
+
 void Session::requireRecordable(OpCode c) const {
   if (recording_ != 0 && !recordable(c)) throw Error("op not recordable inside an open pipeline recording");
 }
 
 std::uint64_t Session::issue(OpDescriptor& op) {
   requireRecordable(op.opcode);
+  joinUploads(op);
   flushWritten(nextExec_);  // earlier ops' device work is enqueued: publish their writes
   op.execId = nextExec_++;
   curExec_ = op.execId;
@@ -767,6 +823,7 @@ void Session::mutationHook(std::uint64_t id, std::uint64_t oldVersion) {
       w.recycle(e.ready);
     }
     w.beforeMutation(id);
+    w.dropChunkDone(id);
     // Peers that pulled from this worker's tiles of the matrix (SPMD
     // copy-engine plane) must be done before it changes.
     auto rr = remoteReaders_.find(id);
@@ -858,6 +915,8 @@ void Session::destroy(DistMatrix m) {
 
 void Session::execDestroy(std::uint64_t id) {
   forEachLocal([&](Worker& w) {
+    w.joinUpload(id);
+    w.dropChunkDone(id);
     w.beforeMutation(id);
     auto lw = w.lastWrite.find(id);
     if (lw != w.lastWrite.end()) {
@@ -1032,6 +1091,7 @@ std::vector<double> Session::getData(DistMatrix m) {
 
 void Session::reshape(DistMatrix m, const Layout& newLayout, std::optional<Precision> newPrecision) {
   requireRecordable(OpCode::Reshape);
+  forEachLocal([&](Worker& w) { w.joinUpload(m.id()); });
   const MatrixDescriptor old = descriptor(m.id());  // copy: the table entry is replaced below
   MatrixDescriptor nd = old;
   nd.layout = newLayout;
@@ -1436,7 +1496,12 @@ void Session::execGemm(const OpDescriptor& op) {
   bool anyGather = false;
   for (const PlannedNeed& nd : plan.needs)
     if (nd.kind == PlannedNeed::Gather) anyGather = true;
-  if (!anyGather || plan.m < 512 * S) S = 1;
+  // Operands streaming in from the host (chunked uploads read in place):
+  // nothing to exchange, so the row chunks follow the upload's instead.
+  bool streamedA = false;
+  forEachLocal([&](Worker& w) { streamedA = streamedA || w.uploads.count(A.matrixId); });
+  if (!anyGather) S = (streamedA && !plan.transA) ? (opts_.pipelineChunks > 0 ? S : 8u) : 1u;
+  while (S > 1 && plan.m < 512ull * S) --S;
 
   std::vector<std::vector<BandView>> aViews(P), bViews(P);
   for (std::uint32_t w = 0; w < P; ++w) {
@@ -1624,11 +1689,34 @@ void Session::execGemm(const OpDescriptor& op) {
 
   const bool alphaZero = op.s0 == 0.0;
   const std::uint64_t ebA = bytesOf(A.precision), ebB = bytesOf(B.precision), ebC = bytesOf(C.precision);
+  // In-place operand reads of a matrix whose chunked upload is still landing
+  // wait only for the upload chunks covering the rows used.
+  std::vector<std::vector<bool>> aLocal(P), bLocal(P);
+  for (std::uint32_t w = 0; w < P; ++w) {
+    aLocal[w].assign(plan.rowsOf[w].size(), false);
+    bLocal[w].assign(plan.colsOf[w].size(), false);
+  }
+  for (const PlannedNeed& nd : plan.needs)
+    if (nd.kind == PlannedNeed::LocalTile) (nd.operand == 0 ? aLocal : bLocal)[nd.worker][nd.interval] = true;
+  auto waitUploadRows = [&](Worker& w, std::uint64_t matrix, std::uint64_t lo, std::uint64_t hi,
+                            std::set<cudaEvent_t>& waited) {
+    auto up = w.uploads.find(matrix);
+    if (up == w.uploads.end()) return;
+    for (const auto& c : up->second.chunks)
+      if (c.r0 < hi && lo < c.r1 && waited.insert(c.done).second)
+        cudaCheck(cudaStreamWaitEvent(w.compute, c.done, 0), "gemm: wait upload chunk");
+  };
   forEachLocal([&](Worker& w) {
+    w.dropChunkDone(C.matrixId);
+    std::set<cudaEvent_t> waited;
     waitGroup(w, 0);
+    if (!alphaZero)
+      for (std::size_t ci = 0; ci < plan.colsOf[w.rank].size(); ++ci)
+        if (bLocal[w.rank][ci]) waitUploadRows(w, B.matrixId, 0, ~0ull, waited);
     cudaCheck(cudaEventRecord(w.kStart, w.compute), "gemm: timing");
     for (std::uint32_t j = 0; j < S; ++j) {
       waitGroup(w, 1 + j);
+      std::vector<std::pair<std::uint64_t, std::uint64_t>> chunkRows;
       for (DeviceTile& ct : w.tiles.at(C.matrixId)) {
         const TileExtent& e = ct.extent;
         std::size_t ri = 0, ci = 0;
@@ -1641,6 +1729,11 @@ void Session::execGemm(const OpDescriptor& op) {
         const std::uint64_t r0 = std::max<std::uint64_t>(e.rowStart, rg.first);
         const std::uint64_t r1 = std::min<std::uint64_t>(e.rowEnd(), rg.second);
         if (r0 >= r1) continue;
+        if (!alphaZero && aLocal[w.rank][ri]) {
+          if (plan.transA) waitUploadRows(w, A.matrixId, 0, ~0ull, waited);
+          else waitUploadRows(w, A.matrixId, r0, r1, waited);
+        }
+        chunkRows.push_back({r0, r1});
         gm_gemm_desc d{};
         d.m = r1 - r0;
         d.n = e.colCount;
@@ -1675,6 +1768,12 @@ void Session::execGemm(const OpDescriptor& op) {
         void* ws = wsb ? w.workspace(wsb) : nullptr;
         gemmLocal(d, ap, bp, cp, ws, wsb, w.compute);
       }
+      // Row-chunk completion of C (chunked downloads drain behind these).
+      for (const auto& rr : chunkRows) {
+        Worker::UploadChunk c{rr.first, rr.second, w.event()};
+        cudaCheck(cudaEventRecord(c.done, w.compute), "gemm: chunk done");
+        w.chunkDone[C.matrixId].push_back(c);
+      }
     }
     cudaCheck(cudaEventRecord(w.tEnd, w.compute), "gemm: timing");
   });
@@ -1695,8 +1794,10 @@ void Session::execGemm(const OpDescriptor& op) {
 
 void Session::synchronize() {
   forEachLocal([&](Worker& w) {
+    cudaCheck(cudaStreamSynchronize(w.h2d), "sync h2d");
     cudaCheck(cudaStreamSynchronize(w.comm), "sync comm");
     cudaCheck(cudaStreamSynchronize(w.compute), "sync compute");
+    cudaCheck(cudaStreamSynchronize(w.d2h), "sync d2h");
   });
 }
 
@@ -1795,11 +1896,13 @@ void Session::getLocalPacked(DistMatrix m, void* host, std::uint64_t bytes) {
 
 void Session::timerStart() {
   forEachLocal([&](Worker& w) {
-    // The comm stream's prior work is part of "before": fold it in.
-    cudaEvent_t e = w.event();
-    cudaCheck(cudaEventRecord(e, w.comm), "timer");
-    cudaCheck(cudaStreamWaitEvent(w.compute, e, 0), "timer");
-    w.recycle(e);
+    // The side streams' prior work is part of "before": fold it in.
+    for (cudaStream_t side : {w.comm, w.h2d, w.d2h}) {
+      cudaEvent_t e = w.event();
+      cudaCheck(cudaEventRecord(e, side), "timer");
+      cudaCheck(cudaStreamWaitEvent(w.compute, e, 0), "timer");
+      w.recycle(e);
+    }
     cudaCheck(cudaEventRecord(w.uStart, w.compute), "timer start");
   });
 }
@@ -1807,10 +1910,12 @@ void Session::timerStart() {
 float Session::timerStop() {
   float best = 0.0f;
   forEachLocal([&](Worker& w) {
-    cudaEvent_t e = w.event();
-    cudaCheck(cudaEventRecord(e, w.comm), "timer");
-    cudaCheck(cudaStreamWaitEvent(w.compute, e, 0), "timer");
-    w.recycle(e);
+    for (cudaStream_t side : {w.comm, w.h2d, w.d2h}) {
+      cudaEvent_t e = w.event();
+      cudaCheck(cudaEventRecord(e, side), "timer");
+      cudaCheck(cudaStreamWaitEvent(w.compute, e, 0), "timer");
+      w.recycle(e);
+    }
     cudaCheck(cudaEventRecord(w.uEnd, w.compute), "timer stop");
     cudaCheck(cudaEventSynchronize(w.uEnd), "timer sync");
     float ms = 0.0f;

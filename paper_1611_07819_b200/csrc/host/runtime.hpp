@@ -173,9 +173,30 @@ class Worker {
   // every peer): written[slot], then readDone[stream][slot].
   std::uint32_t* flags = nullptr;
 
+  // Host<->device streaming (asynchronous packed local I/O): uploads run on
+  // `h2d` in row chunks, each with an event, so a GEMM can start on the rows
+  // that have landed; downloads run on `d2h` behind the producing op's
+  // per-chunk events. Until an op joins it, a matrix's pending upload is
+  // the authority for its tiles' contents (flushWritten publishes it from
+  // the h2d stream).
+  struct UploadChunk {
+    std::uint64_t r0 = 0, r1 = 0;  // global rows of the matrix
+    cudaEvent_t done = nullptr;
+  };
+  struct Upload {
+    std::vector<UploadChunk> chunks;
+    cudaEvent_t done = nullptr;  // after the last chunk
+  };
+  std::map<std::uint64_t, Upload> uploads;
+  // Row-chunk completion events of the last op that wrote a matrix in
+  // chunks (the GEMM's S row chunks), for chunked downloads.
+  std::map<std::uint64_t, std::vector<UploadChunk>> chunkDone;
+  void joinUpload(std::uint64_t matrix);  // compute stream waits; entry dropped
+  void dropChunkDone(std::uint64_t matrix);
+
   std::uint32_t rank;
   int device;
-  cudaStream_t compute = nullptr, comm = nullptr;
+  cudaStream_t compute = nullptr, comm = nullptr, h2d = nullptr, d2h = nullptr;
   DeviceArena arena;
   DescriptorTable descs;
   std::map<std::uint64_t, std::vector<DeviceTile>> tiles;
@@ -310,12 +331,21 @@ class Session {
   std::uint64_t localBytes(DistMatrix m) const;
   void setLocalPacked(DistMatrix m, const void* host, std::uint64_t bytes);
   void getLocalPacked(DistMatrix m, void* host, std::uint64_t bytes);
+  // Asynchronous variants (stream-ordered; the host buffer must stay valid
+  // and unmodified until synchronize()). Uploads move in row chunks of about
+  // `chunkBytes` on the workers' h2d streams; a following GEMM that reads
+  // the tile in place starts on each row chunk as it lands. Downloads follow
+  // the producing GEMM's row chunks on the d2h streams. Pinned host memory
+  // makes them truly asynchronous.
+  void setLocalPackedAsync(DistMatrix m, const void* host, std::uint64_t bytes, std::uint64_t chunkBytes = 0);
+  void getLocalPackedAsync(DistMatrix m, void* host, std::uint64_t bytes);
   void timerStart();
   float timerStop();
 
  private:
   std::uint64_t issue(OpDescriptor& op);  // validate + metadata + per-worker mirror
   void requireRecordable(OpCode c) const;
+  void joinUploads(const OpDescriptor& op);
   Worker* local(std::uint32_t rank) const;
   bool isLocal(std::uint32_t rank) const;
   void execCreate(const OpDescriptor& op);

@@ -349,6 +349,12 @@ class Session:
     def getLocalPacked(self, m: DistMatrix, ptr: int, nbytes: int):
         check(_lib.load().gm_matrix_get_local_packed(self._h, m.id, ptr, nbytes))
 
+    def setLocalPackedAsync(self, m: DistMatrix, ptr: int, nbytes: int, chunk_bytes: int = 0):
+        check(_lib.load().gm_matrix_set_local_packed_async(self._h, m.id, ptr, nbytes, chunk_bytes))
+
+    def getLocalPackedAsync(self, m: DistMatrix, ptr: int, nbytes: int):
+        check(_lib.load().gm_matrix_get_local_packed_async(self._h, m.id, ptr, nbytes))
+
     def timerStart(self):
         check(_lib.load().gm_timer_start(self._h))
 
