@@ -149,7 +149,108 @@ def run(transport, nccl_id):
                 np.abs(vals).max() > 0
             say(f"[rank0 {plane}] async RAW/WAR chain bitwise_vs_1gpu={good} max|C|={np.abs(vals).max():.3g}")
             ok = ok and good
+        # FC train step (reference Trainer order) recorded once and replayed,
+        # vs the same pipeline on one process with `world` workers on one GPU
+        fc = fc_steps(s, 3)
+        if rank == 0:
+            with G.Session(workers=world, devices=[local]) as s1:
+                ref = fc_steps(s1, 3)
+            good = all(np.array_equal(fc[k].view(np.uint8), ref[k].view(np.uint8)) for k in fc)
+            say(f"[rank0 {plane}] FC step record/replay (gemm, biasAdd, relu, reluGrad, rowcolsum, axpy, "
+                f"replication) bitwise_vs_1process={good}")
+            ok = ok and good
+        # chunked async host streaming: upload A/B, gemm, download C
+        n = 1024
+        lay = G.makeGridLayout(n, n, pr, pc, g)
+        A = s.createMatrix(n, n, G.Precision.BF16, lay)
+        B = s.createMatrix(n, n, G.Precision.BF16, lay)
+        C = s.createMatrix(n, n, G.Precision.BF16, lay)
+        s.fillUniform(A, 21)
+        s.fillUniform(B, 22)
+        G.gemm(s, A, B, C, 1.0, 0.0)
+        want_c = np.zeros(s.localBytes(C), np.uint8)
+        s.getLocalPacked(C, want_c.ctypes.data, want_c.nbytes)
+        ha = np.zeros(s.localBytes(A), np.uint8)
+        hb = np.zeros(s.localBytes(B), np.uint8)
+        s.getLocalPacked(A, ha.ctypes.data, ha.nbytes)
+        s.getLocalPacked(B, hb.ctypes.data, hb.nbytes)
+        s.fillUniform(A, 23)
+        s.fillUniform(B, 24)  # overwritten again by the uploads below
+        hc = np.zeros_like(want_c)
+        for _ in range(2):
+            s.setLocalPackedAsync(B, hb.ctypes.data, hb.nbytes, 64 * 1024)
+            s.setLocalPackedAsync(A, ha.ctypes.data, ha.nbytes, 64 * 1024)
+            s.gemmAsync(A, B, C)
+            s.getLocalPackedAsync(C, hc.ctypes.data, hc.nbytes)
+        s.synchronize()
+        good = bool(np.array_equal(hc, want_c))
+        t = torch.tensor([1 if good else 0], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MIN)
+        good = t.item() == 1
+        say(f"[rank0 {plane}] async chunked upload/gemm/download == sync path on every rank: {good}")
+        ok = ok and good
+        # checkpoint (rank 0 writes the DMCK file) and collective restore
+        path = f"/tmp/spmd_ckpt_{os.getpid() if rank == 0 else 0}.dmck"
+        obj = [path]
+        dist.broadcast_object_list(obj, src=0)
+        path = obj[0]
+        before = s.getDataRaw(C)
+        s.checkpoint(path)
+        dist.barrier()
+    with G.Session.restore(path, workers=world, spmd_rank=rank, devices=[local], nccl_id=_fresh_id(),
+                           transport=transport) as s2:
+        after = s2.getDataRaw(s2.matrix(C.id))
+        good = bool(np.array_equal(after, before))
+        say(f"[rank0 {plane}] checkpoint/restore across ranks ok={good}")
+        ok = ok and good
+    dist.barrier()
+    if rank == 0:
+        os.remove(path)
     return ok
+
+
+def _fresh_id():
+    obj = [G.nccl_unique_id() if rank == 0 else None]
+    dist.broadcast_object_list(obj, src=0)
+    return obj[0]
+
+
+def fc_steps(s, steps):
+    S = G.Precision.Single
+    batch, fin, fout = 256, 384, 192
+    M = dict(X=(batch, fin, G.makeRowBlockLayout), W=(fin, fout, G.makeColBlockLayout),
+             B=(1, fout, G.makeColBlockLayout), Z=(batch, fout, G.makeRowBlockLayout),
+             A=(batch, fout, G.makeRowBlockLayout), D=(batch, fout, G.makeRowBlockLayout),
+             DW=(fin, fout, G.makeColBlockLayout), DB=(1, fout, G.makeColBlockLayout),
+             R=(batch, 1, G.makeRowBlockLayout), DX=(batch, fin, G.makeRowBlockLayout))
+    m = {k: s.createMatrix(r, c, S, lay(r, c, g)) for k, (r, c, lay) in M.items()}
+    s.fillUniform(m["X"], 1)
+    s.fillUniform(m["W"], 2, -0.05, 0.05)
+    s.fillUniform(m["B"], 3, -0.1, 0.1)
+    s.replicateSync(m["W"])
+    s.replicateSync(m["B"])
+    for i in range(steps):
+        s.fillUniform(m["D"], 40 + i)
+        if i == 0:
+            pid = s.beginRecord()
+        if i == 0:
+            G.gemm(s, m["X"], m["W"], m["Z"], 1.0, 0.0)
+            G.biasAdd(s, m["Z"], m["B"])
+            G.relu(s, m["Z"], m["A"])
+            G.reluGrad(s, m["Z"], m["D"])
+            G.gemm(s, m["X"], m["D"], m["DW"], 1.0, 0.0, True, False)
+            G.setConst(s, m["R"], 0.0)
+            G.setConst(s, m["DB"], 0.0)
+            G.addRowColSum(s, m["D"], m["R"], m["DB"], 1.0, True)
+            G.gemm(s, m["D"], m["W"], m["DX"], 1.0, 0.0, False, True)
+            G.axpy(s, -0.01, m["DW"], m["W"])
+            G.axpy(s, -0.01, m["DB"], m["B"])
+            s.replicateAsync(m["W"])
+            s.replicateAsync(m["B"])
+            s.endRecord()
+        else:
+            s.replay(pid)
+    return {k: s.getDataRaw(m[k]) for k in ("W", "B", "DX", "DB", "A")}
 
 
 ok = True
