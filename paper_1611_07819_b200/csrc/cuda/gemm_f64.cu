@@ -9,13 +9,15 @@
 // as storeScalar does, precision.hpp:129-149). Each output element is one
 // fixed ascending-k FMA chain, independent of tiling and distribution.
 //
-// Tiling: 128x128 CTA tile, BK=16, 8 warps (2 x 4) of 64x32, 3-stage
-// cp.async ring with zero-filled out-of-range chunks.
+// Tiling: 64x128 CTA tile, BK=16, 4 warps (2 x 2) of 32x64, two CTAs per SM,
+// 3-stage cp.async ring with zero-filled out-of-range chunks; fragments for
+// the next k-step are loaded while the current one's DMMAs issue.
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
 
 #include "convert.h"
 #include "gemm_f64.h"
@@ -24,10 +26,19 @@ namespace gmk {
 
 namespace {
 
-constexpr int kBM = 128, kBN = 128, kBK = 16, kStages = 3, kThreads = 256;
-constexpr int kPadK = kBK + 4;    // [mn][k] tiles: 20 doubles per row
-constexpr int kPadMN = kBM + 4;   // [k][mn] tiles: 132 doubles per row
-constexpr int kTileDoubles = kBM * kPadK > kBK * kPadMN ? kBM * kPadK : kBK * kPadMN;
+constexpr int kBK = 16, kStages = 3;
+
+template <int BM, int BN, int WGM, int WGN>
+struct F64Cfg {
+  static constexpr int kThreads = WGM * WGN * 32;
+  static constexpr int kWM = BM / WGM, kWN = BN / WGN;  // warp tile
+  static constexpr int kMI = kWM / 8, kNJ = kWN / 8;     // m8n8 fragments per warp
+  // A is [BM][BK+4] (k-contiguous) or [BK][BM+4]; B is [BN][BK+4] or [BK][BN+4].
+  static constexpr int kASize = BM * (kBK + 4) > kBK * (BM + 4) ? BM * (kBK + 4) : kBK * (BM + 4);
+  static constexpr int kBSize = BN * (kBK + 4) > kBK * (BN + 4) ? BN * (kBK + 4) : kBK * (BN + 4);
+  static constexpr int kStage = kASize + kBSize;  // doubles
+  static constexpr size_t kSmem = static_cast<size_t>(kStages) * kStage * sizeof(double);
+};
 
 struct F64Params {
   const double* a;
@@ -57,16 +68,15 @@ __device__ __forceinline__ void dmma(double (&d)[2], double a, double b) {
       : "d"(a), "d"(b));
 }
 
-// Loads a (rows x 16) slab of a row-major operand whose contiguous axis is k
-// ("k-contiguous", dst [mn][k]) or a (16 x cols) slab whose contiguous axis is
-// mn ("mn-contiguous", dst [k][mn]). Out-of-range chunks are zero-filled.
-template <bool kKContig>
-__device__ __forceinline__ void load_tile(double* dst, const double* src, uint64_t ld,
-                                          uint32_t mn0, uint32_t mn_lim, uint32_t k0,
-                                          uint32_t k_lim) {
+// Loads a (ROWS x 16) slab of a row-major operand whose contiguous axis is k
+// ("k-contiguous", dst [mn][BK+4]) or a (16 x ROWS) slab whose contiguous
+// axis is mn ("mn-contiguous", dst [k][ROWS+4]). Out-of-range chunks are
+// zero-filled.
+template <bool kKContig, int ROWS, int THREADS>
+__device__ __forceinline__ void load_tile(double* dst, const double* src, uint64_t ld, uint32_t mn0,
+                                          uint32_t mn_lim, uint32_t k0, uint32_t k_lim) {
   if constexpr (kKContig) {
-    // 128 rows x 8 chunks of 2 doubles.
-    for (int i = threadIdx.x; i < kBM * (kBK / 2); i += kThreads) {
+    for (int i = threadIdx.x; i < ROWS * (kBK / 2); i += THREADS) {
       const int r = i / (kBK / 2), ch = i % (kBK / 2);
       const uint32_t gr = mn0 + r, gk = k0 + ch * 2;
       uint32_t bytes = 0;
@@ -75,12 +85,11 @@ __device__ __forceinline__ void load_tile(double* dst, const double* src, uint64
         bytes = (gk + 1 < k_lim) ? 16 : 8;
         g = src + static_cast<uint64_t>(gr) * ld + gk;
       }
-      cp_async16(dst + r * kPadK + ch * 2, g, bytes);
+      cp_async16(dst + r * (kBK + 4) + ch * 2, g, bytes);
     }
   } else {
-    // 16 rows (k) x 64 chunks.
-    for (int i = threadIdx.x; i < kBK * (kBM / 2); i += kThreads) {
-      const int r = i / (kBM / 2), ch = i % (kBM / 2);
+    for (int i = threadIdx.x; i < kBK * (ROWS / 2); i += THREADS) {
+      const int r = i / (ROWS / 2), ch = i % (ROWS / 2);
       const uint32_t gk = k0 + r, gm = mn0 + ch * 2;
       uint32_t bytes = 0;
       const double* g = src;
@@ -88,7 +97,7 @@ __device__ __forceinline__ void load_tile(double* dst, const double* src, uint64
         bytes = (gm + 1 < mn_lim) ? 16 : 8;
         g = src + static_cast<uint64_t>(gk) * ld + gm;
       }
-      cp_async16(dst + r * kPadMN + ch * 2, g, bytes);
+      cp_async16(dst + r * (ROWS + 4) + ch * 2, g, bytes);
     }
   }
 }
@@ -125,29 +134,30 @@ __device__ __forceinline__ void store_c(const F64Params& p, uint32_t r, uint32_t
   }
 }
 
-template <bool kTA, bool kTB>
-__global__ void __launch_bounds__(kThreads, 1) f64_gemm_kernel(const F64Params p) {
+template <int BM, int BN, int WGM, int WGN, int MINB, bool kTA, bool kTB>
+__global__ void __launch_bounds__(WGM * WGN * 32, MINB) f64_gemm_kernel(const F64Params p) {
+  using Cfg = F64Cfg<BM, BN, WGM, WGN>;
+  constexpr int MI = Cfg::kMI, NJ = Cfg::kNJ;
   extern __shared__ __align__(16) double sm[];
-  double* sa = sm;                              // [kStages][kTileDoubles]
-  double* sb = sm + kStages * kTileDoubles;     // [kStages][kTileDoubles]
 
-  const uint32_t m0 = blockIdx.y * kBM, n0 = blockIdx.x * kBN;
+  const uint32_t m0 = blockIdx.y * BM, n0 = blockIdx.x * BN;
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-  const int wm = warp / 4, wn = warp % 4;  // 2 x 4 warps, 64 x 32 each
+  const int wm = warp / WGN, wn = warp % WGN;
   const int gid = lane / 4, tig = lane % 4;
 
-  double acc[8][4][2];
+  double acc[MI][NJ][2];
 #pragma unroll
-  for (int i = 0; i < 8; ++i)
+  for (int i = 0; i < MI; ++i)
 #pragma unroll
-    for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+    for (int j = 0; j < NJ; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
 
   const uint32_t nk = (p.k + kBK - 1) / kBK;
   auto issue = [&](uint32_t kb, int slot) {
+    double* st = sm + slot * Cfg::kStage;
     // A: op(A) is m x k; stored m x k (k-contiguous) or k x m (transA).
-    load_tile<!kTA>(sa + slot * kTileDoubles, p.a, p.lda, m0, p.m, kb * kBK, p.k);
+    load_tile<!kTA, BM, Cfg::kThreads>(st, p.a, p.lda, m0, p.m, kb * kBK, p.k);
     // B: op(B) is k x n; stored k x n (n-contiguous) or n x k (transB).
-    load_tile<kTB>(sb + slot * kTileDoubles, p.b, p.ldb, n0, p.n, kb * kBK, p.k);
+    load_tile<kTB, BN, Cfg::kThreads>(st + Cfg::kASize, p.b, p.ldb, n0, p.n, kb * kBK, p.k);
   };
 
 #pragma unroll
@@ -156,6 +166,20 @@ __global__ void __launch_bounds__(kThreads, 1) f64_gemm_kernel(const F64Params p
     cp_async_commit();
   }
 
+  double af[2][MI], bf[2][NJ];
+  auto frags = [&](const double* ta, const double* tb, int kk, int buf) {
+#pragma unroll
+    for (int i = 0; i < MI; ++i) {
+      const int r = wm * Cfg::kWM + i * 8 + gid;
+      af[buf][i] = kTA ? ta[(kk + tig) * (BM + 4) + r] : ta[r * (kBK + 4) + kk + tig];
+    }
+#pragma unroll
+    for (int j = 0; j < NJ; ++j) {
+      const int c = wn * Cfg::kWN + j * 8 + gid;
+      bf[buf][j] = kTB ? tb[c * (kBK + 4) + kk + tig] : tb[(kk + tig) * (BN + 4) + c];
+    }
+  };
+
   for (uint32_t kb = 0; kb < nk; ++kb) {
     cp_async_wait<kStages - 2>();
     __syncthreads();
@@ -163,38 +187,44 @@ __global__ void __launch_bounds__(kThreads, 1) f64_gemm_kernel(const F64Params p
     if (nxt < nk) issue(nxt, nxt % kStages);
     cp_async_commit();
 
-    const double* ta = sa + (kb % kStages) * kTileDoubles;
-    const double* tb = sb + (kb % kStages) * kTileDoubles;
+    const double* ta = sm + (kb % kStages) * Cfg::kStage;
+    const double* tb = ta + Cfg::kASize;
+    frags(ta, tb, 0, 0);
 #pragma unroll
     for (int kk = 0; kk < kBK; kk += 4) {
-      double af[8], bf[4];
+      const int cur = (kk / 4) & 1;
+      if (kk + 4 < kBK) frags(ta, tb, kk + 4, cur ^ 1);  // next fragments in flight under the MMAs
 #pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        const int r = wm * 64 + i * 8 + gid;
-        af[i] = kTA ? ta[(kk + tig) * kPadMN + r] : ta[r * kPadK + kk + tig];
-      }
+      for (int i = 0; i < MI; ++i)
 #pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        const int c = wn * 32 + j * 8 + gid;
-        bf[j] = kTB ? tb[c * kPadK + kk + tig] : tb[(kk + tig) * kPadMN + c];
-      }
-#pragma unroll
-      for (int i = 0; i < 8; ++i)
-#pragma unroll
-        for (int j = 0; j < 4; ++j) dmma(acc[i][j], af[i], bf[j]);
+        for (int j = 0; j < NJ; ++j) dmma(acc[i][j], af[cur][i], bf[cur][j]);
     }
   }
   cp_async_wait<0>();
 
 #pragma unroll
-  for (int i = 0; i < 8; ++i)
+  for (int i = 0; i < MI; ++i)
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const uint32_t r = m0 + wm * 64 + i * 8 + gid;
-      const uint32_t c = n0 + wn * 32 + j * 8 + tig * 2;
+    for (int j = 0; j < NJ; ++j) {
+      const uint32_t r = m0 + wm * Cfg::kWM + i * 8 + gid;
+      const uint32_t c = n0 + wn * Cfg::kWN + j * 8 + tig * 2;
       store_c(p, r, c, acc[i][j][0]);
       store_c(p, r, c + 1, acc[i][j][1]);
     }
+}
+
+template <int BM, int BN, int WGM, int WGN, int MINB>
+void launch_f64(const F64Params& p, bool ta, bool tb, cudaStream_t stream) {
+  using Cfg = F64Cfg<BM, BN, WGM, WGN>;
+  dim3 grid((p.n + BN - 1) / BN, (p.m + BM - 1) / BM);
+  auto go = [&](auto kern) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(Cfg::kSmem));
+    kern<<<grid, Cfg::kThreads, Cfg::kSmem, stream>>>(p);
+  };
+  if (!ta && !tb) go(f64_gemm_kernel<BM, BN, WGM, WGN, MINB, false, false>);
+  else if (!ta && tb) go(f64_gemm_kernel<BM, BN, WGM, WGN, MINB, false, true>);
+  else if (ta && !tb) go(f64_gemm_kernel<BM, BN, WGM, WGN, MINB, true, false>);
+  else go(f64_gemm_kernel<BM, BN, WGM, WGN, MINB, true, true>);
 }
 
 }  // namespace
@@ -213,17 +243,15 @@ int f64_gemm(const F64GemmArgs& g, cudaStream_t stream, const char** err) {
   p.c_prec = g.c_prec;
   p.alpha = g.alpha;
   p.beta = g.beta;
-  const size_t smem = 2ull * kStages * kTileDoubles * sizeof(double);
-  dim3 grid((p.n + kBN - 1) / kBN, (p.m + kBM - 1) / kBM);
-  auto pick = [&](auto kern) {
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-    kern<<<grid, kThreads, smem, stream>>>(p);
-    count_launch();
-  };
-  if (!g.trans_a && !g.trans_b) pick(f64_gemm_kernel<false, false>);
-  else if (!g.trans_a && g.trans_b) pick(f64_gemm_kernel<false, true>);
-  else if (g.trans_a && !g.trans_b) pick(f64_gemm_kernel<true, false>);
-  else pick(f64_gemm_kernel<true, true>);
+  // 64x128 CTA tiles, 4 warps of 32x64, two CTAs per SM (their barriers
+  // interleave); GM_F64_TILE=128 selects the 128x128 / 8-warp variant.
+  static const int variant = [] {
+    const char* v = std::getenv("GM_F64_TILE");
+    return v ? std::atoi(v) : 64;
+  }();
+  if (variant == 128) launch_f64<128, 128, 2, 4, 1>(p, g.trans_a, g.trans_b, stream);
+  else launch_f64<64, 128, 2, 2, 2>(p, g.trans_a, g.trans_b, stream);
+  count_launch();
   const cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) {
     *err = cudaGetErrorString(e);

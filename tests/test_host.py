@@ -196,3 +196,17 @@ def test_session_without_gpu_fails_loudly():
         pytest.skip("GPU present")
     with pytest.raises(G.GmError):
         G.Session(workers=1)
+
+
+def test_library_then_torch_import_order():
+    """The library must not pull an older libnccl.so.2 into the process ahead
+    of torch's (same SONAME: the first one loaded wins, and torch then fails
+    to import with undefined NCCL symbols)."""
+    import subprocess
+    import sys
+    code = ("import sys; sys.path.insert(0, %r)\n"
+            "from paper_1611_07819_b200 import _lib; _lib.load()\n"
+            "import torch, torch.distributed\n"
+            "print('ok')\n") % ROOT
+    out = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=300)
+    assert out.returncode == 0 and "ok" in out.stdout, out.stderr[-2000:]
