@@ -213,6 +213,175 @@ __global__ void __launch_bounds__(WGM * WGN * 32, MINB) f64_gemm_kernel(const F6
     }
 }
 
+// Paired-fragment variant (64x128 CTA, 4 warps of 32x64, two CTAs per SM):
+// every fragment load is one 16-byte LDS serving two MMAs. Along an
+// operand's contiguous axis two neighbouring elements go to the same lane:
+//   * k-contiguous operands (A, or B^T): lane tig takes k = 2*tig + q of the
+//     8-wide k pair p, i.e. MMA k-step 2p + q uses k = 8p + 2*tig + q;
+//   * mn-contiguous operands (A^T, or B): m/n tiles come in pairs whose
+//     MMA-local row/column g maps to 2g (first) and 2g + 1 (second) of the
+//     16-wide pair, which the epilogue undoes.
+// Each output element is still one fixed-order FMA chain over k (the k
+// order is a fixed global permutation within every 8-wide k group), so the
+// result is independent of tiling and distribution. Shared-memory row
+// pitches of 24 doubles (k-contiguous, 192 B = 64 mod 128) and BM/BN + 2
+// doubles (mn-contiguous: lanes read rows 2*tig + q apart, and 2 x pitch =
+// 32 mod 128 B) keep the 16-byte loads conflict-free.
+namespace paired {
+constexpr int BM = 64, BN = 128, kThreads = 128, kPK = 24;
+constexpr int kASize = BM * kPK > kBK * (BM + 2) ? BM * kPK : kBK * (BM + 2);
+constexpr int kBSize = BN * kPK > kBK * (BN + 2) ? BN * kPK : kBK * (BN + 2);
+constexpr int kStage = kASize + kBSize;
+constexpr size_t kSmem = static_cast<size_t>(kStages) * kStage * sizeof(double);
+
+template <bool kKContig, int ROWS>
+__device__ __forceinline__ void load(double* dst, const double* src, uint64_t ld, uint32_t mn0, uint32_t mn_lim,
+                                     uint32_t k0, uint32_t k_lim) {
+  if constexpr (kKContig) {
+    for (int i = threadIdx.x; i < ROWS * (kBK / 2); i += kThreads) {
+      const int r = i / (kBK / 2), ch = i % (kBK / 2);
+      const uint32_t gr = mn0 + r, gk = k0 + ch * 2;
+      uint32_t bytes = 0;
+      const double* g = src;
+      if (gr < mn_lim && gk < k_lim) {
+        bytes = (gk + 1 < k_lim) ? 16 : 8;
+        g = src + static_cast<uint64_t>(gr) * ld + gk;
+      }
+      cp_async16(dst + r * kPK + ch * 2, g, bytes);
+    }
+  } else {
+    for (int i = threadIdx.x; i < kBK * (ROWS / 2); i += kThreads) {
+      const int r = i / (ROWS / 2), ch = i % (ROWS / 2);
+      const uint32_t gk = k0 + r, gm = mn0 + ch * 2;
+      uint32_t bytes = 0;
+      const double* g = src;
+      if (gk < k_lim && gm < mn_lim) {
+        bytes = (gm + 1 < mn_lim) ? 16 : 8;
+        g = src + static_cast<uint64_t>(gk) * ld + gm;
+      }
+      cp_async16(dst + r * (ROWS + 2) + ch * 2, g, bytes);
+    }
+  }
+}
+
+__device__ __forceinline__ double2 lds2(const double* p) { return *reinterpret_cast<const double2*>(p); }
+
+template <bool kTA, bool kTB>
+__global__ void __launch_bounds__(kThreads, 2) kernel(const F64Params p) {
+  extern __shared__ __align__(16) double sm[];
+  const uint32_t m0 = blockIdx.y * BM, n0 = blockIdx.x * BN;
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int wm = warp / 2, wn = warp % 2;  // warp tile 32 x 64
+  const int gid = lane / 4, tig = lane % 4;
+  constexpr int MI = 4, NJ = 8;
+
+  double acc[MI][NJ][2];
+#pragma unroll
+  for (int i = 0; i < MI; ++i)
+#pragma unroll
+    for (int j = 0; j < NJ; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+
+  const uint32_t nk = (p.k + kBK - 1) / kBK;
+  auto issue = [&](uint32_t kb, int slot) {
+    double* st = sm + slot * kStage;
+    load<!kTA, BM>(st, p.a, p.lda, m0, p.m, kb * kBK, p.k);
+    load<kTB, BN>(st + kASize, p.b, p.ldb, n0, p.n, kb * kBK, p.k);
+  };
+#pragma unroll
+  for (int s = 0; s < kStages - 1; ++s) {
+    if (static_cast<uint32_t>(s) < nk) issue(s, s);
+    cp_async_commit();
+  }
+
+  // Fragment loaders for MMA k-step ks (0..3) of the current block.
+  auto fragA = [&](const double* ta, int ks, double (&a)[MI]) {
+    const int pp = ks / 2, q = ks % 2;
+    if constexpr (!kTA) {  // [m][kPK], k-paired: one LDS per m-tile per k pair
+#pragma unroll
+      for (int i = 0; i < MI; ++i) {
+        const double2 v = lds2(ta + (wm * 32 + i * 8 + gid) * kPK + pp * 8 + 2 * tig);
+        a[i] = q ? v.y : v.x;
+      }
+    } else {  // [k][BM+2], m-paired tiles (2ii, 2ii+1)
+#pragma unroll
+      for (int ii = 0; ii < MI / 2; ++ii) {
+        const double2 v = lds2(ta + (pp * 8 + 2 * tig + q) * (BM + 2) + wm * 32 + ii * 16 + 2 * gid);
+        a[2 * ii] = v.x;
+        a[2 * ii + 1] = v.y;
+      }
+    }
+  };
+  auto fragB = [&](const double* tb, int ks, double (&b)[NJ]) {
+    const int pp = ks / 2, q = ks % 2;
+    if constexpr (kTB) {  // [n][kPK], k-paired
+#pragma unroll
+      for (int j = 0; j < NJ; ++j) {
+        const double2 v = lds2(tb + (wn * 64 + j * 8 + gid) * kPK + pp * 8 + 2 * tig);
+        b[j] = q ? v.y : v.x;
+      }
+    } else {  // [k][BN+2], n-paired tiles (2jj, 2jj+1)
+#pragma unroll
+      for (int jj = 0; jj < NJ / 2; ++jj) {
+        const double2 v = lds2(tb + (pp * 8 + 2 * tig + q) * (BN + 2) + wn * 64 + jj * 16 + 2 * gid);
+        b[2 * jj] = v.x;
+        b[2 * jj + 1] = v.y;
+      }
+    }
+  };
+
+  for (uint32_t kb = 0; kb < nk; ++kb) {
+    cp_async_wait<kStages - 2>();
+    __syncthreads();
+    const uint32_t nxt = kb + kStages - 1;
+    if (nxt < nk) issue(nxt, nxt % kStages);
+    cp_async_commit();
+    const double* ta = sm + (kb % kStages) * kStage;
+    const double* tb = ta + kASize;
+    double a[2][MI], b[2][NJ];
+    fragA(ta, 0, a[0]);
+    fragB(tb, 0, b[0]);
+#pragma unroll
+    for (int ks = 0; ks < 4; ++ks) {
+      const int cur = ks & 1;
+      if (ks + 1 < 4) {
+        fragA(ta, ks + 1, a[cur ^ 1]);
+        fragB(tb, ks + 1, b[cur ^ 1]);
+      }
+#pragma unroll
+      for (int i = 0; i < MI; ++i)
+#pragma unroll
+        for (int j = 0; j < NJ; ++j) dmma(acc[i][j], a[cur][i], b[cur][j]);
+    }
+  }
+  cp_async_wait<0>();
+
+#pragma unroll
+  for (int i = 0; i < MI; ++i) {
+    const uint32_t r = m0 + wm * 32 + (kTA ? (i / 2) * 16 + 2 * gid + (i % 2) : i * 8 + gid);
+#pragma unroll
+    for (int j = 0; j < NJ; ++j)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int cl = 2 * tig + e;  // MMA-local column
+        const uint32_t c = n0 + wn * 64 + (kTB ? j * 8 + cl : (j / 2) * 16 + 2 * cl + (j % 2));
+        store_c(p, r, c, acc[i][j][e]);
+      }
+  }
+}
+
+void launch(const F64Params& p, bool ta, bool tb, cudaStream_t stream) {
+  dim3 grid((p.n + BN - 1) / BN, (p.m + BM - 1) / BM);
+  auto go = [&](auto kern) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kSmem));
+    kern<<<grid, kThreads, kSmem, stream>>>(p);
+  };
+  if (!ta && !tb) go(kernel<false, false>);
+  else if (!ta && tb) go(kernel<false, true>);
+  else if (ta && !tb) go(kernel<true, false>);
+  else go(kernel<true, true>);
+}
+}  // namespace paired
+
 template <int BM, int BN, int WGM, int WGN, int MINB>
 void launch_f64(const F64Params& p, bool ta, bool tb, cudaStream_t stream) {
   using Cfg = F64Cfg<BM, BN, WGM, WGN>;
@@ -243,14 +412,15 @@ int f64_gemm(const F64GemmArgs& g, cudaStream_t stream, const char** err) {
   p.c_prec = g.c_prec;
   p.alpha = g.alpha;
   p.beta = g.beta;
-  // 64x128 CTA tiles, 4 warps of 32x64, two CTAs per SM (their barriers
-  // interleave); GM_F64_TILE=128 selects the 128x128 / 8-warp variant.
+  // Paired-fragment 64x128 kernel (default); GM_F64_TILE=65 selects the
+  // plain 64x128 kernel, GM_F64_TILE=128 the 128x128 / 8-warp one.
   static const int variant = [] {
     const char* v = std::getenv("GM_F64_TILE");
     return v ? std::atoi(v) : 64;
   }();
   if (variant == 128) launch_f64<128, 128, 2, 4, 1>(p, g.trans_a, g.trans_b, stream);
-  else launch_f64<64, 128, 2, 2, 2>(p, g.trans_a, g.trans_b, stream);
+  else if (variant == 65) launch_f64<64, 128, 2, 2, 2>(p, g.trans_a, g.trans_b, stream);
+  else paired::launch(p, g.trans_a, g.trans_b, stream);
   count_launch();
   const cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) {
