@@ -23,12 +23,38 @@ namespace gridmath {
 void Session::setLocalPackedAsync(DistMatrix m, const void* host, std::uint64_t bytes, std::uint64_t chunkBytes) {
   const MatrixDescriptor d = descriptor(m.id());
   if (bytes != localBytes(m)) throw Error("setLocalPacked: byte count mismatch");
+  const std::uint64_t chunk = chunkBytes ? chunkBytes : (256ull << 20);
   OpDescriptor op;
   op.opcode = OpCode::SetData;
   op.ids[0] = m.id();
+  op.ids[1] = chunk;  // the chunk geometry travels with the op: every rank can follow the chunks
   issue(op);  // joins an earlier upload of m (WAW); WAR waits land on the compute stream
   const std::uint64_t eb = bytesOf(d.precision);
-  const std::uint64_t chunk = chunkBytes ? chunkBytes : (256ull << 20);
+  // Replicated chunk bookkeeping: each owner's upload-chunk counter for the
+  // matrix's flag slot advances by its number of chunks.
+  if (ipc_) {
+    ChunkedWrite cw;
+    cw.execId = op.execId;
+    cw.chunkBytes = chunk;
+    cw.base.assign(opts_.workers, 0);
+    const std::uint32_t slot = slotOf(m.id());
+    std::vector<std::uint32_t> n(opts_.workers, 0);
+    for (const auto& t : d.layout.tiles) {
+      const std::uint64_t rpc = std::max<std::uint64_t>(1, chunk / std::max<std::uint64_t>(t.first.colCount * eb, 1));
+      n[t.second.rank] += static_cast<std::uint32_t>((t.first.rowCount + rpc - 1) / rpc);
+    }
+    for (std::uint32_t r = 0; r < opts_.workers; ++r) {
+      std::uint32_t& cnt = upCount_[{r, slot}];
+      cw.base[r] = cnt;
+      cnt += n[r];
+    }
+    chunked_[m.id()] = std::move(cw);
+  } else {
+    ChunkedWrite cw;
+    cw.execId = op.execId;
+    cw.chunkBytes = chunk;
+    chunked_[m.id()] = std::move(cw);
+  }
   const auto* src = static_cast<const std::uint8_t*>(host);
   std::set<Worker*> started;
   for (const auto& t : d.layout.tiles) {
@@ -57,6 +83,9 @@ void Session::setLocalPackedAsync(DistMatrix m, const void* host, std::uint64_t 
                   "upload: chunk");
         Worker::UploadChunk c{e.rowStart + r, e.rowStart + r + n, w->event()};
         cudaCheck(cudaEventRecord(c.done, w->h2d), "upload: chunk event");
+        if (ipc_)  // peers pulling these rows wait for this value (ChunkedWrite::base)
+          ipcWrite(w->h2d, w->flags + kUpChunkOff + slotOf(m.id()),
+                   chunked_.at(m.id()).base[w->rank] + static_cast<std::uint32_t>(up.chunks.size()) + 1);
         up.chunks.push_back(c);
       }
     }

@@ -13,6 +13,11 @@ namespace gridmath {
 
 constexpr std::uint64_t kPitchAlign = 16;  // TMA row-stride rule
 
+// SPMD flag page (u32 words): written[kSlots], readDone[2][kSlots] (comm,
+// compute), upChunk[kSlots] (chunks of chunked uploads completed, per slot).
+constexpr std::uint32_t kSlots = 16384;
+constexpr std::size_t kUpChunkOff = 3ull * kSlots;
+
 // Row pitch (elements) of a device tile / band: 16-byte multiple.
 inline std::uint64_t paddedLd(std::uint64_t cols, std::uint64_t eb) {
   return ((cols * eb + kPitchAlign - 1) / kPitchAlign * kPitchAlign) / eb;

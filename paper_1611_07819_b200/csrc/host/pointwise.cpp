@@ -84,6 +84,9 @@ void Session::resolveReads(std::vector<ReadNeed>& needs, std::uint64_t mutated, 
       x.cols = piece->cols();
       x.eb = static_cast<std::uint32_t>(eb);
       x.matrix = M.matrixId;
+      x.hasOrigin = true;
+      x.r0 = piece->r0;
+      x.c0 = piece->c0;
       const BandView sv = srcView(M, tl.second.rank, *piece);
       x.srcPtr = sv.ptr;
       x.srcLd = sv.ld;

@@ -30,9 +30,7 @@ namespace gridmath {
 
 namespace {
 
-// SPMD flag page: written[kSlots], readDone[2][kSlots] (comm, compute).
-constexpr std::uint32_t kSlots = 16384;
-constexpr std::size_t kFlagBytes = 3ull * kSlots * sizeof(std::uint32_t);
+constexpr std::size_t kFlagBytes = 4ull * kSlots * sizeof(std::uint32_t);
 
 // Stream memory operations and address-range lookup from the driver, via
 // the runtime's entry-point query (the library stays loadable without a
@@ -520,6 +518,34 @@ void Session::ipcWrite(cudaStream_t s, std::uint32_t* addr, std::uint64_t value)
   if (r != CUDA_SUCCESS) throw Error("ipc: cuStreamWriteValue32 failed (" + std::to_string(static_cast<int>(r)) + ")");
 }
 
+const Session::ChunkedWrite* Session::chunkedSource(std::uint64_t matrix) const {
+  auto it = chunked_.find(matrix);
+  if (it == chunked_.end()) return nullptr;
+  auto lm = lastMut_.find(matrix);
+  return (lm != lastMut_.end() && lm->second == it->second.execId) ? &it->second : nullptr;
+}
+
+std::uint32_t Session::chunkOrdinal(const MatrixDescriptor& M, std::size_t tileIdx, std::uint64_t row,
+                                    std::uint64_t chunkBytes, std::uint64_t* lo, std::uint64_t* hi) {
+  const std::uint64_t eb = bytesOf(M.precision);
+  auto rpcOf = [&](const TileExtent& e) {
+    return std::max<std::uint64_t>(1, chunkBytes / std::max<std::uint64_t>(e.colCount * eb, 1));
+  };
+  const std::uint32_t owner = M.layout.tiles[tileIdx].second.rank;
+  std::uint32_t ord = 0;
+  for (std::size_t i = 0; i < tileIdx; ++i)
+    if (M.layout.tiles[i].second.rank == owner) {
+      const TileExtent& e = M.layout.tiles[i].first;
+      ord += static_cast<std::uint32_t>((e.rowCount + rpcOf(e) - 1) / rpcOf(e));
+    }
+  const TileExtent& e = M.layout.tiles[tileIdx].first;
+  const std::uint64_t rpc = rpcOf(e);
+  const std::uint64_t ci = (row - e.rowStart) / rpc;
+  if (lo) *lo = e.rowStart + ci * rpc;
+  if (hi) *hi = std::min(e.rowEnd(), e.rowStart + (ci + 1) * rpc);
+  return ord + static_cast<std::uint32_t>(ci);
+}
+
 std::uint32_t Session::slotOf(std::uint64_t id) const {
   auto it = slots_.find(id);
   if (it == slots_.end()) throw Error("ipc: matrix " + std::to_string(id) + " has no flag slot");
@@ -793,6 +819,7 @@ std::uint64_t Session::issue(OpDescriptor& op) {
   for (const auto& mv : moved) {
     lastMut_[mv.first] = op.execId;
     pendingWritten_.push_back({mv.first, op.execId});
+    chunked_.erase(mv.first);
   }
   if (opts_.checkMetadataEveryOp) verifyMetadataConsistency();
   return op.execId;
@@ -1226,6 +1253,23 @@ void Session::exchange(std::vector<Xfer>& xs, bool onComm, bool commit) {
   const int sIdx = onComm ? 0 : 1;
   if (!nccl_ || ipc_) {
     std::set<std::tuple<std::uint32_t, std::uint32_t, std::uint64_t>> routes;  // (src, dst, matrix)
+    std::set<std::tuple<std::uint32_t, std::uint32_t, std::uint64_t>> waited;  // whole-write waits done
+    std::set<std::pair<std::uint32_t, cudaEvent_t>> chunkWaited;               // (dst, chunk event)
+    std::set<std::tuple<std::uint32_t, std::uint32_t, std::uint32_t>> flagWaited;  // (dst, src, value)
+    // RAW for one piece: the last write of its source, or -- when that write
+    // is a chunked upload and the piece's origin is known -- only the upload
+    // chunks it overlaps (sub-pieces are then copied chunk by chunk).
+    auto wholeWait = [&](const Xfer& x, Worker& d) {
+      if (!waited.insert({x.src, x.dst, x.matrix}).second) return;
+      Worker* s = local(x.src);
+      if (s) {
+        auto it = s->lastWrite.find(x.matrix);
+        if (it != s->lastWrite.end() && (s != &d || onComm))
+          cudaCheck(cudaStreamWaitEvent(streamOf(d), it->second, 0), "exchange: wait writer");
+      } else {
+        ipcWait(streamOf(d), peerFlags_[x.src] + slotOf(x.matrix), lastMut_.at(x.matrix));
+      }
+    };
     for (const Xfer& x : xs) {
       const std::uint64_t bytes = x.rows * x.cols * x.eb;
       if (bytes == 0) continue;
@@ -1240,30 +1284,59 @@ void Session::exchange(std::vector<Xfer>& xs, bool onComm, bool commit) {
         }
         continue;
       }
-      if (!routes.insert({x.src, x.dst, x.matrix}).second) continue;
-      d->activate();
-      if (s) {
-        auto it = s->lastWrite.find(x.matrix);
-        if (it != s->lastWrite.end() && (s != d || onComm))
-          cudaCheck(cudaStreamWaitEvent(streamOf(*d), it->second, 0), "exchange: wait writer");
-      } else {
-        ipcWait(streamOf(*d), peerFlags_[x.src] + slotOf(x.matrix), lastMut_.at(x.matrix));
-      }
-    }
-    for (const Xfer& x : xs) {
-      const std::uint64_t bytes = x.rows * x.cols * x.eb;
-      Worker* d = local(x.dst);
-      if (!d || bytes == 0) continue;
+      routes.insert({x.src, x.dst, x.matrix});
       if (!x.srcPtr)
         throw Error("exchange: no mapping for a piece of matrix " + std::to_string(x.matrix) + " on worker " +
                     std::to_string(x.src));
       d->activate();
-      cudaCheck(cudaMemcpy2DAsync(x.dstPtr, x.dstLd * x.eb, x.srcPtr, x.srcLd * x.eb, x.cols * x.eb, x.rows,
-                                  cudaMemcpyDefault, streamOf(*d)),
-                "exchange: copy");
+      const ChunkedWrite* cw = x.hasOrigin ? chunkedSource(x.matrix) : nullptr;
+      const MatrixDescriptor* M = cw ? &lookup(table_, x.matrix) : nullptr;
+      std::size_t tileIdx = 0;
+      bool found = false;
+      if (cw) {
+        for (std::size_t t = 0; t < M->layout.tiles.size() && !found; ++t) {
+          const auto& tl = M->layout.tiles[t];
+          if (tl.second.rank == x.src && Rect{x.r0, x.r0 + x.rows, x.c0, x.c0 + x.cols}.inside(Rect::ofExtent(tl.first))) {
+            tileIdx = t;
+            found = true;
+          }
+        }
+      }
+      // A local producer whose upload was already joined publishes through
+      // its lastWrite event (recorded after the upload).
+      if (cw && found && s && !s->uploads.count(x.matrix)) found = false;
+      if (!cw || !found) {
+        wholeWait(x, *d);
+        cudaCheck(cudaMemcpy2DAsync(x.dstPtr, x.dstLd * x.eb, x.srcPtr, x.srcLd * x.eb, x.cols * x.eb, x.rows,
+                                    cudaMemcpyDefault, streamOf(*d)),
+                  "exchange: copy");
+      } else {
+        for (std::uint64_t r = x.r0; r < x.r0 + x.rows;) {
+          std::uint64_t lo = 0, hi = 0;
+          const std::uint32_t ord = chunkOrdinal(*M, tileIdx, r, cw->chunkBytes, &lo, &hi);
+          const std::uint64_t r1 = std::min(hi, x.r0 + x.rows);
+          if (s) {
+            const auto& chunks = s->uploads.at(x.matrix).chunks;
+            if (ord >= chunks.size()) throw Error("exchange: upload chunk geometry mismatch");
+            if (s != d || onComm)
+              if (chunkWaited.insert({x.dst, chunks[ord].done}).second)
+                cudaCheck(cudaStreamWaitEvent(streamOf(*d), chunks[ord].done, 0), "exchange: wait chunk");
+          } else {
+            const std::uint32_t v = cw->base[x.src] + ord + 1;
+            if (flagWaited.insert({x.dst, x.src, v}).second)
+              ipcWait(streamOf(*d), peerFlags_[x.src] + kUpChunkOff + slotOf(x.matrix), v);
+          }
+          const std::uint64_t off = r - x.r0;
+          cudaCheck(cudaMemcpy2DAsync(static_cast<std::uint8_t*>(x.dstPtr) + off * x.dstLd * x.eb, x.dstLd * x.eb,
+                                      static_cast<const std::uint8_t*>(x.srcPtr) + off * x.srcLd * x.eb,
+                                      x.srcLd * x.eb, x.cols * x.eb, r1 - r, cudaMemcpyDefault, streamOf(*d)),
+                    "exchange: copy chunk");
+          r = r1;
+        }
+      }
       if (x.src != x.dst) {
         d->bytesReceived += bytes;
-        if (Worker* s = local(x.src)) s->bytesSent += bytes;
+        if (s) s->bytesSent += bytes;
       }
     }
     for (const auto& rt : routes) {
@@ -1501,6 +1574,10 @@ void Session::execGemm(const OpDescriptor& op) {
   bool streamedA = false;
   forEachLocal([&](Worker& w) { streamedA = streamedA || w.uploads.count(A.matrixId); });
   if (!anyGather) S = (streamedA && !plan.transA) ? (opts_.pipelineChunks > 0 ? S : 8u) : 1u;
+  // A streaming in from the hosts in chunks (replicated knowledge, so every
+  // rank picks the same S): finer row chunks let the first GEMMs start on the
+  // first upload chunks pulled from the peers.
+  else if (chunkedSource(A.matrixId) && !plan.transA && opts_.pipelineChunks <= 0) S = 8u;
   while (S > 1 && plan.m < 512ull * S) --S;
 
   std::vector<std::vector<BandView>> aViews(P), bViews(P);
@@ -1622,6 +1699,9 @@ void Session::execGemm(const OpDescriptor& op) {
             x.cols = r.cols();
             x.eb = static_cast<std::uint32_t>(eb);
             x.matrix = M.matrixId;
+            x.hasOrigin = true;
+            x.r0 = r.r0;
+            x.c0 = r.c0;
             if (w || sw) {
               const BandView sv = srcView(M, pr.src, r);
               x.srcPtr = sv.ptr;

@@ -229,6 +229,10 @@ struct Xfer {
   std::uint64_t rows = 0, cols = 0;
   std::uint32_t eb = 0;
   std::uint64_t matrix = 0;  // source matrix id (RAW/WAR tracking)
+  // Global origin of the piece in the source matrix (set by planners that
+  // can; enables per-chunk waits on a chunked upload of the source).
+  bool hasOrigin = false;
+  std::uint64_t r0 = 0, c0 = 0;
 };
 
 // Pure GEMM planning (no device state): merged C row/col intervals per
@@ -386,6 +390,22 @@ class Session {
   std::vector<PanelCache> remoteCaches_;          // directory for non-local workers (SPMD)
   std::map<std::pair<std::uint64_t, std::uint64_t>, bool> replFailed_;
   std::uint64_t nextMatrixId_ = 1;
+  // Chunked uploads that are the last write of a matrix. The op carries the
+  // chunk size, so every rank knows each producer's chunk geometry and the
+  // value its upload-chunk flag reaches after each chunk: consumers (peer
+  // pulls, local copies) wait per chunk instead of for the whole upload.
+  struct ChunkedWrite {
+    std::uint64_t execId = 0, chunkBytes = 0;
+    std::vector<std::uint32_t> base;  // per rank: its upload-chunk counter before this upload
+  };
+  std::map<std::uint64_t, ChunkedWrite> chunked_;
+  std::map<std::pair<std::uint32_t, std::uint32_t>, std::uint32_t> upCount_;  // (rank, slot) -> chunks so far
+  const ChunkedWrite* chunkedSource(std::uint64_t matrix) const;
+  // Ordinal of the upload chunk holding global row `row` of tile `tileIdx`
+  // among its owner's chunks of matrix M (tiles in layout order), and the
+  // chunk's global row range.
+  static std::uint32_t chunkOrdinal(const MatrixDescriptor& M, std::size_t tileIdx, std::uint64_t row,
+                                    std::uint64_t chunkBytes, std::uint64_t* lo, std::uint64_t* hi);
   std::uint64_t recording_ = 0, nextPipelineId_ = 1;
   std::map<std::uint64_t, std::vector<OpDescriptor>> pipelines_;
   std::set<std::uint64_t> closedPipelines_;
