@@ -327,8 +327,9 @@ cudaError_t launch_sums_async(EwView band, uint64_t rows, uint64_t cols, int by_
   constexpr int E = sizeof(S);
   constexpr int kStageR = 32 * (kAsStep * E + 16), kStageC = kAsStep * 32 * E;
   constexpr size_t smem = static_cast<size_t>(kAsStages) * (kStageR > kStageC ? kStageR : kStageC);
-  static const cudaError_t attr = cudaFuncSetAttribute(line_sums_async_kernel<T, P>,
-                                                       cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  // Per device (the attribute lives in each device's context).
+  const cudaError_t attr = cudaFuncSetAttribute(line_sums_async_kernel<T, P>,
+                                                cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (attr != cudaSuccess) return attr;
   const uint64_t outs = by_rows ? rows : cols;
   line_sums_async_kernel<T, P><<<static_cast<unsigned>((outs + 31) / 32), kAsThreads, smem, s>>>(
@@ -419,14 +420,14 @@ cudaError_t line_sums(EwView band, uint64_t rows, uint64_t cols, int by_rows, vo
   const unsigned grid = static_cast<unsigned>((outs + kOut - 1) / kOut);
   if (double_compute) {
     const size_t smem = 2 * kOut * (kStep + 1) * sizeof(double);
-    static const cudaError_t attr =
+    const cudaError_t attr =
         cudaFuncSetAttribute(line_sums_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (attr != cudaSuccess) return attr;
     line_sums_kernel<double><<<grid, kLsThreads, smem, s>>>(band, rows, cols, by_rows, acc, acc_stride, acc_prec,
                                                             alpha);
   } else {
     const size_t smem = 2 * kOut * (kStep + 1) * sizeof(float);
-    static const cudaError_t attr =
+    const cudaError_t attr =
         cudaFuncSetAttribute(line_sums_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (attr != cudaSuccess) return attr;
     line_sums_kernel<float><<<grid, kLsThreads, smem, s>>>(band, rows, cols, by_rows, acc, acc_stride, acc_prec,

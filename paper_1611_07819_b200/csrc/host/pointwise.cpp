@@ -127,6 +127,11 @@ void Session::runPointwise(const OpDescriptor& op0, bool sync) {
   // when an operand aliases the destination.
   op.execId = nextExec_;
   validateOp(table_, op, opts_.workers);
+  // Operands still streaming in from the host are joined before anything
+  // reads them (the pulls below run ahead of issue()).
+  forEachLocal([&](Worker& w) {
+    for (int i = 0; i < 3; ++i) w.joinUpload(op.ids[i]);
+  });
   curExec_ = op.execId;
   flushWritten(curExec_);
 

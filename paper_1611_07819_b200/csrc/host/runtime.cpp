@@ -269,6 +269,8 @@ Worker::Worker(std::uint32_t r, int dev, std::uint64_t budget)
   cudaCheck(cudaStreamCreateWithPriority(&comm, cudaStreamNonBlocking, hi), "worker: comm stream");
   cudaCheck(cudaStreamCreateWithFlags(&h2d, cudaStreamNonBlocking), "worker: h2d stream");
   cudaCheck(cudaStreamCreateWithFlags(&d2h, cudaStreamNonBlocking), "worker: d2h stream");
+  for (cudaStream_t& ps : pulls)
+    cudaCheck(cudaStreamCreateWithPriority(&ps, cudaStreamNonBlocking, hi), "worker: pull stream");
   cudaCheck(cudaEventCreate(&tStart), "worker: event");
   cudaCheck(cudaEventCreate(&tEnd), "worker: event");
   cudaCheck(cudaEventCreate(&uStart), "worker: event");
@@ -284,6 +286,7 @@ Worker::~Worker() {
   cudaStreamSynchronize(comm);
   cudaStreamSynchronize(h2d);
   cudaStreamSynchronize(d2h);
+  for (cudaStream_t ps : pulls) cudaStreamSynchronize(ps);
   for (auto& kv : uploads) {
     for (auto& c : kv.second.chunks) cudaEventDestroy(c.done);
     cudaEventDestroy(kv.second.done);
@@ -310,6 +313,7 @@ Worker::~Worker() {
   cudaStreamDestroy(comm);
   cudaStreamDestroy(h2d);
   cudaStreamDestroy(d2h);
+  for (cudaStream_t ps : pulls) cudaStreamDestroy(ps);
 }
 
 void Worker::joinUpload(std::uint64_t matrix) {
@@ -1256,18 +1260,38 @@ void Session::exchange(std::vector<Xfer>& xs, bool onComm, bool commit) {
     std::set<std::tuple<std::uint32_t, std::uint32_t, std::uint64_t>> waited;  // whole-write waits done
     std::set<std::pair<std::uint32_t, cudaEvent_t>> chunkWaited;               // (dst, chunk event)
     std::set<std::tuple<std::uint32_t, std::uint32_t, std::uint32_t>> flagWaited;  // (dst, src, value)
+    // Pieces from source worker s land on pull stream s % kPullStreams of the
+    // consumer, forked from its base stream (so they see everything the base
+    // stream owes, including this worker's own earlier writes) and joined
+    // back before the op's readers are recorded.
+    std::set<std::pair<Worker*, cudaStream_t>> forked;
+    auto pullOf = [&](Worker& d, std::uint32_t src) {
+      static const std::uint32_t nPull = [] {
+        const char* e = std::getenv("GM_PULL_STREAMS");  // dev switch: 1 = one stream
+        const int v = e ? std::atoi(e) : Worker::kPullStreams;
+        return static_cast<std::uint32_t>(std::clamp(v, 1, Worker::kPullStreams));
+      }();
+      cudaStream_t ps = d.pulls[src % nPull];
+      if (forked.insert({&d, ps}).second) {
+        cudaEvent_t e = d.event();
+        cudaCheck(cudaEventRecord(e, streamOf(d)), "exchange: fork");
+        cudaCheck(cudaStreamWaitEvent(ps, e, 0), "exchange: fork");
+        d.recycle(e);
+      }
+      return ps;
+    };
     // RAW for one piece: the last write of its source, or -- when that write
     // is a chunked upload and the piece's origin is known -- only the upload
     // chunks it overlaps (sub-pieces are then copied chunk by chunk).
-    auto wholeWait = [&](const Xfer& x, Worker& d) {
+    auto wholeWait = [&](const Xfer& x, Worker& d, cudaStream_t ps) {
       if (!waited.insert({x.src, x.dst, x.matrix}).second) return;
       Worker* s = local(x.src);
       if (s) {
         auto it = s->lastWrite.find(x.matrix);
         if (it != s->lastWrite.end() && (s != &d || onComm))
-          cudaCheck(cudaStreamWaitEvent(streamOf(d), it->second, 0), "exchange: wait writer");
+          cudaCheck(cudaStreamWaitEvent(ps, it->second, 0), "exchange: wait writer");
       } else {
-        ipcWait(streamOf(d), peerFlags_[x.src] + slotOf(x.matrix), lastMut_.at(x.matrix));
+        ipcWait(ps, peerFlags_[x.src] + slotOf(x.matrix), lastMut_.at(x.matrix));
       }
     };
     for (const Xfer& x : xs) {
@@ -1305,10 +1329,11 @@ void Session::exchange(std::vector<Xfer>& xs, bool onComm, bool commit) {
       // A local producer whose upload was already joined publishes through
       // its lastWrite event (recorded after the upload).
       if (cw && found && s && !s->uploads.count(x.matrix)) found = false;
+      cudaStream_t ps = pullOf(*d, x.src);
       if (!cw || !found) {
-        wholeWait(x, *d);
+        wholeWait(x, *d, ps);
         cudaCheck(cudaMemcpy2DAsync(x.dstPtr, x.dstLd * x.eb, x.srcPtr, x.srcLd * x.eb, x.cols * x.eb, x.rows,
-                                    cudaMemcpyDefault, streamOf(*d)),
+                                    cudaMemcpyDefault, ps),
                   "exchange: copy");
       } else {
         for (std::uint64_t r = x.r0; r < x.r0 + x.rows;) {
@@ -1318,18 +1343,18 @@ void Session::exchange(std::vector<Xfer>& xs, bool onComm, bool commit) {
           if (s) {
             const auto& chunks = s->uploads.at(x.matrix).chunks;
             if (ord >= chunks.size()) throw Error("exchange: upload chunk geometry mismatch");
-            if (s != d || onComm)
-              if (chunkWaited.insert({x.dst, chunks[ord].done}).second)
-                cudaCheck(cudaStreamWaitEvent(streamOf(*d), chunks[ord].done, 0), "exchange: wait chunk");
+            // (the upload runs on the h2d stream: waited even for own tiles)
+            if (chunkWaited.insert({x.dst, chunks[ord].done}).second)
+              cudaCheck(cudaStreamWaitEvent(ps, chunks[ord].done, 0), "exchange: wait chunk");
           } else {
             const std::uint32_t v = cw->base[x.src] + ord + 1;
             if (flagWaited.insert({x.dst, x.src, v}).second)
-              ipcWait(streamOf(*d), peerFlags_[x.src] + kUpChunkOff + slotOf(x.matrix), v);
+              ipcWait(ps, peerFlags_[x.src] + kUpChunkOff + slotOf(x.matrix), v);
           }
           const std::uint64_t off = r - x.r0;
           cudaCheck(cudaMemcpy2DAsync(static_cast<std::uint8_t*>(x.dstPtr) + off * x.dstLd * x.eb, x.dstLd * x.eb,
                                       static_cast<const std::uint8_t*>(x.srcPtr) + off * x.srcLd * x.eb,
-                                      x.srcLd * x.eb, x.cols * x.eb, r1 - r, cudaMemcpyDefault, streamOf(*d)),
+                                      x.srcLd * x.eb, x.cols * x.eb, r1 - r, cudaMemcpyDefault, ps),
                     "exchange: copy chunk");
           r = r1;
         }
@@ -1338,6 +1363,14 @@ void Session::exchange(std::vector<Xfer>& xs, bool onComm, bool commit) {
         d->bytesReceived += bytes;
         if (s) s->bytesSent += bytes;
       }
+    }
+    for (const auto& fk : forked) {
+      Worker& d = *fk.first;
+      d.activate();
+      cudaEvent_t e = d.event();
+      cudaCheck(cudaEventRecord(e, fk.second), "exchange: join");
+      cudaCheck(cudaStreamWaitEvent(streamOf(d), e, 0), "exchange: join");
+      d.recycle(e);
     }
     for (const auto& rt : routes) {
       Worker& d = *local(std::get<1>(rt));

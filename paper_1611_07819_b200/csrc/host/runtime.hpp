@@ -197,6 +197,11 @@ class Worker {
   std::uint32_t rank;
   int device;
   cudaStream_t compute = nullptr, comm = nullptr, h2d = nullptr, d2h = nullptr;
+  // Copy-engine pull streams: one exchange's pieces from different source
+  // workers run on different streams (different copy engines), forked from
+  // and joined back into the comm or compute stream.
+  static constexpr int kPullStreams = 4;
+  std::array<cudaStream_t, kPullStreams> pulls{};
   DeviceArena arena;
   DescriptorTable descs;
   std::map<std::uint64_t, std::vector<DeviceTile>> tiles;
