@@ -62,12 +62,9 @@ void Session::setLocalPackedAsync(DistMatrix m, const void* host, std::uint64_t 
     if (!w) continue;
     w->activate();
     if (started.insert(w).second) {
-      // The upload starts after everything the compute stream owes the old
-      // contents (readers, the WAR waits issue() just enqueued).
-      cudaEvent_t e0 = w->event();
-      cudaCheck(cudaEventRecord(e0, w->compute), "upload: order");
-      cudaCheck(cudaStreamWaitEvent(w->h2d, e0, 0), "upload: order");
-      w->recycle(e0);
+      // WAR: issue() made the h2d stream wait for the old contents' last use
+      // on the compute stream, their readers on other streams and the peers'
+      // pulls -- not for unrelated compute, which the upload overlaps.
       w->dropChunkDone(m.id());
     }
     Worker::Upload& up = w->uploads[m.id()];

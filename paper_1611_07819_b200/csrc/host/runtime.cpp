@@ -299,6 +299,7 @@ Worker::~Worker() {
   for (auto& kv : replicas)
     if (kv.second.ready) cudaEventDestroy(kv.second.ready);
   for (auto& kv : lastWrite) cudaEventDestroy(kv.second);
+  for (auto& kv : lastTouch) cudaEventDestroy(kv.second);
   if (flags) cudaFree(flags);
   if (nccl) ncclCommDestroy(nccl);
   for (cudaEvent_t e : pool_) cudaEventDestroy(e);
@@ -365,12 +366,12 @@ void Worker::releaseReaders() {
   readers_.clear();
 }
 
-void Worker::beforeMutation(std::uint64_t matrix) {
+void Worker::beforeMutation(std::uint64_t matrix, cudaStream_t on) {
   auto it = readers_.find(matrix);
   if (it == readers_.end()) return;
   activate();
   for (auto& rd : it->second) {
-    cudaCheck(cudaStreamWaitEvent(compute, rd.first, 0), "worker: wait reader");
+    cudaCheck(cudaStreamWaitEvent(on ? on : compute, rd.first, 0), "worker: wait reader");
     rd.second->recycle(rd.first);
   }
   readers_.erase(it);
@@ -786,6 +787,19 @@ void Session::requireRecordable(OpCode c) const {
 std::uint64_t Session::issue(OpDescriptor& op) {
   requireRecordable(op.opcode);
   joinUploads(op);
+  // The previous op's device work is enqueued: mark where its uses of its
+  // matrices end on each compute stream.
+  for (std::uint64_t id : pendingTouched_)
+    for (auto& wp : workers_) {
+      if (!wp || !wp->tiles.count(id)) continue;
+      wp->activate();
+      cudaEvent_t& e = wp->lastTouch[id];
+      if (!e) cudaCheck(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "worker: touch event");
+      cudaCheck(cudaEventRecord(e, wp->compute), "worker: record touch");
+    }
+  pendingTouched_.clear();
+  for (std::uint64_t id : op.ids)
+    if (id && table_.count(id)) pendingTouched_.push_back(id);
   flushWritten(nextExec_);  // earlier ops' device work is enqueued: publish their writes
   op.execId = nextExec_++;
   curExec_ = op.execId;
@@ -804,7 +818,9 @@ std::uint64_t Session::issue(OpDescriptor& op) {
   const std::vector<std::uint8_t> wire = op.encode();
   for (auto& w : workers_)
     if (w) applyOpMetadata(OpDescriptor::decode(wire), w->descs);
-  for (const auto& mv : moved) mutationHook(mv.first, mv.second);
+  // SetData carrying a chunk size is an asynchronous upload (hostio.cpp).
+  const bool asyncUpload = op.opcode == OpCode::SetData && op.ids[1] != 0;
+  for (const auto& mv : moved) mutationHook(mv.first, mv.second, asyncUpload);
   // Flag slots follow the (replicated) op stream, so every rank agrees.
   if (op.opcode == OpCode::CreateMatrix) {
     std::uint32_t slot = kSlots;
@@ -832,7 +848,7 @@ std::uint64_t Session::issue(OpDescriptor& op) {
 // A matrix is about to change: in-flight replicas of the old version fail
 // (reference worker.cpp:207-239), cached panels of it die, and its owners'
 // compute streams wait for every reader of their tiles (WAR).
-void Session::mutationHook(std::uint64_t id, std::uint64_t oldVersion) {
+void Session::mutationHook(std::uint64_t id, std::uint64_t oldVersion, bool toH2d) {
   const std::uint64_t newVersion = table_.count(id) ? table_.at(id).version : ~0ull;
   for (auto& wp : workers_) {
     if (!wp) continue;
@@ -853,14 +869,19 @@ void Session::mutationHook(std::uint64_t id, std::uint64_t oldVersion) {
       w.arena.free(e.ptr, w.compute);
       w.recycle(e.ready);
     }
-    w.beforeMutation(id);
+    cudaStream_t ws = toH2d ? w.h2d : w.compute;
+    w.beforeMutation(id, ws);
     w.dropChunkDone(id);
+    if (toH2d) {
+      auto lt = w.lastTouch.find(id);
+      if (lt != w.lastTouch.end()) cudaCheck(cudaStreamWaitEvent(w.h2d, lt->second, 0), "upload: wait last use");
+    }
     // Peers that pulled from this worker's tiles of the matrix (SPMD
     // copy-engine plane) must be done before it changes.
     auto rr = remoteReaders_.find(id);
     if (rr != remoteReaders_.end() && w.tiles.count(id))
       for (const auto& rd : rr->second)
-        ipcWait(w.compute, peerFlags_[rd.first.first] + kSlots * (1 + rd.first.second) + slotOf(id), rd.second);
+        ipcWait(ws, peerFlags_[rd.first.first] + kSlots * (1 + rd.first.second) + slotOf(id), rd.second);
   }
   remoteReaders_.erase(id);
   for (std::uint32_t r = 0; r < opts_.workers; ++r)
@@ -949,6 +970,11 @@ void Session::execDestroy(std::uint64_t id) {
     w.joinUpload(id);
     w.dropChunkDone(id);
     w.beforeMutation(id);
+    auto lt = w.lastTouch.find(id);
+    if (lt != w.lastTouch.end()) {
+      cudaEventDestroy(lt->second);
+      w.lastTouch.erase(lt);
+    }
     auto lw = w.lastWrite.find(id);
     if (lw != w.lastWrite.end()) {
       cudaEventDestroy(lw->second);

@@ -162,13 +162,18 @@ class Worker {
   // them before that matrix is mutated or freed. `owner` is the worker whose
   // pool the event came from (recycled there).
   void addReader(std::uint64_t matrix, cudaEvent_t e, Worker* owner) { readers_[matrix].push_back({e, owner}); }
-  void beforeMutation(std::uint64_t matrix);
+  void beforeMutation(std::uint64_t matrix, cudaStream_t on = nullptr);  // default: compute
   void releaseReaders();
   // RAW: event on the compute stream after the last op that wrote this
   // worker's tiles of a matrix; readers on other streams wait on it instead
   // of on the whole compute stream (so the next op's panel pulls overlap
   // the current GEMM).
   std::map<std::uint64_t, cudaEvent_t> lastWrite;
+  // Event on the compute stream after the last op that used (read or wrote)
+  // this worker's tiles of a matrix there: an asynchronous upload into the
+  // matrix waits on it instead of on everything the compute stream holds, so
+  // it overlaps compute that does not involve the matrix.
+  std::map<std::uint64_t, cudaEvent_t> lastTouch;
   // SPMD copy-engine plane: this rank's flag page (device memory, mapped by
   // every peer): written[slot], then readDone[stream][slot].
   std::uint32_t* flags = nullptr;
@@ -373,7 +378,10 @@ class Session {
   };
   void resolveReads(std::vector<ReadNeed>& needs, std::uint64_t mutated, std::vector<Xfer>& xs,
                     std::vector<std::pair<Worker*, void*>>& temps);
-  void mutationHook(std::uint64_t id, std::uint64_t oldVersion);
+  // toH2d: the mutation is an asynchronous upload on the h2d streams -- the
+  // WAR waits land there instead of on the compute streams.
+  void mutationHook(std::uint64_t id, std::uint64_t oldVersion, bool toH2d = false);
+  std::vector<std::uint64_t> pendingTouched_;  // matrices the previous op used
   void exchange(std::vector<Xfer>& xs, bool onComm, bool commit = true);
   // --- RAW/WAR bookkeeping shared by the planes
   void flushWritten(std::uint64_t before);  // publish mutations of ops with exec id < before

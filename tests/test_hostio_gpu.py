@@ -96,3 +96,37 @@ def test_other_ops_join_pending_upload():
         back = s.getDataRaw(X)
     assert np.array_equal(got, np.maximum(x, 0))
     assert np.array_equal(back, x)
+
+
+@pytest.mark.parametrize("p,grid", [(1, (1, 1)), (4, (2, 2))])
+def test_double_buffered_stream_equals_sync(p, grid):
+    """Uploads into the other buffer set overlap the running GEMM; each
+    upload waits only for the last use of the buffer it overwrites (WAR),
+    so results must still equal the synchronous path step by step."""
+    n, steps = 1024, 5
+    want, _ = run(p, grid, steps, False, n=n)
+    with G.Session(workers=p) as s:
+        lay = G.makeGridLayout(n, n, grid[0], grid[1], G.makeWorkerGroup(p))
+        bufs = [tuple(s.createMatrix(n, n, G.Precision.BF16, lay) for _ in range(3)) for _ in range(2)]
+        hosts = []
+        A0, B0, _ = bufs[0]
+        for i in range(steps):  # the same inputs run() generates per step
+            s.fillUniform(A0, 10 + i)
+            s.fillUniform(B0, 50 + i)
+            ha, hb = packed(s, A0), packed(s, B0)
+            s.getLocalPacked(A0, ha.ctypes.data, ha.nbytes)
+            s.getLocalPacked(B0, hb.ctypes.data, hb.nbytes)
+            hosts.append((ha, hb))
+        s.synchronize()
+        outs = []
+        for i, (ha, hb) in enumerate(hosts):
+            A, B, C = bufs[i % 2]
+            hc = packed(s, C)
+            s.setLocalPackedAsync(B, hb.ctypes.data, hb.nbytes, 48 * 1024)
+            s.setLocalPackedAsync(A, ha.ctypes.data, ha.nbytes, 48 * 1024)
+            s.gemmAsync(A, B, C)
+            s.getLocalPackedAsync(C, hc.ctypes.data, hc.nbytes)
+            outs.append(hc)
+        s.synchronize()
+    for i, (g, w) in enumerate(zip(outs, want)):
+        assert np.array_equal(g, w), i
