@@ -337,6 +337,10 @@ int gm_session_transport(gm_session* s, int32_t* kind);
 int gm_last_op_device_ms(gm_session* s, float* ms, uint32_t cap, uint32_t* n);
 /* Same, restricted to the local GEMM kernels of the last gemm (no exchange). */
 int gm_last_op_kernel_ms(gm_session* s, float* ms, uint32_t cap, uint32_t* n);
+/* Per local worker: summed duration of the local GEMM kernels (compute
+ * phase) of every gemm issued between gm_timer_start and gm_timer_stop, and
+ * the number of those gemms (average kernel time = ms_sum / count). */
+int gm_timer_kernel_ms(gm_session* s, float* ms_sum, uint32_t* count, uint32_t cap, uint32_t* n);
 /* Duration of the last gemm's panel exchange on each local worker's comm
  * stream (0 when nothing moved). */
 int gm_last_op_comm_ms(gm_session* s, float* ms, uint32_t cap, uint32_t* n);

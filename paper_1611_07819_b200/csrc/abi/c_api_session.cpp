@@ -447,6 +447,17 @@ int gm_last_op_kernel_ms(gm_session* s, float* ms, uint32_t cap, uint32_t* n) {
   });
 }
 
+int gm_timer_kernel_ms(gm_session* s, float* ms_sum, uint32_t* count, uint32_t cap, uint32_t* n) {
+  return guard([&] {
+    const auto v = s->s->timerKernelMs();
+    *n = static_cast<uint32_t>(v.size());
+    for (uint32_t i = 0; i < v.size() && i < cap; ++i) {
+      ms_sum[i] = v[i].first;
+      count[i] = v[i].second;
+    }
+  });
+}
+
 int gm_last_op_comm_ms(gm_session* s, float* ms, uint32_t cap, uint32_t* n) {
   return guard([&] {
     const auto v = s->s->lastOpCommMs();

@@ -593,7 +593,7 @@ int launch(const TcOperand& a, const TcOperand& b, const TcOperand* a_lo, const 
       const char* e = std::getenv("GM_RASTER_GROUP");
       return e ? static_cast<uint32_t>(std::atoi(e)) : 0u;
     }();
-    p.group = env_group ? env_group : 32;
+    p.group = env_group ? env_group : 16;  // interleaved sweep at 32768^3: 12-16 beat 32 by 2% (DRAM 84 -> 67 GB)
     static const uint32_t ha = std::getenv("GM_HINT_A") ? std::atoi(std::getenv("GM_HINT_A")) : 0;
     static const uint32_t hb = std::getenv("GM_HINT_B") ? std::atoi(std::getenv("GM_HINT_B")) : 0;
     p.hint_a = ha;

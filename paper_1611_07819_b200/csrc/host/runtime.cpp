@@ -300,6 +300,10 @@ Worker::~Worker() {
     if (kv.second.ready) cudaEventDestroy(kv.second.ready);
   for (auto& kv : lastWrite) cudaEventDestroy(kv.second);
   for (auto& kv : lastTouch) cudaEventDestroy(kv.second);
+  for (auto& ev : kernelWindow) {
+    cudaEventDestroy(ev.first);
+    cudaEventDestroy(ev.second);
+  }
   if (flags) cudaFree(flags);
   if (nccl) ncclCommDestroy(nccl);
   for (cudaEvent_t e : pool_) cudaEventDestroy(e);
@@ -1853,6 +1857,13 @@ void Session::execGemm(const OpDescriptor& op) {
       for (std::size_t ci = 0; ci < plan.colsOf[w.rank].size(); ++ci)
         if (bLocal[w.rank][ci]) waitUploadRows(w, B.matrixId, 0, ~0ull, waited);
     cudaCheck(cudaEventRecord(w.kStart, w.compute), "gemm: timing");
+    if (w.windowOpen) {
+      std::pair<cudaEvent_t, cudaEvent_t> ev{};
+      cudaCheck(cudaEventCreate(&ev.first), "gemm: window event");
+      cudaCheck(cudaEventCreate(&ev.second), "gemm: window event");
+      cudaCheck(cudaEventRecord(ev.first, w.compute), "gemm: timing");
+      w.kernelWindow.push_back(ev);
+    }
     for (std::uint32_t j = 0; j < S; ++j) {
       waitGroup(w, 1 + j);
       std::vector<std::pair<std::uint64_t, std::uint64_t>> chunkRows;
@@ -1915,6 +1926,7 @@ void Session::execGemm(const OpDescriptor& op) {
       }
     }
     cudaCheck(cudaEventRecord(w.tEnd, w.compute), "gemm: timing");
+    if (w.windowOpen) cudaCheck(cudaEventRecord(w.kernelWindow.back().second, w.compute), "gemm: timing");
   });
   for (auto& tp : temps) {
     tp.first->activate();
@@ -2043,7 +2055,28 @@ void Session::timerStart() {
       w.recycle(e);
     }
     cudaCheck(cudaEventRecord(w.uStart, w.compute), "timer start");
+    for (auto& ev : w.kernelWindow) {
+      cudaEventDestroy(ev.first);
+      cudaEventDestroy(ev.second);
+    }
+    w.kernelWindow.clear();
+    w.windowOpen = true;
   });
+}
+
+std::vector<std::pair<float, std::uint32_t>> Session::timerKernelMs() {
+  std::vector<std::pair<float, std::uint32_t>> out;
+  forEachLocal([&](Worker& w) {
+    float sum = 0.0f;
+    for (auto& ev : w.kernelWindow) {
+      float ms = 0.0f;
+      cudaCheck(cudaEventSynchronize(ev.second), "timing sync");
+      cudaCheck(cudaEventElapsedTime(&ms, ev.first, ev.second), "timing");
+      sum += ms;
+    }
+    out.push_back({sum, static_cast<std::uint32_t>(w.kernelWindow.size())});
+  });
+  return out;
 }
 
 float Session::timerStop() {
@@ -2056,6 +2089,7 @@ float Session::timerStop() {
       w.recycle(e);
     }
     cudaCheck(cudaEventRecord(w.uEnd, w.compute), "timer stop");
+    w.windowOpen = false;
     cudaCheck(cudaEventSynchronize(w.uEnd), "timer sync");
     float ms = 0.0f;
     cudaCheck(cudaEventElapsedTime(&ms, w.uStart, w.uEnd), "timer elapsed");

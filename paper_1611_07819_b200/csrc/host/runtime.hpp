@@ -219,6 +219,10 @@ class Worker {
   cudaEvent_t cStart = nullptr, cEnd = nullptr;  // comm-stream exchange of the last gemm
   bool commTimed = false;
   bool timed = false;
+  // Compute phase of every gemm between timerStart() and timerStop()
+  // (timing-enabled event pairs, drained by timerKernelMs()).
+  bool windowOpen = false;
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> kernelWindow;
   ncclComm_t nccl = nullptr;
 
  private:
@@ -355,6 +359,9 @@ class Session {
   void getLocalPackedAsync(DistMatrix m, void* host, std::uint64_t bytes);
   void timerStart();
   float timerStop();
+  // Per local worker: {sum of gemm compute-phase ms, gemm count} over the
+  // last timerStart()/timerStop() window.
+  std::vector<std::pair<float, std::uint32_t>> timerKernelMs();
 
  private:
   std::uint64_t issue(OpDescriptor& op);  // validate + metadata + per-worker mirror

@@ -332,6 +332,15 @@ class Session:
         check(_lib.load().gm_last_op_kernel_ms(self._h, arr, 64, ctypes.byref(n)))
         return list(arr[: n.value])
 
+    def timerKernelMs(self) -> List[tuple]:
+        """[(sum of gemm compute-phase ms, gemm count)] per local worker over
+        the last timerStart()/timerStop() window."""
+        arr = (ctypes.c_float * 64)()
+        cnt = (ctypes.c_uint32 * 64)()
+        n = ctypes.c_uint32()
+        check(_lib.load().gm_timer_kernel_ms(self._h, arr, cnt, 64, ctypes.byref(n)))
+        return [(arr[i], cnt[i]) for i in range(n.value)]
+
     def lastOpCommMs(self) -> List[float]:
         arr = (ctypes.c_float * 64)()
         n = ctypes.c_uint32()

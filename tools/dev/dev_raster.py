@@ -13,7 +13,10 @@ d = L.gm_gemm_desc(m=n, n=n, k=n, lda=n + pad, ldb=n + pad, ldc=n, trans_a=0, tr
                    cta_group=0, max_ctas=0, alpha=1.0, beta=0.0)
 st = torch.cuda.current_stream().cuda_stream
 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+ts = []
 for i in range(reps):
     e0.record(); L.check(lib.gm_gemm_local(ctypes.byref(d), A.data_ptr(), B.data_ptr(), C.data_ptr(), None, 0, st)); e1.record()
     torch.cuda.synchronize()
-print(f"pad={pad} group={os.environ.get('GM_RASTER_GROUP','32')} n={n} last {e0.elapsed_time(e1):.3f} ms {2*n**3/e0.elapsed_time(e1)/1e9:.1f} TFLOP/s")
+    ts.append(e0.elapsed_time(e1))
+med = sorted(ts[reps // 3:])[len(ts[reps // 3:]) // 2]
+print(f"pad={pad} group={os.environ.get('GM_RASTER_GROUP','32')} n={n} median {med:.3f} ms {2*n**3/med/1e9:.1f} TFLOP/s (last {ts[-1]:.3f})")

@@ -21,6 +21,9 @@ from paper_1611_07819_b200 import gridmath as G  # noqa: E402
 import oracle as O  # noqa: E402
 
 rank, world, local = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"]), int(os.environ["LOCAL_RANK"])
+# More ranks than GPUs (e.g. the 2x4 grid's 8 ranks on a 4-GPU box): ranks
+# share devices round-robin; the IPC plane maps same-device peers too.
+local = local % torch.cuda.device_count()
 torch.cuda.set_device(local)
 dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 pr, pc = {1: (1, 1), 2: (1, 2), 4: (2, 2), 8: (2, 4)}[world]
