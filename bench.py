@@ -416,6 +416,7 @@ def run_ours(args):
             "roofline": {"bound": "tensor", "achieved": round(achieved, 1), "peak": peak, "unit": "TFLOP/s",
                          "frac": round(achieved / peak, 4), "traffic": traffic,
                          "peak_kind": f"{peak_kind} bf16_tflops_sustained (cuBLAS, long loop)",
+                         "peak_sm_mhz": (peaks.get("clocks_under_load") or {}).get("sm_mhz_median"),
                          "frac_of_burst_peak": round(achieved / float(peaks.get("bf16_tflops", 1657.1)), 4),
                          "frac_of_spec_2250": round(achieved / 2250.0, 4),
                          "kernel": "tc_gemm_kernel<2,2,0> (tcgen05 2-SM UMMA, bf16)",

@@ -254,3 +254,40 @@ def test_layout_invariance_bitwise_wide_tiles():
     rows = (100, 116)
     want = O.gemm_c(m, n, k, a, 3, b, 3, c, 1, 1.0, 0.0, 0, 0, rows)
     assert O.rel_fro(outs[0][rows[0]:rows[1]], want[rows[0]:rows[1]]) < 1e-5
+
+
+RAGGED_SHAPES = [(1, 1, 1), (3, 5, 7), (37, 53, 29), (1, 300, 1), (300, 1, 300), (129, 257, 65), (17, 9, 1031)]
+RAGGED_PRECS = [(3, 3, 1), (0, 0, 0), (1, 1, 1), (2, 2, 2), (3, 1, 2), (0, 0, 3)]
+
+
+@pytest.mark.parametrize("m,n,k", RAGGED_SHAPES)
+def test_ragged_shapes_vs_oracle(m, n, k):
+    # Edge shapes (single elements, odd sizes, rows/cols below 16 bytes so
+    # tiles need padded pitches, k = 1, long thin k): every precision mix
+    # and transpose, on 1 worker and on 4 workers with idle owners where a
+    # dimension is smaller than the worker count.
+    def tiles(rows, cols, kind, p):
+        if p == 1:
+            return [(0, rows, 0, cols, 0)]
+        if kind == "row" and rows >= p:
+            return O.row_block_tiles(rows, cols, p)
+        if kind == "col" and cols >= p:
+            return O.col_block_tiles(rows, cols, p)
+        if kind == "grid" and rows >= 2 and cols >= 2:
+            return O.grid_tiles(rows, cols, 2, 2)
+        return [(0, rows, 0, cols, p - 1)]  # one owner, the others idle
+
+    for (pa, pb, pc) in RAGGED_PRECS:
+        for ta, tb in [(0, 0), (1, 1), (1, 0)]:
+            seed = m * 7 + n * 11 + k * 13 + pa + 4 * pb + 16 * pc + 64 * ta + 128 * tb
+            a = O.fill_uniform(k if ta else m, m if ta else k, pa, seed)
+            b = O.fill_uniform(n if tb else k, k if tb else n, pb, seed + 1)
+            c = O.fill_uniform(m, n, pc, seed + 2)
+            want = O.gemm_c(m, n, k, a, pa, b, pb, c, pc, 0.75, 0.5, ta, tb)
+            tol = 1e-12 if 2 in (pa, pb, pc) and pc == 2 else (1e-3 if pc == 0 else TOL[pc])
+            for p in (1, 4):
+                got = run_session_gemm(p, a, pa, tiles(a.shape[0], a.shape[1], "row", p), b, pb,
+                                       tiles(b.shape[0], b.shape[1], "col", p), c, pc, tiles(m, n, "grid", p),
+                                       0.75, 0.5, ta, tb)
+                err = O.rel_fro(O.to_f64(got, pc), O.to_f64(want, pc))
+                assert err <= tol, (m, n, k, pa, pb, pc, ta, tb, p, err)

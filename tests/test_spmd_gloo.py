@@ -1,5 +1,5 @@
 # SPDX-License-Identifier: Apache-2.0
-"""N > 1 host logic on CPU: world_size-2 gloo processes each compute the
+"""N > 1 host logic on CPU: world_size-2 and -8 (the 2x4 grid) gloo processes each compute the
 GEMM plan from their own replicated metadata (the SPMD master logic) and
 check that every send a rank will post is matched, in order, by the peer's
 receive -- the property the NCCL data plane relies on."""
@@ -30,10 +30,11 @@ def _worker(rank, world, port, cases, q):
     ok = True
     for (m, n, k, kind) in cases:
         g = G.makeWorkerGroup(world)
-        if kind == "grid":
-            A = G.makeGridLayout(m, k, 1, world, g)
-            B = G.makeGridLayout(k, n, 1, world, g)
-            C = G.makeGridLayout(m, n, 1, world, g)
+        if kind == "grid":  # the bench's 2D grids: 1x2, 2x2, 2x4
+            pr, pc = {2: (1, 2), 4: (2, 2), 8: (2, 4)}[world]
+            A = G.makeGridLayout(m, k, pr, pc, g)
+            B = G.makeGridLayout(k, n, pr, pc, g)
+            C = G.makeGridLayout(m, n, pr, pc, g)
         else:
             A = G.makeRowBlockLayout(m, k, g)
             B = G.makeColBlockLayout(k, n, g)
@@ -54,8 +55,8 @@ def _worker(rank, world, port, cases, q):
 
 
 @pytest.mark.timeout(300)
-def test_spmd_plans_agree_across_ranks():
-    world = 2
+@pytest.mark.parametrize("world", [2, 8])
+def test_spmd_plans_agree_across_ranks(world):
     cases = [(256, 192, 320, "grid"), (300, 520, 260, "grid"), (128, 96, 160, "rowcol")]
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
