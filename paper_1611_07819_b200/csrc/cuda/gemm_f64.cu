@@ -329,12 +329,36 @@ __global__ void __launch_bounds__(kThreads, 2) kernel(const F64Params p) {
     }
   };
 
+  // Interior CTAs (the whole 64 x 128 tile inside C) refill full k-blocks
+  // through precomputed per-thread source pointers: thread t copies A rows
+  // t/8 + 16j (j < 4) at k chunk t%8 and, NN, B k-rows t/64 + 2j (j < 8) at
+  // n chunk t%64 -- two base pointers and two strides instead of per-copy
+  // index math and bounds checks. Edge CTAs and the last partial k-block use
+  // the general loader.
+  const bool fast = !kTA && !kTB && m0 + BM <= p.m && n0 + BN <= p.n;
+  const double* fa = p.a + static_cast<uint64_t>(m0 + threadIdx.x / 8) * p.lda + 2 * (threadIdx.x % 8);
+  const double* fb = p.b + static_cast<uint64_t>(threadIdx.x / 64) * p.ldb + n0 + 2 * (threadIdx.x % 64);
+  const uint64_t sa16 = 16 * p.lda, sb2 = 2 * p.ldb;
+  const uint32_t da = (threadIdx.x / 8) * kPK + 2 * (threadIdx.x % 8);
+  const uint32_t db = (threadIdx.x / 64) * (BN + 2) + 2 * (threadIdx.x % 64);
+  auto refill = [&](uint32_t kb, int slot) {
+    if (fast && (kb + 1) * kBK <= p.k) {
+      double* st = sm + slot * kStage;
+      const double* ga = fa + kb * kBK;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) cp_async16(st + da + j * 16 * kPK, ga + j * sa16, 16);
+      const double* gb = fb + static_cast<uint64_t>(kb * kBK) * p.ldb;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) cp_async16(st + kASize + db + j * 2 * (BN + 2), gb + j * sb2, 16);
+    } else {
+      issue(kb, slot);
+    }
+  };
+
   for (uint32_t kb = 0; kb < nk; ++kb) {
     cp_async_wait<kStages - 2>();
     __syncthreads();
     const uint32_t nxt = kb + kStages - 1;
-    if (nxt < nk) issue(nxt, nxt % kStages);
-    cp_async_commit();
     const double* ta = sm + (kb % kStages) * kStage;
     const double* tb = ta + kASize;
     double a[2][MI], b[2][NJ];
@@ -351,6 +375,12 @@ __global__ void __launch_bounds__(kThreads, 2) kernel(const F64Params p) {
       for (int i = 0; i < MI; ++i)
 #pragma unroll
         for (int j = 0; j < NJ; ++j) dmma(acc[i][j], a[cur][i], b[cur][j]);
+      if (ks == 0) {
+        // Refill the slot every thread finished reading before the barrier
+        // above, once this k-block's first DMMAs are queued.
+        if (nxt < nk) refill(nxt, nxt % kStages);
+        cp_async_commit();
+      }
     }
   }
   cp_async_wait<0>();
