@@ -22,16 +22,21 @@
 
 namespace gmk {
 
+// Rectangle iteration without a 64-bit division per element: rows go over
+// blockIdx.x (grid-stride), columns over blockIdx.y * blockDim.x + threadIdx.x
+// (stride gridDim.y * blockDim.x). rect_grid() sizes the grid.
+#define GM_FOR_RECT(rows, cols, r, c)                                                   \
+  for (uint64_t r = blockIdx.x; r < (rows); r += gridDim.x)                            \
+    for (uint64_t c = static_cast<uint64_t>(blockIdx.y) * blockDim.x + threadIdx.x; c < (cols); \
+         c += static_cast<uint64_t>(gridDim.y) * blockDim.x)
+
 // Elementwise rectangle conversion. Single->Half takes the float fast path
 // (the reference's convertBuffer does the same; the results are identical).
 __global__ void convert_rect_kernel(const void* __restrict__ src, int sp, uint64_t sld,
                                     void* __restrict__ dst, int dp, uint64_t dld, uint64_t rows,
                                     uint64_t cols) {
-  const uint64_t total = rows * cols;
   const bool via_f32 = (sp != 2 && dp != 2);
-  for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < total;
-       i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
-    const uint64_t r = i / cols, c = i % cols;
+  GM_FOR_RECT(rows, cols, r, c) {
     if (via_f32)
       store_elem_f32(dst, dp, r * dld + c, load_elem_f32(src, sp, r * sld + c));
     else
@@ -43,10 +48,7 @@ __global__ void convert_rect_kernel(const void* __restrict__ src, int sp, uint64
 __global__ void split_tf32_kernel(const void* __restrict__ src, int sp, uint64_t sld,
                                   float* __restrict__ hi, float* __restrict__ lo, uint64_t dld,
                                   uint64_t rows, uint64_t cols) {
-  const uint64_t total = rows * cols;
-  for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < total;
-       i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
-    const uint64_t r = i / cols, c = i % cols;
+  GM_FOR_RECT(rows, cols, r, c) {
     const float x = load_elem_f32(src, sp, r * sld + c);
     uint32_t h;
     asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(h) : "f"(x));
@@ -101,10 +103,7 @@ __device__ __forceinline__ uint64_t avalanche64(uint64_t z) {
 __global__ void fill_uniform_kernel(void* __restrict__ dst, int prec, uint64_t ld, uint64_t r0,
                                     uint64_t rows, uint64_t c0, uint64_t cols, uint64_t full_cols,
                                     uint64_t seed, double lo, double hi) {
-  const uint64_t total = rows * cols;
-  for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < total;
-       i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
-    const uint64_t r = i / cols, c = i % cols;
+  GM_FOR_RECT(rows, cols, r, c) {
     const uint64_t draw = (r0 + r) * full_cols + (c0 + c);
     const uint64_t x = avalanche64(seed + (draw + 1) * 0x9E3779B97F4A7C15ull);
     const double u = static_cast<double>(x >> 11) * 0x1.0p-53;
@@ -117,10 +116,7 @@ __global__ void fill_uniform_kernel(void* __restrict__ dst, int prec, uint64_t l
 // C = beta * C (alpha == 0 path; beta == 0 writes zeros without reading C).
 __global__ void scale_rect_kernel(void* __restrict__ c, int prec, uint64_t ld, uint64_t rows,
                                   uint64_t cols, double beta) {
-  const uint64_t total = rows * cols;
-  for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < total;
-       i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
-    const uint64_t r = i / cols, cc = i % cols;
+  GM_FOR_RECT(rows, cols, r, cc) {
     const uint64_t idx = r * ld + cc;
     if (beta == 0.0) {
       store_elem(c, prec, idx, 0.0);
@@ -141,18 +137,23 @@ uint64_t kernel_launches() { return g_launches.load(); }
 void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 
 namespace {
-unsigned grid_for(uint64_t total) {
-  uint64_t g = (total + 255) / 256;
-  if (g > 148ull * 16) g = 148ull * 16;
-  if (g == 0) g = 1;
-  return static_cast<unsigned>(g);
+// ~16 blocks of 256 threads per SM in total: columns get up to
+// ceil(cols / 256) blocks (at most 16), rows the rest.
+dim3 rect_grid(uint64_t rows, uint64_t cols) {
+  uint64_t gy = (cols + 255) / 256;
+  if (gy > 16) gy = 16;
+  if (gy == 0) gy = 1;
+  uint64_t gx = 148ull * 16 / gy;
+  if (gx > rows) gx = rows;
+  if (gx == 0) gx = 1;
+  return dim3(static_cast<unsigned>(gx), static_cast<unsigned>(gy), 1);
 }
 }  // namespace
 
 cudaError_t convert_rect(const void* src, int sp, uint64_t sld, void* dst, int dp, uint64_t dld,
                          uint64_t rows, uint64_t cols, cudaStream_t s) {
   if (rows == 0 || cols == 0) return cudaSuccess;
-  convert_rect_kernel<<<grid_for(rows * cols), 256, 0, s>>>(src, sp, sld, dst, dp, dld, rows, cols);
+  convert_rect_kernel<<<rect_grid(rows, cols), 256, 0, s>>>(src, sp, sld, dst, dp, dld, rows, cols);
   count_launch();
   return cudaGetLastError();
 }
@@ -160,7 +161,7 @@ cudaError_t convert_rect(const void* src, int sp, uint64_t sld, void* dst, int d
 cudaError_t split_tf32(const void* src, int sp, uint64_t sld, float* hi, float* lo, uint64_t dld,
                        uint64_t rows, uint64_t cols, cudaStream_t s) {
   if (rows == 0 || cols == 0) return cudaSuccess;
-  split_tf32_kernel<<<grid_for(rows * cols), 256, 0, s>>>(src, sp, sld, hi, lo, dld, rows, cols);
+  split_tf32_kernel<<<rect_grid(rows, cols), 256, 0, s>>>(src, sp, sld, hi, lo, dld, rows, cols);
   count_launch();
   return cudaGetLastError();
 }
@@ -178,7 +179,7 @@ cudaError_t fill_uniform(void* dst, int prec, uint64_t ld, uint64_t r0, uint64_t
                          uint64_t cols, uint64_t full_cols, uint64_t seed, double lo, double hi,
                          cudaStream_t s) {
   if (rows == 0 || cols == 0) return cudaSuccess;
-  fill_uniform_kernel<<<grid_for(rows * cols), 256, 0, s>>>(dst, prec, ld, r0, rows, c0, cols,
+  fill_uniform_kernel<<<rect_grid(rows, cols), 256, 0, s>>>(dst, prec, ld, r0, rows, c0, cols,
                                                             full_cols, seed, lo, hi);
   count_launch();
   return cudaGetLastError();
@@ -187,7 +188,7 @@ cudaError_t fill_uniform(void* dst, int prec, uint64_t ld, uint64_t r0, uint64_t
 cudaError_t scale_rect(void* c, int prec, uint64_t ld, uint64_t rows, uint64_t cols, double beta,
                        cudaStream_t s) {
   if (rows == 0 || cols == 0) return cudaSuccess;
-  scale_rect_kernel<<<grid_for(rows * cols), 256, 0, s>>>(c, prec, ld, rows, cols, beta);
+  scale_rect_kernel<<<rect_grid(rows, cols), 256, 0, s>>>(c, prec, ld, rows, cols, beta);
   count_launch();
   return cudaGetLastError();
 }

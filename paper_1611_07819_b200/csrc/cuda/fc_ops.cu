@@ -220,7 +220,10 @@ __global__ void __launch_bounds__(kLsThreads) line_sums_kernel(EwView a, uint64_
 //   by cols: stage = 128 rows x 32 elements (lane o reads column o).
 // Zero padding is exact: a chain that starts at +0 never holds -0, so adding
 // +0 leaves it unchanged.
-constexpr int kAsStep = 128, kAsStages = 4, kAsThreads = 128;
+constexpr int kAsStep = 128, kAsThreads = 128;
+// Ring depth: the folding warp eats a chunk in ~512 cycles, so keep ~5 chunks
+// in flight to cover HBM latency (4 for 8-byte elements: smem).
+constexpr int as_stages(int elem_bytes) { return elem_bytes >= 8 ? 4 : 6; }
 
 __device__ __forceinline__ void cp_async16(uint32_t saddr, const void* g, uint32_t bytes) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(saddr), "l"(g), "r"(bytes) : "memory");
@@ -238,6 +241,7 @@ __global__ void __launch_bounds__(kAsThreads) line_sums_async_kernel(const void*
                                                                       int acc_prec, T alpha) {
   using S = typename Stor<P>::type;
   constexpr int E = sizeof(S), VE = 16 / E;
+  constexpr int kAsStages = as_stages(E);
   constexpr int kPitchR = kAsStep * E + 16, kStageR = 32 * kPitchR;
   constexpr int kPitchC = 32 * E, kStageC = kAsStep * kPitchC;
   constexpr int kStage = kStageR > kStageC ? kStageR : kStageC;
@@ -326,7 +330,7 @@ cudaError_t launch_sums_async(EwView band, uint64_t rows, uint64_t cols, int by_
   using S = typename Stor<P>::type;
   constexpr int E = sizeof(S);
   constexpr int kStageR = 32 * (kAsStep * E + 16), kStageC = kAsStep * 32 * E;
-  constexpr size_t smem = static_cast<size_t>(kAsStages) * (kStageR > kStageC ? kStageR : kStageC);
+  constexpr size_t smem = static_cast<size_t>(as_stages(E)) * (kStageR > kStageC ? kStageR : kStageC);
   // Per device (the attribute lives in each device's context).
   const cudaError_t attr = cudaFuncSetAttribute(line_sums_async_kernel<T, P>,
                                                 cudaFuncAttributeMaxDynamicSharedMemorySize, smem);

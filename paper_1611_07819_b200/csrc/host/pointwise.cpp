@@ -15,6 +15,7 @@
 // the same need resolution as the GEMM (replica, own tile, cached panel,
 // else a copy-engine gather of the owners' pieces). Fast-mode addRowColSum
 // runs the deterministic chain too (one of the orders fast mode allows).
+#include <set>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -204,6 +205,21 @@ void Session::runPointwise(const OpDescriptor& op0, bool sync) {
   }
   issue(op);  // version bump, replica/cache invalidation, WAR waits on the destination
 
+  // addRowColSum: the column-sum jobs run on each worker's aux stream beside
+  // the row sums (each output is one sequential chain, so one direction alone
+  // leaves most SMs idle). Forked from and joined back into compute.
+  std::set<Worker*> forked;
+  if (sums)
+    for (const Job& j : jobs) {
+      Worker* w = local(j.owner);
+      if (!w || j.byRows || forked.count(w)) continue;
+      w->activate();
+      cudaEvent_t e = w->event();
+      cudaCheck(cudaEventRecord(e, w->compute), "addRowColSum: fork");
+      cudaCheck(cudaStreamWaitEvent(w->aux, e, 0), "addRowColSum: fork");
+      w->recycle(e);
+      forked.insert(w);
+    }
   for (const Job& j : jobs) {
     Worker* w = local(j.owner);
     if (!w) continue;
@@ -218,7 +234,7 @@ void Session::runPointwise(const OpDescriptor& op0, bool sync) {
     if (sums) {
       cudaCheck(gmk::line_sums(xv, xn.rect.rows(), xn.rect.cols(), j.byRows ? 1 : 0, tile->ptr,
                                j.byRows ? tile->ld : 1, static_cast<int>(T.precision), op.s0, dbl ? 1 : 0,
-                               w->compute),
+                               j.byRows || !forked.count(w) ? w->compute : w->aux),
                 "addRowColSum");
       continue;
     }
@@ -227,6 +243,13 @@ void Session::runPointwise(const OpDescriptor& op0, bool sync) {
     cudaCheck(gmk::ew_apply(xv, yv, bias ? 1 : 0, tile->ptr, tile->ld, static_cast<int>(T.precision),
                             j.extent.rowCount, j.extent.colCount, kind, op.s0, dbl ? 1 : 0, w->compute),
               "elementwise");
+  }
+  for (Worker* w : forked) {
+    w->activate();
+    cudaEvent_t e = w->event();
+    cudaCheck(cudaEventRecord(e, w->aux), "addRowColSum: join");
+    cudaCheck(cudaStreamWaitEvent(w->compute, e, 0), "addRowColSum: join");
+    w->recycle(e);
   }
   for (auto& tp : temps) {
     tp.first->activate();

@@ -269,6 +269,7 @@ Worker::Worker(std::uint32_t r, int dev, std::uint64_t budget)
   cudaCheck(cudaStreamCreateWithPriority(&comm, cudaStreamNonBlocking, hi), "worker: comm stream");
   cudaCheck(cudaStreamCreateWithFlags(&h2d, cudaStreamNonBlocking), "worker: h2d stream");
   cudaCheck(cudaStreamCreateWithFlags(&d2h, cudaStreamNonBlocking), "worker: d2h stream");
+  cudaCheck(cudaStreamCreateWithFlags(&aux, cudaStreamNonBlocking), "worker: aux stream");
   for (cudaStream_t& ps : pulls)
     cudaCheck(cudaStreamCreateWithPriority(&ps, cudaStreamNonBlocking, hi), "worker: pull stream");
   cudaCheck(cudaEventCreate(&tStart), "worker: event");
@@ -286,6 +287,7 @@ Worker::~Worker() {
   cudaStreamSynchronize(comm);
   cudaStreamSynchronize(h2d);
   cudaStreamSynchronize(d2h);
+  cudaStreamSynchronize(aux);
   for (cudaStream_t ps : pulls) cudaStreamSynchronize(ps);
   for (auto& kv : uploads) {
     for (auto& c : kv.second.chunks) cudaEventDestroy(c.done);
@@ -318,6 +320,7 @@ Worker::~Worker() {
   cudaStreamDestroy(comm);
   cudaStreamDestroy(h2d);
   cudaStreamDestroy(d2h);
+  cudaStreamDestroy(aux);
   for (cudaStream_t ps : pulls) cudaStreamDestroy(ps);
 }
 

@@ -202,6 +202,9 @@ class Worker {
   std::uint32_t rank;
   int device;
   cudaStream_t compute = nullptr, comm = nullptr, h2d = nullptr, d2h = nullptr;
+  // Forked from and joined back into `compute` inside one op (e.g. the
+  // column sums of addRowColSum run beside the row sums).
+  cudaStream_t aux = nullptr;
   // Copy-engine pull streams: one exchange's pieces from different source
   // workers run on different streams (different copy engines), forked from
   // and joined back into the comm or compute stream.

@@ -40,6 +40,7 @@ def main():
             "relu": (timed(s, lambda: s.opIssue(8, [Z.id, A.id], flags=(0,))), 2 * e),
             "reluGrad": (timed(s, lambda: s.opIssue(9, [Z.id, D.id, D.id], flags=(3,))), 3 * e),
             "axpy W": (timed(s, lambda: s.opIssue(9, [dW.id, W.id, W.id], -1e-3, flags=(2,))), 3 * fi * fo * 2),
+            "fillUniform (SplitMix64)": (timed(s, lambda: s.fillUniform(D, 77)), e),
         }
         for k, (us, byts) in res.items():
             print(f"{k:30s} {us:8.1f} us  {byts / (us * 1e-6) / 1e9:8.1f} GB/s")
