@@ -18,5 +18,6 @@ for i in range(reps):
     e0.record(); L.check(lib.gm_gemm_local(ctypes.byref(d), A.data_ptr(), B.data_ptr(), C.data_ptr(), None, 0, st)); e1.record()
     torch.cuda.synchronize()
     ts.append(e0.elapsed_time(e1))
+cs = int(C.view(torch.int16).to(torch.int64).sum().item())
 med = sorted(ts[reps // 3:])[len(ts[reps // 3:]) // 2]
-print(f"pad={pad} group={os.environ.get('GM_RASTER_GROUP','32')} n={n} median {med:.3f} ms {2*n**3/med/1e9:.1f} TFLOP/s (last {ts[-1]:.3f})")
+print(f"pad={pad} group={os.environ.get('GM_RASTER_GROUP','32')} n={n} median {med:.3f} ms {2*n**3/med/1e9:.1f} TFLOP/s (last {ts[-1]:.3f}) die={os.environ.get('GM_DIE_AWARE','0')} checksum={cs}")
