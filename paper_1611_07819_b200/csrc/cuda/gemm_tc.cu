@@ -35,7 +35,6 @@
 #include <mutex>
 
 #include "convert.h"
-#include "die_map.h"
 #include "gemm_tc.h"
 #include "ptx.cuh"
 
@@ -88,25 +87,7 @@ struct TcParams {
   uint32_t* sync_ctr;                   // lockstep counter (zeroed per launch) or null
   uint32_t sync_every;                  // k-blocks per lockstep checkpoint
   uint32_t tma_store;                   // C written by TMA stores (beta == 0, aligned C)
-  // Die-aware schedule (opt-in, GM_DIE_AWARE=1): each die's pairs take their
-  // own half of every raster group's M-blocks, so the A panels a die reads
-  // are read only by that die. sync_ctr[1 + die] hands out die-local unit
-  // tickets at launch.
-  uint32_t die_aware;
-  uint64_t die1_mask[3];  // bit s: SM s is on die 1
 };
-
-__device__ __forceinline__ uint32_t ld_shared_cluster_u32(const void* local, uint32_t cta) {
-  uint32_t v;
-  asm volatile(
-      "{\n\t.reg .b32 ra;\n\t"
-      "mapa.shared::cluster.u32 ra, %1, %2;\n\t"
-      "ld.shared::cluster.u32 %0, [ra];\n\t}"
-      : "=r"(v)
-      : "r"(static_cast<uint32_t>(__cvta_generic_to_shared(local))), "r"(cta)
-      : "memory");
-  return v;
-}
 
 // Lockstep: persistent CTA pairs run ~100 tiles back to back and drift apart,
 // after which pairs that share a panel no longer read it while it is in L2.
@@ -144,19 +125,6 @@ __device__ __forceinline__ void tile_coords(uint32_t t, const TcParams& p, uint3
   const uint32_t r = t % per_group;
   mb = first_m + r % gsize;
   nb = r / gsize;
-}
-
-// Die-aware variant: die d owns M-blocks [first_m + d*half, +half) of every
-// group (half = group / 2; the host enables it only when group divides the
-// M-blocks evenly), rasterised m-fastest; t counts that die's tiles.
-__device__ __forceinline__ void tile_coords_die(uint32_t t, const TcParams& p, uint32_t num_n, uint32_t die,
-                                                uint32_t& mb, uint32_t& nb) {
-  const uint32_t half = p.group / 2;
-  const uint32_t per_group = half * num_n;
-  const uint32_t g = t / per_group;
-  const uint32_t r = t % per_group;
-  mb = g * p.group + die * half + r % half;
-  nb = r / half;
 }
 
 __device__ __forceinline__ float load_c(const TcParams& p, uint64_t off) {
@@ -271,32 +239,6 @@ __global__ void __launch_bounds__(kNumThreads, 1)
     fence_barrier_init();
   }
   if (warp == 1) tmem_alloc<kCG>(tmem_slot, 512);
-  uint32_t* die_slot = tmem_slot + 1;  // [die, ticket, units on this die]
-  if (kCG == 2 && kPairs == 1 && p.die_aware && crank == 0 && warp == 0 && lane == 0) {
-    uint32_t smid;
-    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
-    const uint32_t d = static_cast<uint32_t>((p.die1_mask[smid >> 6] >> (smid & 63)) & 1);
-    die_slot[0] = d;
-    die_slot[1] = atomicAdd(p.sync_ctr + 1 + d, 1u);
-    // Every pair of the (co-resident) grid takes its ticket before any tile
-    // work starts; then the per-die unit counts are final.
-    const uint32_t total = gridDim.x / Cfg::kClusterCtas;
-    uint64_t t0;
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
-    for (;;) {
-      uint32_t a, b;
-      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(a) : "l"(p.sync_ctr + 1) : "memory");
-      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(b) : "l"(p.sync_ctr + 2) : "memory");
-      if (a + b >= total) {
-        die_slot[2] = d ? b : a;
-        break;
-      }
-      uint64_t t1;
-      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
-      if (t1 - t0 > 200000000ull) __trap();  // a pair never became resident: fail, do not hang
-      __nanosleep(100);
-    }
-  }
   if constexpr (kCG == 2) {
     cluster_sync();
   } else {
@@ -310,21 +252,7 @@ __global__ void __launch_bounds__(kNumThreads, 1)
   const uint32_t num_nbu = (p.num_n_blocks + kPairs - 1) / kPairs;
   const uint32_t num_tiles = p.num_m_blocks * num_nbu;
   const uint32_t num_kb = (p.k + kBlockK - 1) / kBlockK;
-  uint32_t unit = blockIdx.x / Cfg::kClusterCtas, num_units = gridDim.x / Cfg::kClusterCtas;
-  uint32_t die = 0;
-  uint32_t tiles_here = num_tiles;  // tiles this unit's stream draws from
-  const bool die_aware = kCG == 2 && kPairs == 1 && p.die_aware;
-  if (die_aware) {
-    die = ld_shared_cluster_u32(die_slot, 0);
-    unit = ld_shared_cluster_u32(die_slot + 1, 0);
-    num_units = ld_shared_cluster_u32(die_slot + 2, 0);
-    tiles_here = num_tiles / 2;
-  }
-  auto coords = [&](uint32_t t, uint32_t& mb, uint32_t& nbu) {
-    if (die_aware) tile_coords_die(t, p, num_nbu, die, mb, nbu);
-    else tile_coords(t, p, num_nbu, mb, nbu);
-  };
-  const uint32_t lock_units = gridDim.x / Cfg::kClusterCtas;
+  const uint32_t unit = blockIdx.x / Cfg::kClusterCtas, num_units = gridDim.x / Cfg::kClusterCtas;
 
   if (warp == 0) {
     // ------------------------------------------------------------ producer
@@ -336,14 +264,14 @@ __global__ void __launch_bounds__(kNumThreads, 1)
       const bool synced = sync;
       const uint32_t cps_per_tile = sync ? (num_kb + p.sync_every - 1) / p.sync_every : 0;
       uint32_t local_tile = 0;
-      for (uint32_t t = unit; t < tiles_here; t += num_units, ++local_tile) {
+      for (uint32_t t = unit; t < num_tiles; t += num_units, ++local_tile) {
         uint32_t mb, nbu;
-        coords(t, mb, nbu);
+        tile_coords(t, p, num_nbu, mb, nbu);
         const uint32_t nb = nbu * kPairs + pair;
         const int32_t m0 = static_cast<int32_t>(mb * kBlockMcta * kCG + rank * kBlockMcta);
         for (uint32_t kb = 0; kb < num_kb; ++kb) {
           if (sync && kb % p.sync_every == 0)
-            sync = lockstep(p.sync_ctr, local_tile * cps_per_tile + kb / p.sync_every, lock_units);
+            sync = lockstep(p.sync_ctr, local_tile * cps_per_tile + kb / p.sync_every, num_units);
           mbar_wait(&empty_bar[stage], phase ^ 1);
           uint8_t* sa = smem + stage * Cfg::kStageBytes;
           uint8_t* sb = sa + Cfg::kParts * Cfg::kBytesA;
@@ -418,7 +346,7 @@ __global__ void __launch_bounds__(kNumThreads, 1)
       const uint32_t b_lbo = p.b_mn_major ? kBlockK * kSwizzleBytes : 16;
       const uint32_t a_step = p.a_mn_major ? kMmaK * kSwizzleBytes : 32;
       const uint32_t b_step = p.b_mn_major ? kMmaK * kSwizzleBytes : 32;
-      for (uint32_t t = unit; t < tiles_here; t += num_units) {
+      for (uint32_t t = unit; t < num_tiles; t += num_units) {
         mbar_wait(&tempty_bar[acc], acc_phase ^ 1);
         tc_fence_after();
         const uint32_t tmem_acc = tmem_base + acc * kChunks * kMmaN;
@@ -473,9 +401,9 @@ __global__ void __launch_bounds__(kNumThreads, 1)
     uint8_t* stg = staging + ew * 2 * 4096;
     const uint32_t cbytes = p.c_dtype == 2 ? 4 : 2;
     uint32_t acc = 0, acc_phase = 0, iter = 0;
-    for (uint32_t t = unit; t < tiles_here; t += num_units) {
+    for (uint32_t t = unit; t < num_tiles; t += num_units) {
       uint32_t mb, nbu;
-      coords(t, mb, nbu);
+      tile_coords(t, p, num_nbu, mb, nbu);
       const uint32_t nb = nbu * kPairs + pair;
       mbar_wait(&tfull_bar[acc], acc_phase);
       tc_fence_after();
@@ -710,26 +638,12 @@ int launch(const TcOperand& a, const TcOperand& b, const TcOperand* a_lo, const 
   const int need = static_cast<int>((p.num_n_blocks + kPairs - 1) / kPairs * p.num_m_blocks) * Cfg::kClusterCtas;
   if (need < ctas) ctas = need;
   cfg.gridDim = dim3(ctas, 1, 1);
-  p.die_aware = 0;
-  {
-    static const bool env_die = std::getenv("GM_DIE_AWARE") && std::atoi(std::getenv("GM_DIE_AWARE")) != 0;
-    if (env_die && kCG == 2 && kPairs == 1 && p.group >= 2 && p.group % 2 == 0 &&
-        p.num_m_blocks % p.group == 0) {
-      const DieMap& dm = die_map(dev);
-      if (dm.valid) {
-        p.die_aware = 1;
-        for (int i = 0; i < 3; ++i) p.die1_mask[i] = dm.die1_mask[i];
-      }
-    }
-  }
-  if (p.sync_every > 0 || p.die_aware) {
+  if (p.sync_every > 0) {
     static uint32_t* ctr[64] = {nullptr};
     if (dev < 64 && !ctr[dev]) cudaMalloc(&ctr[dev], 256);
     if (dev < 64 && ctr[dev]) {
       p.sync_ctr = ctr[dev];
-      cudaMemsetAsync(p.sync_ctr, 0, 12, stream);
-    } else {
-      p.die_aware = 0;
+      cudaMemsetAsync(p.sync_ctr, 0, 4, stream);
     }
   }
   static const bool debug = std::getenv("GM_DEBUG") != nullptr;
