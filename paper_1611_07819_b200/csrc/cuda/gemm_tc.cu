@@ -702,7 +702,23 @@ int tc_gemm(const TcGemmArgs& g, cudaStream_t stream, const char** err) {
   if (g.kind == TcKind::F16 || g.kind == TcKind::BF16) {
     const uint32_t fmt = g.kind == TcKind::BF16 ? 1 : 0;
     p.idesc = make_idesc(fmt, fmt, p.a_mn_major, p.b_mn_major, mrows, kMmaN);
-    const bool wide = env_chunks ? env_chunks == 2 : (g.k >= 4096 && g.n > kMmaN);
+    // Wide tiles only when they fill the persistent grid's waves as well as
+    // 256-wide tiles do (a 1024 x 4096 output is 32 wide tiles for 74 pairs:
+    // 43% of the SMs; 64 narrow tiles fill 86%). Same bits either way.
+    bool wide = env_chunks ? env_chunks == 2 : (g.k >= 4096 && g.n > kMmaN);
+    if (wide && !env_chunks) {
+      int dev = 0;
+      cudaGetDevice(&dev);
+      const uint64_t units = static_cast<uint64_t>(sm_count(dev)) / cg;
+      auto fill = [&](uint64_t tiles) {
+        const uint64_t waves = (tiles + units - 1) / units;
+        return static_cast<double>(tiles) / static_cast<double>(waves * units);
+      };
+      const uint64_t mb = (g.m + mrows - 1) / mrows;
+      const double f_wide = fill(mb * ((g.n + 2 * kMmaN - 1) / (2 * kMmaN)));
+      const double f_narrow = fill(mb * ((g.n + kMmaN - 1) / kMmaN));
+      if (f_narrow > f_wide + 0.05) wide = false;
+    }
     static const int env_pairs = [] {
       const char* e = std::getenv("GM_TC_PAIRS");
       return e ? std::atoi(e) : 0;
