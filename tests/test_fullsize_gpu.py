@@ -12,7 +12,9 @@ size-independent properties plus sampled rows:
   * C5 fp64 16384^3 on a 2x4 grid (DMMA): sampled rows within 1e-12 of the
     fp64 restatement; the mixed-precision mode (Half A/B, Single C: Single
     compute with fp32 accumulation) within 1e-2 of the reference's Half/Half/
-    Single result on the same rows, and of the fp64 result.
+    Single result on the same rows, and of the fp64 result;
+  * C4 FC step (batch 4096, 9216 -> 4096, bf16, 4 workers): GEMMs on sampled
+    rows within 1e-2, every neighbour op bit-for-bit on the device's inputs.
 """
 import numpy as np
 import pytest
@@ -82,3 +84,87 @@ def test_c5_fp64_16384_grid_2x4_and_mixed_mode():
     got_h = ch[rows[0]:rows[1]]
     assert O.rel_fro(got_h, want_h) <= 1e-2
     assert O.rel_fro(got_h, c64[rows[0]:rows[1]]) <= 1e-2
+
+
+def _same_bits(got, want):
+    return np.array_equal(np.ascontiguousarray(got).view(np.uint8), np.ascontiguousarray(want).view(np.uint8))
+
+
+def test_c4_fc_step_full_size_bf16():
+    """C4 at its full size: one hidden FC layer of the reference Trainer
+    (batch 4096, 9216 -> 4096, bf16 storage, 4 workers: X row-block, W col-block
+    and replicated, dW col-block). Each op is checked on the device's own
+    inputs: the three GEMMs on sampled rows against the C restatement
+    (bf16 C with fp32 accumulation: <= 1e-2), every neighbour op (biasAdd,
+    relu, reluGrad, addRowColSum, axpy) bit-for-bit on the whole matrix."""
+    batch, fin, fout, p, lr = 4096, 9216, 4096, 4, 1e-3
+    BF = 3
+    grp = list(range(p))
+    x = O.fill_uniform(batch, fin, BF, 51)
+    w = O.fill_uniform(fin, fout, BF, 52, -1 / 96.0, 1 / 96.0)
+    b = O.fill_uniform(1, fout, BF, 53, -0.1, 0.1)
+    dact = O.fill_uniform(batch, fout, BF, 54)
+    rows = [(0, 8), (2040, 2056), (4088, 4096)]
+    with G.Session(workers=p) as s:
+        def mk(r, c, lay, img=None):
+            m = s.createMatrix(r, c, G.Precision.BF16, lay(r, c, grp))
+            if img is not None:
+                s.setDataRaw(m, img)
+            return m
+        X = mk(batch, fin, G.makeRowBlockLayout, x)
+        W = mk(fin, fout, G.makeColBlockLayout, w)
+        Bv = mk(1, fout, G.makeColBlockLayout, b)
+        Z = mk(batch, fout, G.makeRowBlockLayout)
+        ACT = mk(batch, fout, G.makeRowBlockLayout)
+        DEL = mk(batch, fout, G.makeRowBlockLayout, dact)
+        DW = mk(fin, fout, G.makeColBlockLayout)
+        DB = mk(1, fout, G.makeColBlockLayout)
+        ROW = mk(batch, 1, G.makeRowBlockLayout)
+        DX = mk(batch, fin, G.makeRowBlockLayout)
+        s.replicateSync(W)
+        s.replicateSync(Bv)
+
+        G.gemm(s, X, W, Z, 1.0, 0.0)  # forward reads the W replica
+        z0 = s.getDataRaw(Z)
+        for r0, r1 in rows:
+            want = O.gemm_c(r1 - r0, fout, fin, np.ascontiguousarray(x[r0:r1]), BF, w, BF,
+                            np.zeros((r1 - r0, fout), np.uint16), BF, 1.0, 0.0, 0, 0)
+            assert O.rel_fro(O.to_f64(z0[r0:r1], BF), O.to_f64(want, BF)) <= 1e-2
+        G.biasAdd(s, Z, Bv)
+        z = s.getDataRaw(Z)
+        assert _same_bits(z, O.ew_c(False, 5, 0.0, z0, BF, b, BF, z0, BF))
+        G.relu(s, Z, ACT)
+        assert _same_bits(s.getDataRaw(ACT), O.ew_c(True, 0, 0.0, z, BF, None, 1, z, BF))
+        G.reluGrad(s, Z, DEL)
+        dl = s.getDataRaw(DEL)
+        assert _same_bits(dl, O.ew_c(False, 3, 0.0, z, BF, dact, BF, dact, BF))
+
+        G.gemm(s, X, DEL, DW, 1.0, 0.0, True, False)  # dW = x^T . delta
+        dw = s.getDataRaw(DW)
+        for r0, r1 in [(0, 8), (4600, 4608), (9208, 9216)]:
+            xt = np.ascontiguousarray(x.T[r0:r1])
+            want = O.gemm_c(r1 - r0, fout, batch, xt, BF, dl, BF, np.zeros((r1 - r0, fout), np.uint16), BF,
+                            1.0, 0.0, 0, 0)
+            assert O.rel_fro(O.to_f64(dw[r0:r1], BF), O.to_f64(want, BF)) <= 1e-2
+        G.setConst(s, ROW, 0.0)
+        G.setConst(s, DB, 0.0)
+        G.addRowColSum(s, DEL, ROW, DB, 1.0, True)
+        want_r, want_c = O.rowcolsum_c(1.0, dl, BF, np.zeros((batch, 1), np.uint16), BF,
+                                       np.zeros((1, fout), np.uint16), BF)
+        db = s.getDataRaw(DB)
+        assert _same_bits(db, want_c)
+        assert _same_bits(s.getDataRaw(ROW), want_r)
+
+        G.gemm(s, DEL, W, DX, 1.0, 0.0, False, True)  # dX = delta . W^T (replica)
+        dx = s.getDataRaw(DX)
+        wt = np.ascontiguousarray(w.T)
+        for r0, r1 in rows:
+            want = O.gemm_c(r1 - r0, fin, fout, np.ascontiguousarray(dl[r0:r1]), BF, wt, BF,
+                            np.zeros((r1 - r0, fin), np.uint16), BF, 1.0, 0.0, 0, 0)
+            assert O.rel_fro(O.to_f64(dx[r0:r1], BF), O.to_f64(want, BF)) <= 1e-2
+
+        G.axpy(s, -lr, DW, W)
+        G.axpy(s, -lr, DB, Bv)
+        assert _same_bits(s.getDataRaw(W), O.ew_c(False, 2, -lr, dw, BF, w, BF, w, BF))
+        assert _same_bits(s.getDataRaw(Bv), O.ew_c(False, 2, -lr, db, BF, b, BF, b, BF))
+        s.verifyMetadataConsistency()
