@@ -87,6 +87,7 @@ struct TcParams {
   uint32_t* sync_ctr;                   // lockstep counter (zeroed per launch) or null
   uint32_t sync_every;                  // k-blocks per lockstep checkpoint
   uint32_t tma_store;                   // C written by TMA stores (beta == 0, aligned C)
+  uint32_t fold_kb;                     // k-blocks per folded k-chunk (Single compute), 0 = off
 };
 
 // Lockstep: persistent CTA pairs run ~100 tiles back to back and drift apart,
@@ -134,12 +135,12 @@ __device__ __forceinline__ float load_c(const TcParams& p, uint64_t off) {
 }
 
 __device__ __forceinline__ void store_row32(const TcParams& p, uint32_t row, uint32_t col0,
-                                            const uint32_t (&v)[32]) {
+                                            const uint32_t (&v)[32], float alpha) {
   if (row >= p.m || col0 >= p.n) return;
   const uint64_t base = static_cast<uint64_t>(row) * p.ldc + col0;
   float f[32];
 #pragma unroll
-  for (int i = 0; i < 32; ++i) f[i] = p.alpha * __uint_as_float(v[i]);
+  for (int i = 0; i < 32; ++i) f[i] = alpha * __uint_as_float(v[i]);
   const bool full = col0 + 32 <= p.n;
   if (p.beta != 0.0f) {
     if (full) {
@@ -252,6 +253,9 @@ __global__ void __launch_bounds__(kNumThreads, 1)
   const uint32_t num_nbu = (p.num_n_blocks + kPairs - 1) / kPairs;
   const uint32_t num_tiles = p.num_m_blocks * num_nbu;
   const uint32_t num_kb = (p.k + kBlockK - 1) / kBlockK;
+  // Fold mode (tf32 kinds, 256-wide tiles): one chunk accumulator plus a
+  // running-sum region in TMEM instead of two tile accumulators.
+  const bool fold = kChunks == 1 && kElemBytes == 4 && p.fold_kb > 0;
   const uint32_t unit = blockIdx.x / Cfg::kClusterCtas, num_units = gridDim.x / Cfg::kClusterCtas;
 
   if (warp == 0) {
@@ -346,18 +350,26 @@ __global__ void __launch_bounds__(kNumThreads, 1)
       const uint32_t b_lbo = p.b_mn_major ? kBlockK * kSwizzleBytes : 16;
       const uint32_t a_step = p.a_mn_major ? kMmaK * kSwizzleBytes : 32;
       const uint32_t b_step = p.b_mn_major ? kMmaK * kSwizzleBytes : 32;
+      uint32_t fq = 0;  // fold mode: k-chunks issued so far
       for (uint32_t t = unit; t < num_tiles; t += num_units) {
-        mbar_wait(&tempty_bar[acc], acc_phase ^ 1);
-        tc_fence_after();
-        const uint32_t tmem_acc = tmem_base + acc * kChunks * kMmaN;
+        if (!fold) {
+          mbar_wait(&tempty_bar[acc], acc_phase ^ 1);
+          tc_fence_after();
+        }
+        const uint32_t tmem_acc = fold ? tmem_base : tmem_base + acc * kChunks * kMmaN;
         for (uint32_t kb = 0; kb < num_kb; ++kb) {
+          const uint32_t kq = fold ? kb % p.fold_kb : kb;  // k-block within the accumulation
+          if (fold && kq == 0) {
+            mbar_wait(&tempty_bar[0], (fq & 1) ^ 1);  // chunk buffer folded by the epilogue
+            tc_fence_after();
+          }
           mbar_wait(&full_bar[stage], phase);
           tc_fence_after();
           const uint32_t sa = smem_u32(smem + stage * Cfg::kStageBytes);
           const uint32_t sb = sa + Cfg::kParts * Cfg::kBytesA;
 #pragma unroll
           for (uint32_t kk = 0; kk < kBlockK / kMmaK; ++kk) {
-            const uint32_t first = (kb | kk) == 0 ? 0u : 1u;
+            const uint32_t first = (kq | kk) == 0 ? 0u : 1u;
             const uint64_t ah = sdesc_sw128(sa + kk * a_step, a_lbo, 1024);
 #pragma unroll
             for (uint32_t c = 0; c < kChunks; ++c) {
@@ -379,16 +391,17 @@ __global__ void __launch_bounds__(kNumThreads, 1)
           }
           if constexpr (kCG == 2) mma_commit_2sm(&empty_bar[stage], all_mask);
           else mma_commit(&empty_bar[stage]);
-          if (kb + 1 == num_kb) {
-            if constexpr (kCG == 2) mma_commit_2sm(&tfull_bar[acc], pair_mask);
-            else mma_commit(&tfull_bar[acc]);
+          if (fold ? (kq + 1 == p.fold_kb || kb + 1 == num_kb) : kb + 1 == num_kb) {
+            if constexpr (kCG == 2) mma_commit_2sm(&tfull_bar[fold ? 0 : acc], pair_mask);
+            else mma_commit(&tfull_bar[fold ? 0 : acc]);
+            if (fold) ++fq;
           }
           if (++stage == kStages) {
             stage = 0;
             phase ^= 1;
           }
         }
-        if (++acc == kAcc) {
+        if (!fold && ++acc == kAcc) {
           acc = 0;
           acc_phase ^= 1;
         }
@@ -401,90 +414,120 @@ __global__ void __launch_bounds__(kNumThreads, 1)
     uint8_t* stg = staging + ew * 2 * 4096;
     const uint32_t cbytes = p.c_dtype == 2 ? 4 : 2;
     uint32_t acc = 0, acc_phase = 0, iter = 0;
+    uint32_t fq = 0;  // fold mode: k-chunks consumed so far
+    // Writes 32 columns (c .. c+31 of the tile) of this thread's row:
+    // out = alpha_eff * v (+ beta * C), through swizzled smem + TMA store, or
+    // direct stores. The smem buffer is reused two slices later, after its
+    // TMA store has finished reading it.
+    auto emit = [&](uint32_t nb, uint32_t row0, uint32_t row, uint32_t c, const uint32_t (&v)[32],
+                    float alpha_eff) {
+      if (!p.tma_store) {
+        store_row32(p, row, nb * Cfg::kBlockN + c, v, alpha_eff);
+        return;
+      }
+      uint8_t* buf = stg + (iter & 1) * 4096;
+      if (lane == 0 && iter >= 2) bulk_wait_read<1>();
+      ++iter;
+      __syncwarp();
+      if (cbytes == 2) {
+        // 32 x 64 B rows, 64-byte swizzle: chunk j of row r at (j ^ ((r >> 1) & 3)).
+        uint32_t packed[16];
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+          const float x0 = alpha_eff * __uint_as_float(v[2 * i]), x1 = alpha_eff * __uint_as_float(v[2 * i + 1]);
+          if (p.c_dtype == 1) {
+            __nv_bfloat162 h = __floats2bfloat162_rn(x0, x1);
+            packed[i] = *reinterpret_cast<uint32_t*>(&h);
+          } else {
+            __half2 h = __floats2half2_rn(x0, x1);
+            packed[i] = *reinterpret_cast<uint32_t*>(&h);
+          }
+        }
+#pragma unroll
+        for (uint32_t j = 0; j < 4; ++j) {
+          const uint32_t pj = j ^ ((lane >> 1) & 3);
+          *reinterpret_cast<uint4*>(buf + lane * 64 + pj * 16) =
+              make_uint4(packed[4 * j], packed[4 * j + 1], packed[4 * j + 2], packed[4 * j + 3]);
+        }
+      } else {
+        // 32 x 128 B rows, 128-byte swizzle: chunk j of row r at (j ^ (r & 7)).
+#pragma unroll
+        for (uint32_t j = 0; j < 8; ++j) {
+          const uint32_t pj = j ^ (lane & 7);
+          *reinterpret_cast<float4*>(buf + lane * 128 + pj * 16) =
+              make_float4(alpha_eff * __uint_as_float(v[4 * j]), alpha_eff * __uint_as_float(v[4 * j + 1]),
+                          alpha_eff * __uint_as_float(v[4 * j + 2]), alpha_eff * __uint_as_float(v[4 * j + 3]));
+        }
+      }
+      fence_proxy_async_smem();
+      __syncwarp();
+      if (lane == 0) {
+        tma_store_2d(&tm_c, buf, static_cast<int32_t>(nb * Cfg::kBlockN + c), static_cast<int32_t>(row0));
+        bulk_commit();
+      }
+    };
+    auto release = [&](uint32_t a) {
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) {
+        if (kCG == 2 && !leader) mbar_arrive_cluster(&tempty_bar[a], pair * kCG);
+        else mbar_arrive(&tempty_bar[a]);
+      }
+    };
     for (uint32_t t = unit; t < num_tiles; t += num_units) {
       uint32_t mb, nbu;
       tile_coords(t, p, num_nbu, mb, nbu);
       const uint32_t nb = nbu * kPairs + pair;
-      mbar_wait(&tfull_bar[acc], acc_phase);
-      tc_fence_after();
       const uint32_t row0 = mb * kBlockMcta * kCG + rank * kBlockMcta + lane_grp * 32;
       const uint32_t row = row0 + lane;
-      const uint32_t taddr = tmem_base + ((lane_grp * 32) << 16) + acc * kChunks * kMmaN;
-      if (p.tma_store) {
-        // TMEM -> registers -> swizzled smem (32 x 32 chunk) -> TMA store.
-        // The chunk buffer is reused two chunks later, after its store has
-        // finished reading shared memory.
+      if (fold) {
+        // k-chunk folding (Single compute): TMEM columns [0, 256) take chunk
+        // q's products, [256, 512) hold the running fp32 sum of this thread's
+        // row: s = alpha*P_0, then s = fma(alpha, P_q, s) -- one rounding per
+        // fixed 256-wide k-chunk instead of the tensor cores' truncating
+        // accumulation over all of k. The last chunk writes C.
+        const uint32_t lanes = (lane_grp * 32) << 16;
+        const uint32_t tchunk = tmem_base + lanes, tsum = tmem_base + lanes + kMmaN;
+        const uint32_t nq = (num_kb + p.fold_kb - 1) / p.fold_kb;
+        for (uint32_t q = 0; q < nq; ++q, ++fq) {
+          mbar_wait(&tfull_bar[0], fq & 1);
+          tc_fence_after();
+          const bool last = q + 1 == nq;
 #pragma unroll 1
-        for (uint32_t c = 0; c < Cfg::kBlockN; c += 32, ++iter) {
-          uint32_t v[32];
-          __syncwarp();
-          tmem_ld_32x32b_x32(taddr + c, v);
-          tmem_wait_ld();
-          if (c + 32 == Cfg::kBlockN) {
-            // Accumulator fully read: release TMEM before the last stores.
-            tc_fence_before();
+          for (uint32_t c = 0; c < Cfg::kBlockN; c += 32) {
+            uint32_t v[32], sum[32];
             __syncwarp();
-            if (lane == 0) {
-              if (kCG == 2 && !leader) mbar_arrive_cluster(&tempty_bar[acc], pair * kCG);
-              else mbar_arrive(&tempty_bar[acc]);
-            }
-          }
-          uint8_t* buf = stg + (iter & 1) * 4096;
-          if (lane == 0 && iter >= 2) bulk_wait_read<1>();
-          __syncwarp();
-          if (cbytes == 2) {
-            // 32 x 64 B rows, 64-byte swizzle: chunk j of row r at (j ^ ((r >> 1) & 3)).
-            uint32_t packed[16];
+            tmem_ld_32x32b_x32(tchunk + c, v);
+            if (q > 0) tmem_ld_32x32b_x32(tsum + c, sum);
+            tmem_wait_ld();
+            if (c + 32 == Cfg::kBlockN) release(0);  // chunk buffer fully read
 #pragma unroll
-            for (int i = 0; i < 16; ++i) {
-              const float x0 = p.alpha * __uint_as_float(v[2 * i]), x1 = p.alpha * __uint_as_float(v[2 * i + 1]);
-              if (p.c_dtype == 1) {
-                __nv_bfloat162 h = __floats2bfloat162_rn(x0, x1);
-                packed[i] = *reinterpret_cast<uint32_t*>(&h);
-              } else {
-                __half2 h = __floats2half2_rn(x0, x1);
-                packed[i] = *reinterpret_cast<uint32_t*>(&h);
-              }
+            for (int i = 0; i < 32; ++i) {
+              const float x = __uint_as_float(v[i]);
+              sum[i] = __float_as_uint(q > 0 ? __fmaf_rn(p.alpha, x, __uint_as_float(sum[i])) : __fmul_rn(p.alpha, x));
             }
-#pragma unroll
-            for (uint32_t j = 0; j < 4; ++j) {
-              const uint32_t pj = j ^ ((lane >> 1) & 3);
-              *reinterpret_cast<uint4*>(buf + lane * 64 + pj * 16) =
-                  make_uint4(packed[4 * j], packed[4 * j + 1], packed[4 * j + 2], packed[4 * j + 3]);
-            }
-          } else {
-            // 32 x 128 B rows, 128-byte swizzle: chunk j of row r at (j ^ (r & 7)).
-#pragma unroll
-            for (uint32_t j = 0; j < 8; ++j) {
-              const uint32_t pj = j ^ (lane & 7);
-              *reinterpret_cast<float4*>(buf + lane * 128 + pj * 16) =
-                  make_float4(p.alpha * __uint_as_float(v[4 * j]), p.alpha * __uint_as_float(v[4 * j + 1]),
-                              p.alpha * __uint_as_float(v[4 * j + 2]), p.alpha * __uint_as_float(v[4 * j + 3]));
-            }
+            if (!last) tmem_st_32x32b_x32(tsum + c, sum);
+            else emit(nb, row0, row, c, sum, 1.0f);
           }
-          fence_proxy_async_smem();
-          __syncwarp();
-          if (lane == 0) {
-            tma_store_2d(&tm_c, buf, static_cast<int32_t>(nb * Cfg::kBlockN + c), static_cast<int32_t>(row0));
-            bulk_commit();
-          }
+          if (!last) tmem_wait_st();
         }
-      } else {
-#pragma unroll 1
-        for (uint32_t c = 0; c < Cfg::kBlockN; c += 32) {
-          uint32_t v[32];
-          __syncwarp();
-          tmem_ld_32x32b_x32(taddr + c, v);
-          tmem_wait_ld();
-          store_row32(p, row, nb * Cfg::kBlockN + c, v);
-        }
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) {
-          if (kCG == 2 && !leader) mbar_arrive_cluster(&tempty_bar[acc], pair * kCG);
-          else mbar_arrive(&tempty_bar[acc]);
-        }
+        continue;
       }
+      mbar_wait(&tfull_bar[acc], acc_phase);
+      tc_fence_after();
+      const uint32_t taddr = tmem_base + ((lane_grp * 32) << 16) + acc * kChunks * kMmaN;
+#pragma unroll 1
+      for (uint32_t c = 0; c < Cfg::kBlockN; c += 32) {
+        uint32_t v[32];
+        __syncwarp();
+        tmem_ld_32x32b_x32(taddr + c, v);
+        tmem_wait_ld();
+        // TMA-store path: the accumulator is released before the last
+        // slice's stores; the direct path after all of them.
+        if (p.tma_store && c + 32 == Cfg::kBlockN) release(acc);
+        emit(nb, row0, row, c, v, p.alpha);
+      }
+      if (!p.tma_store) release(acc);
       if (++acc == kAcc) {
         acc = 0;
         acc_phase ^= 1;
@@ -735,6 +778,13 @@ int tc_gemm(const TcGemmArgs& g, cudaStream_t stream, const char** err) {
                 : launch<2, 2, 0, 1>(g.a, g.b, nullptr, nullptr, p, g.max_ctas, stream, err);
   }
   p.idesc = make_idesc(2, 2, p.a_mn_major, p.b_mn_major, mrows, kMmaN);
+  if (g.fold_k) {
+    if (g.fold_k % 32) {
+      *err = "tc_gemm: fold_k must be a multiple of 32";
+      return 1;
+    }
+    p.fold_kb = static_cast<uint32_t>(g.fold_k / 32);  // 32 tf32 elements per k-block
+  }
   if (g.kind == TcKind::TF32)
     return cg == 1 ? launch<1, 4, 0, 1>(g.a, g.b, nullptr, nullptr, p, g.max_ctas, stream, err)
                    : launch<2, 4, 0, 1>(g.a, g.b, nullptr, nullptr, p, g.max_ctas, stream, err);

@@ -24,6 +24,9 @@ struct TcGemmArgs {
   double alpha = 1.0, beta = 0.0;
   int cta_group = 2;     // 1 or 2 (2-SM UMMA)
   int max_ctas = 0;      // 0 = all SMs (persistent grid); else cap (leaves SMs for comm)
+  // TF32 kinds: fold the tensor-core accumulation into an fp32 running sum
+  // every fold_k of k (a multiple of 32; 0 = accumulate all of k in TMEM).
+  uint64_t fold_k = 0;
 };
 
 // Launches on `stream`; returns 0 or 1 with *err set (static string).

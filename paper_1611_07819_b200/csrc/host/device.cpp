@@ -183,20 +183,17 @@ Plan makePlan(const gm_gemm_desc& d, const void* a, const void* b) {
   // Staged shapes: A as m x k, B as n x k.
   const std::uint64_t aBytes = roundUp(d.m * stagedLd(d.k, 4) * 4, kAlign);
   const std::uint64_t bBytes = roundUp(d.n * stagedLd(d.k, 4) * 4, kAlign);
-  // fp32 accumulator for k-chunked accumulation when C is not Single (or misaligned).
-  const std::uint64_t accBytes = roundUp(d.m * stagedLd(d.n, 4) * 4, kAlign);
   if (d.math == GM_MATH_TF32) {
     pl.path = Plan::TF32;
     pl.stageA = d.prec_a != GM_SINGLE || d.trans_a || !tmaOk(a, d.lda, 4);
     pl.stageB = d.prec_b != GM_SINGLE || !d.trans_b || !tmaOk(b, d.ldb, 4);
     if (pl.stageA) pl.bytes += aBytes;
     if (pl.stageB) pl.bytes += bBytes;
-    pl.bytes += accBytes;
     return pl;
   }
   pl.path = Plan::TF32X3;  // hi + lo for both operands, always staged
   pl.stageA = pl.stageB = true;
-  pl.bytes = 2 * aBytes + 2 * bBytes + accBytes;
+  pl.bytes = 2 * aBytes + 2 * bBytes;
   (void)sa;
   (void)sb;
   return pl;
@@ -342,41 +339,13 @@ void gemmLocal(const gm_gemm_desc& d, const void* a, const void* b, void* c, voi
   }
   if (g.kind == gmk::TcKind::TF32X3 || g.kind == gmk::TcKind::TF32) {
     // The tensor cores' fp32 accumulation truncates, so its error grows
-    // linearly with k. Accumulate fixed global k-chunks of kTf32Chunk in
-    // TMEM and fold each chunk into an fp32 C with a round-to-nearest FMA
-    // in the epilogue (C = alpha*P_c + 1*C). Chunk boundaries are fixed
-    // multiples, so the result stays layout/P independent.
+    // linearly with k. The kernel accumulates fixed global k-chunks of
+    // kTf32Chunk in TMEM and folds each into an fp32 running sum with a
+    // round-to-nearest FMA (TMEM-resident, inside the one launch); chunk
+    // boundaries are fixed multiples, so the result stays layout/P
+    // independent.
     const std::uint64_t L = tf32Chunk();
-    if (d.k > L) {
-      float* acc = static_cast<float*>(c);
-      std::uint64_t ldacc = d.ldc;
-      const bool inPlace = d.prec_c == GM_SINGLE && tmaOk(c, d.ldc, 4);
-      if (!inPlace) {
-        acc = reinterpret_cast<float*>(ws);
-        ldacc = stagedLd(d.n, 4);
-        if (d.beta != 0.0)
-          cudaCheck(gmk::convert_rect(c, d.prec_c, d.ldc, acc, GM_SINGLE, ldacc, d.m, d.n, stream), "gemm: C to fp32");
-      }
-      for (std::uint64_t k0 = 0; k0 < d.k; k0 += L) {
-        gmk::TcGemmArgs gc = g;
-        gc.k = std::min(L, d.k - k0);
-        gc.a.ptr = static_cast<const float*>(g.a.ptr) + k0;
-        gc.b.ptr = static_cast<const float*>(g.b.ptr) + k0;
-        if (g.kind == gmk::TcKind::TF32X3) {
-          gc.a_lo.ptr = static_cast<const float*>(g.a_lo.ptr) + k0;
-          gc.b_lo.ptr = static_cast<const float*>(g.b_lo.ptr) + k0;
-        }
-        gc.c = acc;
-        gc.ldc = ldacc;
-        gc.c_dtype = 2;
-        gc.beta = k0 == 0 ? d.beta : 1.0;
-        if (k0 == 0 && !inPlace && d.beta == 0.0) gc.beta = 0.0;
-        if (gmk::tc_gemm(gc, stream, &err)) throw Error(std::string("gemm(tcgen05): ") + err);
-      }
-      if (!inPlace)
-        cudaCheck(gmk::convert_rect(acc, GM_SINGLE, ldacc, c, d.prec_c, d.ldc, d.m, d.n, stream), "gemm: fp32 to C");
-      return;
-    }
+    if (d.k > L) g.fold_k = L;
   }
   if (gmk::tc_gemm(g, stream, &err)) throw Error(std::string("gemm(tcgen05): ") + err);
 }
