@@ -425,8 +425,16 @@ __global__ void __launch_bounds__(kNumThreads, 1)
         store_row32(p, row, nb * Cfg::kBlockN + c, v, alpha_eff);
         return;
       }
-      uint8_t* buf = stg + (iter & 1) * 4096;
-      if (lane == 0 && iter >= 2) bulk_wait_read<1>();
+      // 16-bit C: a slice is 2 KB, so the warp's 8 KB holds four of them
+      // (three stores in flight while the next slice is staged); fp32 C: two.
+      uint8_t* buf;
+      if (cbytes == 2) {
+        buf = stg + (iter & 3) * 2048;
+        if (lane == 0 && iter >= 4) bulk_wait_read<3>();
+      } else {
+        buf = stg + (iter & 1) * 4096;
+        if (lane == 0 && iter >= 2) bulk_wait_read<1>();
+      }
       ++iter;
       __syncwarp();
       if (cbytes == 2) {

@@ -20,4 +20,4 @@ for i in range(reps):
     ts.append(e0.elapsed_time(e1))
 cs = int(C.view(torch.int16).to(torch.int64).sum().item())
 med = sorted(ts[reps // 3:])[len(ts[reps // 3:]) // 2]
-print(f"pad={pad} group={os.environ.get('GM_RASTER_GROUP','32')} n={n} median {med:.3f} ms {2*n**3/med/1e9:.1f} TFLOP/s (last {ts[-1]:.3f}) die={os.environ.get('GM_DIE_AWARE','0')} checksum={cs}")
+print(f"chunks={os.environ.get("GM_TC_CHUNKS","auto")} sync={os.environ.get("GM_TC_SYNC","auto")} group={os.environ.get("GM_RASTER_GROUP","16")} n={n} median {med:.3f} ms {2*n**3/med/1e9:.1f} TFLOP/s (last {ts[-1]:.3f}) die={os.environ.get('GM_DIE_AWARE','0')} checksum={cs}")
