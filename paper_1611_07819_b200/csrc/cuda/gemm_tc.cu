@@ -524,16 +524,24 @@ __global__ void __launch_bounds__(kNumThreads, 1)
       mbar_wait(&tfull_bar[acc], acc_phase);
       tc_fence_after();
       const uint32_t taddr = tmem_base + ((lane_grp * 32) << 16) + acc * kChunks * kMmaN;
+      // Slices of 32 columns, the TMEM load of slice s+1 in flight while
+      // slice s is converted and stored. TMA-store path: the accumulator is
+      // released as soon as the last slice is in registers; the direct path
+      // after all stores.
+      uint32_t va[32], vb[32];
+      __syncwarp();
+      tmem_ld_32x32b_x32(taddr, va);
+      tmem_wait_ld();
 #pragma unroll 1
-      for (uint32_t c = 0; c < Cfg::kBlockN; c += 32) {
-        uint32_t v[32];
-        __syncwarp();
-        tmem_ld_32x32b_x32(taddr + c, v);
+      for (uint32_t c = 0; c < Cfg::kBlockN; c += 64) {
+        const bool more = c + 64 < Cfg::kBlockN;
+        tmem_ld_32x32b_x32(taddr + c + 32, vb);
+        emit(nb, row0, row, c, va, p.alpha);
         tmem_wait_ld();
-        // TMA-store path: the accumulator is released before the last
-        // slice's stores; the direct path after all of them.
-        if (p.tma_store && c + 32 == Cfg::kBlockN) release(acc);
-        emit(nb, row0, row, c, v, p.alpha);
+        if (p.tma_store && !more) release(acc);
+        if (more) tmem_ld_32x32b_x32(taddr + c + 64, va);
+        emit(nb, row0, row, c + 32, vb, p.alpha);
+        if (more) tmem_wait_ld();
       }
       if (!p.tma_store) release(acc);
       if (++acc == kAcc) {
