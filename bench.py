@@ -468,7 +468,7 @@ def run_extra_config(args):
         # replica), SGD update (axpy on W and b) and the re-replication of the
         # new W and b that the next step's forward reads.
         batch, fi, fo = 4096, 9216, 4096
-        P = G.Precision.BF16
+        P = G.Precision.Single if args.fc_dtype == "f32" else G.Precision.BF16
         X = s.createMatrix(batch, fi, P, G.makeRowBlockLayout(batch, fi, g))
         W = s.createMatrix(fi, fo, P, G.makeColBlockLayout(fi, fo, g))
         Bv = s.createMatrix(1, fo, P, G.makeColBlockLayout(1, fo, g))
@@ -515,7 +515,7 @@ def run_extra_config(args):
             s.replay(pid, sync=False)
 
         flops = 3 * 2.0 * batch * fi * fo
-        workload = (f"FC train step bf16 batch {batch}, {fi}->{fo}: fwd (gemm, biasAdd, relu), bwd (reluGrad, "
+        workload = (f"FC train step {args.fc_dtype} batch {batch}, {fi}->{fo}: fwd (gemm, biasAdd, relu), bwd (reluGrad, "
                     "dW gemm, addRowColSum, dX gemm), SGD axpy, W/b re-replication; W col-block + replicated, "
                     "X row-block; value counts the 3 GEMMs' flops")
     else:
@@ -571,6 +571,8 @@ def main():
     ap.add_argument("--no-c2", dest="c2", action="store_false")
     ap.add_argument("--no-numa-bind", action="store_true", help="do not place pinned e2e buffers on the GPU's NUMA node")
     ap.add_argument("--config", default="c3", choices=["c3", "fc", "fp64"])
+    ap.add_argument("--fc-dtype", default="bf16", choices=["bf16", "f32"],
+                    help="--config fc storage: bf16 (fp32 accumulate) or f32 (Single compute, 3xTF32)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
