@@ -233,7 +233,7 @@ __global__ void __launch_bounds__(kNumThreads, 1)
       mbar_init(&full_bar[s], 1);
       mbar_init(&empty_bar[s], kPairs);  // a commit from every pair that reads the slot
     }
-    for (uint32_t a = 0; a < 2; ++a) {  // wide tiles: tempty_bar[0/1] = low/high TMEM half
+    for (uint32_t a = 0; a < kAcc; ++a) {
       mbar_init(&tfull_bar[a], 1);
       mbar_init(&tempty_bar[a], 4 * kCG);
     }
@@ -351,83 +351,13 @@ __global__ void __launch_bounds__(kNumThreads, 1)
       const uint32_t a_step = p.a_mn_major ? kMmaK * kSwizzleBytes : 32;
       const uint32_t b_step = p.b_mn_major ? kMmaK * kSwizzleBytes : 32;
       uint32_t fq = 0;  // fold mode: k-chunks issued so far
-      // The UMMAs of one k-block (stage) for the chunks in [c0, c1).
-      auto issue_kblock = [&](uint32_t stg_idx, uint32_t tmem_acc, uint32_t kq, uint32_t c0, uint32_t c1) {
-        const uint32_t sa = smem_u32(smem + stg_idx * Cfg::kStageBytes);
-        const uint32_t sb = sa + Cfg::kParts * Cfg::kBytesA;
-#pragma unroll
-        for (uint32_t kk = 0; kk < kBlockK / kMmaK; ++kk) {
-          const uint32_t first = (kq | kk) == 0 ? 0u : 1u;
-          const uint64_t ah = sdesc_sw128(sa + kk * a_step, a_lbo, 1024);
-#pragma unroll
-          for (uint32_t c = 0; c < kChunks; ++c) {
-            if (c < c0 || c >= c1) continue;
-            const uint32_t tmem_d = tmem_acc + c * kMmaN;
-            const uint32_t bc = sb + c * Cfg::kBytesBChunk;
-            const uint64_t bh = sdesc_sw128(bc + kk * b_step, b_lbo, 1024);
-            if constexpr (kSplit) {
-              const uint64_t al = sdesc_sw128(sa + Cfg::kBytesA + kk * a_step, a_lbo, 1024);
-              const uint64_t bl = sdesc_sw128(bc + Cfg::kBytesB + kk * b_step, b_lbo, 1024);
-              mma_tf32<kCG>(tmem_d, al, bh, p.idesc, first);
-              mma_tf32<kCG>(tmem_d, ah, bl, p.idesc, 1u);
-              mma_tf32<kCG>(tmem_d, ah, bh, p.idesc, 1u);
-            } else if constexpr (kElemBytes == 4) {
-              mma_tf32<kCG>(tmem_d, ah, bh, p.idesc, first);
-            } else {
-              mma_f16<kCG>(tmem_d, ah, bh, p.idesc, first);
-            }
-          }
-        }
-      };
-      auto commit_stage = [&](uint32_t stg_idx) {
-        if constexpr (kCG == 2) mma_commit_2sm(&empty_bar[stg_idx], all_mask);
-        else mma_commit(&empty_bar[stg_idx]);
-      };
-      auto commit_full = [&](uint32_t a) {
-        if constexpr (kCG == 2) mma_commit_2sm(&tfull_bar[a], pair_mask);
-        else mma_commit(&tfull_bar[a]);
-      };
-      auto advance = [&]() {
-        if (++stage == kStages) {
-          stage = 0;
-          phase ^= 1;
-        }
-      };
       for (uint32_t t = unit; t < num_tiles; t += num_units) {
-        uint32_t kb0 = 0;
-        if (kChunks == 2 && !fold) {
-          // Wide tile, one accumulator over all 512 TMEM columns, released
-          // by the epilogue in halves. Start the tile on the low half: the
-          // first (up to kStages) k-blocks' chunk-0 UMMAs, while the
-          // epilogue still drains the high half; then their chunk-1 UMMAs
-          // once the high half is free (the stages stay held until then).
-          const uint32_t pre = num_kb < kStages ? num_kb : kStages;
-          const uint32_t s0 = stage, ph0 = phase;
-          mbar_wait(&tempty_bar[0], acc_phase ^ 1);
-          tc_fence_after();
-          for (uint32_t j = 0; j < pre; ++j) {
-            mbar_wait(&full_bar[stage], phase);
-            tc_fence_after();
-            issue_kblock(stage, tmem_base, j, 0, 1);
-            advance();
-          }
-          mbar_wait(&tempty_bar[1], acc_phase ^ 1);
-          tc_fence_after();
-          stage = s0;
-          phase = ph0;
-          for (uint32_t j = 0; j < pre; ++j) {
-            issue_kblock(stage, tmem_base, j, 1, 2);
-            commit_stage(stage);
-            if (j + 1 == num_kb) commit_full(0);
-            advance();
-          }
-          kb0 = pre;
-        } else if (!fold) {
+        if (!fold) {
           mbar_wait(&tempty_bar[acc], acc_phase ^ 1);
           tc_fence_after();
         }
         const uint32_t tmem_acc = fold ? tmem_base : tmem_base + acc * kChunks * kMmaN;
-        for (uint32_t kb = kb0; kb < num_kb; ++kb) {
+        for (uint32_t kb = 0; kb < num_kb; ++kb) {
           const uint32_t kq = fold ? kb % p.fold_kb : kb;  // k-block within the accumulation
           if (fold && kq == 0) {
             mbar_wait(&tempty_bar[0], (fq & 1) ^ 1);  // chunk buffer folded by the epilogue
@@ -435,13 +365,41 @@ __global__ void __launch_bounds__(kNumThreads, 1)
           }
           mbar_wait(&full_bar[stage], phase);
           tc_fence_after();
-          issue_kblock(stage, tmem_acc, kq, 0, kChunks);
-          commit_stage(stage);
+          const uint32_t sa = smem_u32(smem + stage * Cfg::kStageBytes);
+          const uint32_t sb = sa + Cfg::kParts * Cfg::kBytesA;
+#pragma unroll
+          for (uint32_t kk = 0; kk < kBlockK / kMmaK; ++kk) {
+            const uint32_t first = (kq | kk) == 0 ? 0u : 1u;
+            const uint64_t ah = sdesc_sw128(sa + kk * a_step, a_lbo, 1024);
+#pragma unroll
+            for (uint32_t c = 0; c < kChunks; ++c) {
+              const uint32_t tmem_d = tmem_acc + c * kMmaN;
+              const uint32_t bc = sb + c * Cfg::kBytesBChunk;
+              const uint64_t bh = sdesc_sw128(bc + kk * b_step, b_lbo, 1024);
+              if constexpr (kSplit) {
+                const uint64_t al = sdesc_sw128(sa + Cfg::kBytesA + kk * a_step, a_lbo, 1024);
+                const uint64_t bl = sdesc_sw128(bc + Cfg::kBytesB + kk * b_step, b_lbo, 1024);
+                mma_tf32<kCG>(tmem_d, al, bh, p.idesc, first);
+                mma_tf32<kCG>(tmem_d, ah, bl, p.idesc, 1u);
+                mma_tf32<kCG>(tmem_d, ah, bh, p.idesc, 1u);
+              } else if constexpr (kElemBytes == 4) {
+                mma_tf32<kCG>(tmem_d, ah, bh, p.idesc, first);
+              } else {
+                mma_f16<kCG>(tmem_d, ah, bh, p.idesc, first);
+              }
+            }
+          }
+          if constexpr (kCG == 2) mma_commit_2sm(&empty_bar[stage], all_mask);
+          else mma_commit(&empty_bar[stage]);
           if (fold ? (kq + 1 == p.fold_kb || kb + 1 == num_kb) : kb + 1 == num_kb) {
-            commit_full(fold ? 0 : acc);
+            if constexpr (kCG == 2) mma_commit_2sm(&tfull_bar[fold ? 0 : acc], pair_mask);
+            else mma_commit(&tfull_bar[fold ? 0 : acc]);
             if (fold) ++fq;
           }
-          advance();
+          if (++stage == kStages) {
+            stage = 0;
+            phase ^= 1;
+          }
         }
         if (!fold && ++acc == kAcc) {
           acc = 0;
@@ -567,10 +525,9 @@ __global__ void __launch_bounds__(kNumThreads, 1)
       tc_fence_after();
       const uint32_t taddr = tmem_base + ((lane_grp * 32) << 16) + acc * kChunks * kMmaN;
       // Slices of 32 columns, the TMEM load of slice s+1 in flight while
-      // slice s is converted and stored. TMEM is released as soon as it is
-      // in registers: a wide tile's low half (columns [0, 256), which the
-      // next tile's first UMMAs write) after slice 7, its high half after
-      // the last slice; a 256-wide tile's accumulator after its last slice.
+      // slice s is converted and stored. TMA-store path: the accumulator is
+      // released as soon as the last slice is in registers; the direct path
+      // after all stores.
       uint32_t va[32], vb[32];
       __syncwarp();
       tmem_ld_32x32b_x32(taddr, va);
@@ -581,16 +538,12 @@ __global__ void __launch_bounds__(kNumThreads, 1)
         tmem_ld_32x32b_x32(taddr + c + 32, vb);
         emit(nb, row0, row, c, va, p.alpha);
         tmem_wait_ld();
-        if (kChunks == 2) {
-          if (c + 64 == kMmaN) release(0);
-          if (!more) release(1);
-        } else if (!more) {
-          release(acc);
-        }
+        if (p.tma_store && !more) release(acc);
         if (more) tmem_ld_32x32b_x32(taddr + c + 64, va);
         emit(nb, row0, row, c + 32, vb, p.alpha);
         if (more) tmem_wait_ld();
       }
+      if (!p.tma_store) release(acc);
       if (++acc == kAcc) {
         acc = 0;
         acc_phase ^= 1;
