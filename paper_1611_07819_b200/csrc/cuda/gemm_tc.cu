@@ -28,6 +28,7 @@
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
+#include <atomic>
 #include <cstdint>
 #include <cstring>
 #include <cstdio>
@@ -84,7 +85,7 @@ struct TcParams {
   uint32_t num_m_blocks, num_n_blocks;  // in units of the CTA(-pair) tile
   uint32_t group;                       // raster group (M-blocks)
   uint32_t hint_a, hint_b;              // L2 policy for A / B loads (0 normal, 1 evict_last, 2 evict_first)
-  uint32_t* sync_ctr;                   // lockstep counter (zeroed per launch) or null
+  uint32_t* sync_ctr;                   // lockstep counter (a zeroed ring slot) or null
   uint32_t sync_every;                  // k-blocks per lockstep checkpoint
   uint32_t tma_store;                   // C written by TMA stores (beta == 0, aligned C)
   uint32_t fold_kb;                     // k-blocks per folded k-chunk (Single compute), 0 = off
@@ -338,7 +339,13 @@ __global__ void __launch_bounds__(kNumThreads, 1)
           }
         }
       }
-      if (synced) atomicAdd(p.sync_ctr, 1u << 24);  // finished: release the others' waits
+      if (synced) {
+        // Finished: release the others' waits. The last pair to finish
+        // (nobody waits any more) zeroes the counter for the launch that
+        // reuses this slot, so launches need no memset in between.
+        const uint32_t old = atomicAdd(p.sync_ctr, 1u << 24);
+        if ((old >> 24) + 1 == num_units) atomicExch(p.sync_ctr, 0u);
+      }
     }
   } else if (warp == 1) {
     // ------------------------------------------------------------ MMA issuer
@@ -698,12 +705,19 @@ int launch(const TcOperand& a, const TcOperand& b, const TcOperand* a_lo, const 
   if (need < ctas) ctas = need;
   cfg.gridDim = dim3(ctas, 1, 1);
   if (p.sync_every > 0) {
+    // A ring of 64 counters per device, zeroed once; each launch takes the
+    // next slot and its last finishing pair zeroes it again.
     static uint32_t* ctr[64] = {nullptr};
-    if (dev < 64 && !ctr[dev]) cudaMalloc(&ctr[dev], 256);
-    if (dev < 64 && ctr[dev]) {
-      p.sync_ctr = ctr[dev];
-      cudaMemsetAsync(p.sync_ctr, 0, 4, stream);
+    static std::atomic<uint32_t> next[64];
+    if (dev < 64 && !ctr[dev]) {
+      if (cudaMalloc(&ctr[dev], 64 * sizeof(uint32_t)) == cudaSuccess) {
+        cudaMemset(ctr[dev], 0, 64 * sizeof(uint32_t));
+      } else {
+        cudaGetLastError();
+        ctr[dev] = nullptr;
+      }
     }
+    if (dev < 64 && ctr[dev]) p.sync_ctr = ctr[dev] + (next[dev].fetch_add(1) % 64);
   }
   static const bool debug = std::getenv("GM_DEBUG") != nullptr;
   if (debug)
