@@ -1284,7 +1284,7 @@ void Session::reshape(DistMatrix m, const Layout& newLayout, std::optional<Preci
 // before it next mutates that matrix.
 // NCCL plane (SPMD fallback): grouped ncclSend/ncclRecv, packing/unpacking
 // strided pieces through arena staging.
-void Session::exchange(std::vector<Xfer>& xs, bool onComm, bool commit) {
+void Session::exchange(std::vector<Xfer>& xs, bool onComm, bool commit, int maxPull) {
   flushWritten(curExec_);
   auto streamOf = [&](Worker& w) { return onComm ? w.comm : w.compute; };
   const int sIdx = onComm ? 0 : 1;
@@ -1304,7 +1304,8 @@ void Session::exchange(std::vector<Xfer>& xs, bool onComm, bool commit) {
         const int v = e ? std::atoi(e) : Worker::kPullStreams;
         return static_cast<std::uint32_t>(std::clamp(v, 1, Worker::kPullStreams));
       }();
-      cudaStream_t ps = d.pulls[src % nPull];
+      const std::uint32_t np = maxPull > 0 ? std::min<std::uint32_t>(nPull, static_cast<std::uint32_t>(maxPull)) : nPull;
+      cudaStream_t ps = d.pulls[src % np];
       if (forked.insert({&d, ps}).second) {
         cudaEvent_t e = d.event();
         cudaCheck(cudaEventRecord(e, streamOf(d)), "exchange: fork");
@@ -2189,7 +2190,17 @@ void Session::execReplicate(std::uint64_t id) {
       entry = &e;
       targets.push_back(w);
     }
-    for (const auto& t : M.layout.tiles) {
+    // Ring order: consumer r pulls from r+1, r+2, ... and copies its own
+    // tile last, so pieces queued on one stream never have every consumer
+    // hitting the same source at once.
+    std::vector<std::size_t> order(M.layout.tiles.size());
+    for (std::size_t i = 0; i < order.size(); ++i) order[i] = i;
+    const std::uint32_t P = opts_.workers;
+    std::stable_sort(order.begin(), order.end(), [&](std::size_t a, std::size_t b) {
+      return (M.layout.tiles[a].second.rank + P - r - 1) % P < (M.layout.tiles[b].second.rank + P - r - 1) % P;
+    });
+    for (std::size_t ti : order) {
+      const auto& t = M.layout.tiles[ti];
       const std::uint32_t src = t.second.rank;
       Worker* sw = local(src);
       if (!w && !sw) continue;
@@ -2210,7 +2221,11 @@ void Session::execReplicate(std::uint64_t id) {
       xs.push_back(x);
     }
   }
-  exchange(xs, true);
+  // Every worker gathers from every other at once here (all-to-all): two
+  // pull streams per consumer, in ring order, measured 478 GB/s per GPU at
+  // N = 4 against 357 with four streams and 382 with one
+  // (tools/dev/dev_repl.py, profiles/r01_multigpu.md).
+  exchange(xs, true, true, 2);
   for (Worker* w : targets) {
     w->activate();
     cudaCheck(cudaEventRecord(w->replicas[id].ready, w->comm), "replica ready");

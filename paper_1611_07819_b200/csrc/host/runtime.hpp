@@ -392,7 +392,9 @@ class Session {
   // WAR waits land there instead of on the compute streams.
   void mutationHook(std::uint64_t id, std::uint64_t oldVersion, bool toH2d = false);
   std::vector<std::uint64_t> pendingTouched_;  // matrices the previous op used
-  void exchange(std::vector<Xfer>& xs, bool onComm, bool commit = true);
+  // maxPull caps the copy-engine pull streams this exchange spreads its
+  // sources over (0 = all of Worker::kPullStreams).
+  void exchange(std::vector<Xfer>& xs, bool onComm, bool commit = true, int maxPull = 0);
   // --- RAW/WAR bookkeeping shared by the planes
   void flushWritten(std::uint64_t before);  // publish mutations of ops with exec id < before
   void commitReads();    // consumers publish readDone for this op's pulls
