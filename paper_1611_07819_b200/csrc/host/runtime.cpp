@@ -997,7 +997,7 @@ void Session::execDestroy(std::uint64_t id) {
     auto rit = w.replicas.find(id);
     if (rit != w.replicas.end()) {
       cudaStreamWaitEvent(w.compute, rit->second.ready, 0);
-      w.arena.free(rit->second.full, w.compute);
+      if (!rit->second.alias) w.arena.free(rit->second.full, w.compute);
       cudaEventDestroy(rit->second.ready);
       w.replicas.erase(rit);
     }
@@ -2171,22 +2171,40 @@ void Session::execReplicate(std::uint64_t id) {
     if (w) {
       w->activate();
       ReplicaEntry& e = w->replicas[id];
+      if (!e.ready) cudaCheck(cudaEventCreateWithFlags(&e.ready, cudaEventDisableTiming), "replica event");
+      e.version = M.version;
+      e.state = ReplicaState::Pending;
+      if (M.layout.tiles.size() == 1 && M.layout.tiles[0].second.rank == r) {
+        // Sole owner of a single-tile matrix: the replica is the tile itself.
+        // Ready once the tile's pending writes (compute stream) are done.
+        const DeviceTile& dt = w->tiles.at(id).front();
+        if (e.full && !e.alias) {
+          cudaEvent_t ev = w->event();
+          cudaCheck(cudaEventRecord(ev, w->compute), "replica: record readers");
+          cudaCheck(cudaStreamWaitEvent(w->comm, ev, 0), "replica: wait readers");
+          w->recycle(ev);
+          w->arena.free(e.full, w->comm);
+        }
+        e.full = dt.ptr;
+        e.ld = dt.ld;
+        e.alias = true;
+        cudaCheck(cudaEventRecord(e.ready, w->compute), "replica ready");
+        continue;
+      }
       const std::uint64_t ld = paddedLd(M.cols, eb);
-      if (e.full) {
+      if (e.full && !e.alias) {
         // GEMMs on the compute stream may still read the previous version.
         cudaEvent_t ev = w->event();
         cudaCheck(cudaEventRecord(ev, w->compute), "replica: record readers");
         cudaCheck(cudaStreamWaitEvent(w->comm, ev, 0), "replica: wait readers");
         w->recycle(ev);
       }
-      if (!e.full || e.ld != ld) {
-        if (e.full) w->arena.free(e.full, w->comm);
+      if (!e.full || e.alias || e.ld != ld) {
+        if (e.full && !e.alias) w->arena.free(e.full, w->comm);
         e.full = w->arena.alloc(M.rows * ld * eb, w->comm);
         e.ld = ld;
+        e.alias = false;
       }
-      if (!e.ready) cudaCheck(cudaEventCreateWithFlags(&e.ready, cudaEventDisableTiming), "replica event");
-      e.version = M.version;
-      e.state = ReplicaState::Pending;
       entry = &e;
       targets.push_back(w);
     }

@@ -135,6 +135,10 @@ enum class ReplicaState : std::uint8_t { Valid = 0, Pending = 1, Stale = 2 };
 struct ReplicaEntry {
   void* full = nullptr;  // whole matrix, row-major, pitch `ld`
   std::uint64_t ld = 0;
+  // The worker owns the whole matrix as one tile: `full` is that tile (no
+  // copy, not owned by the entry). Mutations bump the version, so a replica
+  // read only ever sees the version it was made for.
+  bool alias = false;
   std::uint64_t version = 0;
   ReplicaState state = ReplicaState::Pending;
   cudaEvent_t ready = nullptr;

@@ -156,3 +156,49 @@ def test_panel_cache_off_moves_panels_every_op():
     expect = 4 * 2 * 2 * (n // 2) * (n // 2)
     assert moved[1] == [expect] * 3
     assert moved[0][0] == expect and moved[0][1] == 0 and moved[0][2] == 0
+
+
+def test_single_tile_owner_replica_aliases_the_tile():
+    """A worker that owns a whole single-tile matrix replicates it without a
+    copy (the replica is the tile): no bytes move, no new allocation, reads
+    through the replica see exactly the replicated version, a mutation makes
+    it stale (the next GEMM reads the tile), re-replication and a reshape to
+    a multi-tile layout (real copies again) stay correct."""
+    p, batch, fi, fo = 4, 256, 384, 320
+    g = G.makeWorkerGroup(p)
+    with G.Session(workers=p) as s:
+        X = s.createMatrix(batch, fi, G.Precision.BF16, G.makeRowBlockLayout(batch, fi, g))
+        W = s.createMatrix(fi, fo, G.Precision.BF16, G.makeSingleTileLayout(fi, fo, 2))
+        Z = s.createMatrix(batch, fo, G.Precision.Single, G.makeRowBlockLayout(batch, fo, g))
+        s.fillUniform(X, 1)
+        s.fillUniform(W, 2, -0.05, 0.05)
+        x = s.getDataRaw(X)
+
+        def check(w):
+            G.gemm(s, X, W, Z, 1.0, 0.0)
+            want = O.gemm_c(batch, fo, fi, x, 3, w, 3, np.zeros((batch, fo), np.float32), 1, 1.0, 0.0, 0, 0)
+            assert O.rel_fro(s.getDataRaw(Z), want) <= 1e-5
+
+        w0 = s.getDataRaw(W)
+        before = s.queryWorkerStats()
+        assert s.wait(s.replicateAsync(W)) == G.ReplState.Done
+        after = s.queryWorkerStats()
+        # workers 0, 1, 3 copy W; worker 2 (the owner) aliases its tile
+        moved = [a["bytes_received"] - b["bytes_received"] for a, b in zip(after, before)]
+        assert moved[2] == 0 and sum(moved) == (p - 1) * fi * fo * 2
+        check(w0)
+        G.mulScalar(s, W, 1.5)  # in place: the replica is stale now
+        w1 = s.getDataRaw(W)
+        assert not np.array_equal(w0, w1)
+        check(w1)
+        assert s.wait(s.replicateAsync(W)) == G.ReplState.Done
+        check(w1)
+        # multi-tile layout: every worker now needs a real replica copy
+        s.reshape(W, G.makeColBlockLayout(fi, fo, g), G.Precision.BF16)
+        assert s.wait(s.replicateAsync(W)) == G.ReplState.Done
+        check(s.getDataRaw(W))
+        s.destroy(W)
+        W = s.createMatrix(fi, fo, G.Precision.BF16, G.makeSingleTileLayout(fi, fo, 0))
+        s.fillUniform(W, 5, -0.05, 0.05)
+        assert s.wait(s.replicateAsync(W)) == G.ReplState.Done
+        check(s.getDataRaw(W))
