@@ -58,6 +58,22 @@ def test_device_generator_matches_oracle_every_precision():
             assert np.array_equal(got.view(np.uint8), want.view(np.uint8)), p
 
 
+@pytest.mark.gpu
+@pytest.mark.parametrize("rows,cols,pr,pc", [(40, 96, 1, 3), (41, 180, 2, 2), (33, 184, 1, 2), (300, 1024, 2, 2)])
+def test_device_generator_vector_path_matches_oracle(rows, cols, pr, pc):
+    # Tiles with 16-byte aligned rows take the 8-columns-per-thread generator;
+    # 90- and 92-wide tiles leave a scalar tail (fp64 / fp32) or fall back
+    # (16-bit rows not 16-byte aligned).
+    with G.Session(workers=pr * pc) as s:
+        for p in (0, 1, 2, 3):
+            M = s.createMatrix(rows, cols, G.Precision(p),
+                               G.makeGridLayout(rows, cols, pr, pc, G.makeWorkerGroup(pr * pc)))
+            s.fillUniform(M, 23, -1.0, 1.0)
+            got = s.getDataRaw(M)
+            want = O.fill_uniform(rows, cols, p, 23, -1.0, 1.0)
+            assert np.array_equal(got.view(np.uint8), want.view(np.uint8)), p
+
+
 def test_arena_reuse_and_counters():
     lib = _lib.load()
     a = ctypes.c_void_p()
