@@ -89,6 +89,13 @@ struct TcParams {
   uint32_t sync_every;                  // k-blocks per lockstep checkpoint
   uint32_t tma_store;                   // C written by TMA stores (beta == 0, aligned C)
   uint32_t fold_kb;                     // k-blocks per folded k-chunk (Single compute), 0 = off
+  // Fused FC forward epilogue (bf16 C only; null = off): bias[col] of the
+  // local C columns, act = relu output with pitch ld_act.
+  const uint16_t* bias;
+  uint16_t* act;
+  uint64_t ld_act;
+  uint32_t bias_vec, act_vec;           // 16-byte loads / stores legal
+  uint32_t act_tma;                     // act written by TMA stores beside C's
 };
 
 // Lockstep: persistent CTA pairs run ~100 tiles back to back and drift apart,
@@ -135,6 +142,60 @@ __device__ __forceinline__ float load_c(const TcParams& p, uint64_t off) {
   return __half2float(reinterpret_cast<const __half*>(p.c)[off]);
 }
 
+// Replayed `gemm -> biasAdd -> relu` (bf16, Single compute) in one pass:
+// each op of the unfused sequence rounds its result to storage precision, so
+// z = bf16(float(bf16(x)) + b) and act = z > 0 ? z : 0 exactly as the
+// separate ops compute them (reference kernels.cpp:741-815; biasAdd adds in
+// float without FMA, relu maps NaN and -0 to +0). f becomes float(z); act is
+// written with direct stores (each thread owns 64 contiguous bytes of a row).
+// act_out != null: the relu words are returned (staged for a TMA store)
+// instead of stored.
+__device__ __forceinline__ void bias_relu32(const TcParams& p, uint32_t row, uint32_t col0, float (&f)[32],
+                                            uint32_t* act_out = nullptr) {
+  const bool full = col0 + 32 <= p.n;
+  const bool vec = full && p.bias_vec && p.act_vec;
+  uint16_t* dst = p.act + static_cast<uint64_t>(row) * p.ld_act + col0;
+  // Eight columns at a time: one 16-byte bias load and one 16-byte act store.
+#pragma unroll
+  for (int g = 0; g < 4; ++g) {
+    uint32_t bw[4];
+    if (vec) {
+      const uint4 w = __ldg(reinterpret_cast<const uint4*>(p.bias + col0) + g);
+      bw[0] = w.x; bw[1] = w.y; bw[2] = w.z; bw[3] = w.w;
+    } else {
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const uint32_t c = col0 + 8 * g + 2 * j;
+        bw[j] = (c < p.n ? p.bias[c] : 0u) | ((c + 1 < p.n ? p.bias[c + 1] : 0u) << 16);
+      }
+    }
+    uint32_t packed[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int i0 = 8 * g + 2 * j;
+      const float b0 = __uint_as_float(bw[j] << 16), b1 = __uint_as_float(bw[j] & 0xFFFF0000u);
+      const float h0 = __bfloat162float(__float2bfloat16_rn(f[i0]));
+      const float h1 = __bfloat162float(__float2bfloat16_rn(f[i0 + 1]));
+      f[i0] = __bfloat162float(__float2bfloat16_rn(__fadd_rn(h0, b0)));
+      f[i0 + 1] = __bfloat162float(__float2bfloat16_rn(__fadd_rn(h1, b1)));
+      const uint32_t lo = f[i0] > 0.0f ? (__float_as_uint(f[i0]) >> 16) : 0u;
+      const uint32_t hi = f[i0 + 1] > 0.0f ? (__float_as_uint(f[i0 + 1]) >> 16) : 0u;
+      packed[j] = lo | (hi << 16);
+    }
+    if (act_out) {
+#pragma unroll
+      for (int j = 0; j < 4; ++j) act_out[4 * g + j] = packed[j];
+    } else if (row < p.m) {
+      if (vec) {
+        reinterpret_cast<uint4*>(dst)[g] = make_uint4(packed[0], packed[1], packed[2], packed[3]);
+      } else {
+        for (uint32_t i = 0; i < 8 && col0 + 8 * g + i < p.n; ++i)
+          dst[8 * g + i] = static_cast<uint16_t>(i & 1 ? packed[i >> 1] >> 16 : packed[i >> 1] & 0xFFFFu);
+      }
+    }
+  }
+}
+
 __device__ __forceinline__ void store_row32(const TcParams& p, uint32_t row, uint32_t col0,
                                             const uint32_t (&v)[32], float alpha) {
   if (row >= p.m || col0 >= p.n) return;
@@ -151,6 +212,7 @@ __device__ __forceinline__ void store_row32(const TcParams& p, uint32_t row, uin
       for (uint32_t i = 0; i < 32 && col0 + i < p.n; ++i) f[i] += p.beta * load_c(p, base + i);
     }
   }
+  if (p.bias) bias_relu32(p, row, col0, f);
   if (full && p.c_vec) {
     if (p.c_dtype == 2) {
       float4* dst = reinterpret_cast<float4*>(reinterpret_cast<float*>(p.c) + base);
@@ -195,7 +257,8 @@ __global__ void __launch_bounds__(kNumThreads, 1)
     tc_gemm_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid_constant__ CUtensorMap tm_b,
                    const __grid_constant__ CUtensorMap tm_a_lo,
                    const __grid_constant__ CUtensorMap tm_b_lo,
-                   const __grid_constant__ CUtensorMap tm_c, const TcParams p) {
+                   const __grid_constant__ CUtensorMap tm_c,
+                   const __grid_constant__ CUtensorMap tm_act, const TcParams p) {
   using Cfg = TcCfg<kCG, kElemBytes, kSplit, kChunks, kPairs>;
   constexpr uint32_t kStages = Cfg::kStages;
   constexpr uint32_t kBlockK = Cfg::kBlockK;
@@ -226,6 +289,7 @@ __global__ void __launch_bounds__(kNumThreads, 1)
     tma_prefetch_desc(&tm_a);
     tma_prefetch_desc(&tm_b);
     if (p.tma_store) tma_prefetch_desc(&tm_c);
+    if (p.act_tma) tma_prefetch_desc(&tm_act);
     if (kSplit) {
       tma_prefetch_desc(&tm_a_lo);
       tma_prefetch_desc(&tm_b_lo);
@@ -435,7 +499,11 @@ __global__ void __launch_bounds__(kNumThreads, 1)
       // 16-bit C: a slice is 2 KB, so the warp's 8 KB holds four of them
       // (three stores in flight while the next slice is staged); fp32 C: two.
       uint8_t* buf;
-      if (cbytes == 2) {
+      if (p.act_tma) {
+        // Fused bias/relu: C and act slices side by side (2 x 2 KB), two pairs in flight.
+        buf = stg + (iter & 1) * 4096;
+        if (lane == 0 && iter >= 2) bulk_wait_read<1>();
+      } else if (cbytes == 2) {
         buf = stg + (iter & 3) * 2048;
         if (lane == 0 && iter >= 4) bulk_wait_read<3>();
       } else {
@@ -447,9 +515,24 @@ __global__ void __launch_bounds__(kNumThreads, 1)
       if (cbytes == 2) {
         // 32 x 64 B rows, 64-byte swizzle: chunk j of row r at (j ^ ((r >> 1) & 3)).
         uint32_t packed[16];
+        float xf[32];
+#pragma unroll
+        for (int i = 0; i < 32; ++i) xf[i] = alpha_eff * __uint_as_float(v[i]);
+        if (p.act_tma) {
+          uint32_t ap[16];
+          bias_relu32(p, row, nb * Cfg::kBlockN + c, xf, ap);
+#pragma unroll
+          for (uint32_t j = 0; j < 4; ++j) {
+            const uint32_t pj = j ^ ((lane >> 1) & 3);
+            *reinterpret_cast<uint4*>(buf + 2048 + lane * 64 + pj * 16) =
+                make_uint4(ap[4 * j], ap[4 * j + 1], ap[4 * j + 2], ap[4 * j + 3]);
+          }
+        } else if (p.bias) {
+          bias_relu32(p, row, nb * Cfg::kBlockN + c, xf);
+        }
 #pragma unroll
         for (int i = 0; i < 16; ++i) {
-          const float x0 = alpha_eff * __uint_as_float(v[2 * i]), x1 = alpha_eff * __uint_as_float(v[2 * i + 1]);
+          const float x0 = xf[2 * i], x1 = xf[2 * i + 1];
           if (p.c_dtype == 1) {
             __nv_bfloat162 h = __floats2bfloat162_rn(x0, x1);
             packed[i] = *reinterpret_cast<uint32_t*>(&h);
@@ -478,6 +561,8 @@ __global__ void __launch_bounds__(kNumThreads, 1)
       __syncwarp();
       if (lane == 0) {
         tma_store_2d(&tm_c, buf, static_cast<int32_t>(nb * Cfg::kBlockN + c), static_cast<int32_t>(row0));
+        if (p.act_tma)
+          tma_store_2d(&tm_act, buf + 2048, static_cast<int32_t>(nb * Cfg::kBlockN + c), static_cast<int32_t>(row0));
         bulk_commit();
       }
     };
@@ -737,7 +822,15 @@ int launch(const TcOperand& a, const TcOperand& b, const TcOperand* a_lo, const 
         p.tma_store = 1;
     }
   }
-  cudaError_t e = cudaLaunchKernelEx(&cfg, kern, ma, mb, mal, mbl, mc, p);
+  CUtensorMap mact = mc;
+  p.act_tma = 0;
+  if (p.tma_store && p.bias && p.act_vec) {
+    const char* e2 = nullptr;
+    if (make_map_2d(&mact, p.act, CU_TENSOR_MAP_DATA_TYPE_UINT16, 2, p.n, p.m, p.ld_act, 32, 32, &e2,
+                    CU_TENSOR_MAP_SWIZZLE_64B) == 0)
+      p.act_tma = 1;
+  }
+  cudaError_t e = cudaLaunchKernelEx(&cfg, kern, ma, mb, mal, mbl, mc, mact, p);
   count_launch();
   if (e != cudaSuccess) {
     *err = cudaGetErrorString(e);
@@ -762,6 +855,17 @@ int tc_gemm(const TcGemmArgs& g, cudaStream_t stream, const char** err) {
   p.c_dtype = g.c_dtype;
   const uint32_t cb = g.c_dtype == 2 ? 4 : 2;
   p.c_vec = ((reinterpret_cast<uintptr_t>(g.c) % 16) == 0 && (g.ldc * cb) % 16 == 0) ? 1 : 0;
+  if (g.bias) {
+    if (g.c_dtype != 1 || !g.act) {
+      *err = "fused bias/relu epilogue needs bf16 C and an output";
+      return 1;
+    }
+    p.bias = static_cast<const uint16_t*>(g.bias);
+    p.act = static_cast<uint16_t*>(g.act);
+    p.ld_act = g.ld_act;
+    p.bias_vec = (reinterpret_cast<uintptr_t>(g.bias) % 16) == 0 ? 1 : 0;
+    p.act_vec = ((reinterpret_cast<uintptr_t>(g.act) % 16) == 0 && (g.ld_act * 2) % 16 == 0) ? 1 : 0;
+  }
   const int cg = g.cta_group == 1 ? 1 : 2;
   const uint32_t mrows = kBlockMcta * cg;
   // Wide tiles (256 x 512 per CTA pair, two UMMAs per k-step) halve the

@@ -27,6 +27,11 @@ struct TcGemmArgs {
   // TF32 kinds: fold the tensor-core accumulation into an fp32 running sum
   // every fold_k of k (a multiple of 32; 0 = accumulate all of k in TMEM).
   uint64_t fold_k = 0;
+  // Fused `biasAdd + relu` epilogue (bf16 C): C = bf16(bf16(alpha*acc) +
+  // bias[col]), act = relu(C). bias holds the local C's n columns.
+  const void* bias = nullptr;
+  void* act = nullptr;
+  uint64_t ld_act = 0;
 };
 
 // Launches on `stream`; returns 0 or 1 with *err set (static string).

@@ -216,8 +216,10 @@ std::uint64_t gemmWorkspaceBytes(const gm_gemm_desc& d, const void* a, const voi
 }
 
 void gemmLocal(const gm_gemm_desc& d, const void* a, const void* b, void* c, void* workspace,
-               std::uint64_t workspaceBytes, cudaStream_t stream) {
+               std::uint64_t workspaceBytes, cudaStream_t stream, const BiasReluEpilogue* ep) {
   if (d.m == 0 || d.n == 0) return;
+  if (ep && (d.alpha == 0.0 || d.k == 0 || d.prec_c != GM_BF16 || d.prec_a == GM_DOUBLE || d.prec_b == GM_DOUBLE))
+    throw Error("gemm: fused bias/relu epilogue needs the tcgen05 path with bf16 C");
   for (int p : {d.prec_a, d.prec_b, d.prec_c}) (void)elemBytes(p);
   if (d.m > 0x7FFFFFFFull || d.n > 0x7FFFFFFFull || d.k > 0x7FFFFFFFull)
     throw Error("gemm: dimension exceeds 2^31");
@@ -346,6 +348,11 @@ void gemmLocal(const gm_gemm_desc& d, const void* a, const void* b, void* c, voi
     // independent.
     const std::uint64_t L = tf32Chunk();
     if (d.k > L) g.fold_k = L;
+  }
+  if (ep) {
+    g.bias = ep->bias;
+    g.act = ep->act;
+    g.ld_act = ep->ldAct;
   }
   if (gmk::tc_gemm(g, stream, &err)) throw Error(std::string("gemm(tcgen05): ") + err);
 }

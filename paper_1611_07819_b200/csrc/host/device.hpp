@@ -63,7 +63,14 @@ class DeviceArena {
 std::uint64_t gemmWorkspaceBytes(const gm_gemm_desc& d);  // worst case over alignment
 std::uint64_t gemmWorkspaceBytes(const gm_gemm_desc& d, const void* a, const void* b);
 // Throws gridmath::Error on failure.
+// Optional fused epilogue (replayed gemm -> biasAdd -> relu, bf16 C on the
+// tcgen05 path): bias = the C tile's n bias columns, act = relu output.
+struct BiasReluEpilogue {
+  const void* bias = nullptr;
+  void* act = nullptr;
+  std::uint64_t ldAct = 0;
+};
 void gemmLocal(const gm_gemm_desc& d, const void* a, const void* b, void* c, void* workspace,
-               std::uint64_t workspaceBytes, cudaStream_t stream);
+               std::uint64_t workspaceBytes, cudaStream_t stream, const BiasReluEpilogue* ep = nullptr);
 
 }  // namespace gridmath

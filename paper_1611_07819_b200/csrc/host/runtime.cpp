@@ -1920,7 +1920,17 @@ void Session::execGemm(const OpDescriptor& op) {
         }
         const std::uint64_t wsb = alphaZero ? 0 : gemmWorkspaceBytes(d, ap, bp);
         void* ws = wsb ? w.workspace(wsb) : nullptr;
-        gemmLocal(d, ap, bp, cp, ws, wsb, w.compute);
+        BiasReluEpilogue ep;
+        if (fused_) {
+          DeviceTile* at = nullptr;
+          for (DeviceTile& t : w.tiles.at(fused_->act))
+            if (t.extent == e) at = &t;
+          if (!at) throw Error("gemm: fused relu output tile missing on worker " + std::to_string(w.rank));
+          ep.bias = fused_->bias.at({w.rank, e.rowStart, e.colStart});
+          ep.act = static_cast<std::uint8_t*>(at->ptr) + (r0 - e.rowStart) * at->ld * 2;
+          ep.ldAct = at->ld;
+        }
+        gemmLocal(d, ap, bp, cp, ws, wsb, w.compute, fused_ ? &ep : nullptr);
       }
       // Row-chunk completion of C (chunked downloads drain behind these).
       for (const auto& rr : chunkRows) {
@@ -2121,10 +2131,19 @@ void Session::replay(std::uint64_t pipelineId, bool sync) {
   if (recording_ != 0) throw Error("replay: recording still open");
   if (!closedPipelines_.count(pipelineId))
     throw Error("replay: unknown or unfinished pipeline " + std::to_string(pipelineId));
-  for (const OpDescriptor& recorded : pipelines_.at(pipelineId)) {
-    OpDescriptor step = recorded;
+  const std::vector<OpDescriptor>& ops = pipelines_.at(pipelineId);
+  for (std::size_t i = 0; i < ops.size(); ++i) {
+    OpDescriptor step = ops[i];
     step.execId = 0;
     step.recordPipeline = 0;
+    if (fusableBiasRelu(ops, i)) {
+      OpDescriptor bo = ops[i + 1], ro = ops[i + 2];
+      bo.execId = ro.execId = 0;
+      bo.recordPipeline = ro.recordPipeline = 0;
+      runGemmBiasRelu(step, bo, ro);
+      i += 2;
+      continue;
+    }
     switch (step.opcode) {
       case OpCode::Gemm:
         runGemm(step, false);
@@ -2143,6 +2162,91 @@ void Session::replay(std::uint64_t pipelineId, bool sync) {
     }
   }
   if (sync) synchronize();
+}
+
+bool Session::fusableBiasRelu(const std::vector<OpDescriptor>& ops, std::size_t i) const {
+  static const bool enabled = [] {
+    const char* e = std::getenv("GM_FUSE_EPILOGUE");
+    return !(e && e[0] == '0');
+  }();
+  if (!enabled || i + 2 >= ops.size()) return false;
+  const OpDescriptor& g = ops[i];
+  const OpDescriptor& bo = ops[i + 1];
+  const OpDescriptor& ro = ops[i + 2];
+  if (g.opcode != OpCode::Gemm || bo.opcode != OpCode::EwBinary || ro.opcode != OpCode::EwUnary) return false;
+  if (bo.flags[0] != static_cast<std::uint8_t>(BinaryKind::BiasAdd) ||
+      ro.flags[0] != static_cast<std::uint8_t>(UnaryKind::Relu))
+    return false;
+  const std::uint64_t a = g.ids[0], b = g.ids[1], c = g.ids[2], bias = bo.ids[1], act = ro.ids[1];
+  if (bo.ids[0] != c || bo.ids[2] != c || ro.ids[0] != c) return false;
+  if (act == c || act == a || act == b || act == bias || bias == c) return false;
+  if (g.s0 == 0.0 || g.s1 != 0.0 || g.flags[3] != 0) return false;
+  for (std::uint64_t id : {a, b, c, bias, act})
+    if (!table_.count(id) || table_.at(id).precision != Precision::BF16) return false;
+  const MatrixDescriptor& C = table_.at(c);
+  const MatrixDescriptor& Bv = table_.at(bias);
+  const MatrixDescriptor& Act = table_.at(act);
+  const std::uint64_t k = g.flags[0] ? table_.at(a).rows : table_.at(a).cols;
+  if (k == 0 || C.rows == 0 || C.cols == 0) return false;
+  if (Bv.rows != 1 || Bv.cols != C.cols || Act.rows != C.rows || Act.cols != C.cols) return false;
+  if (!(Act.layout == C.layout)) return false;
+  // The bias columns of every C tile must be readable in place on its owner
+  // (a fresh replica, or a bias tile the owner holds): no transfer is needed.
+  if (Bv.replicaFresh()) return true;
+  for (const auto& tl : C.layout.tiles) {
+    const Rect need{0, 1, tl.first.colStart, tl.first.colEnd()};
+    bool own = false;
+    for (const auto& bt : Bv.layout.tiles)
+      if (bt.second.rank == tl.second.rank && need.inside(Rect::ofExtent(bt.first))) own = true;
+    if (!own) return false;
+  }
+  return true;
+}
+
+void Session::runGemmBiasRelu(const OpDescriptor& g0, const OpDescriptor& bo0, const OpDescriptor& ro0) {
+  OpDescriptor g = g0, bo = bo0, ro = ro0;
+  const std::uint64_t c = g.ids[2], bias = bo.ids[1], act = ro.ids[1];
+  forEachLocal([&](Worker& w) {
+    w.joinUpload(bias);
+    w.joinUpload(act);
+  });
+  // Bias views (fusableBiasRelu guarantees no transfer and no scratch).
+  std::vector<ReadNeed> needs;
+  std::vector<std::tuple<std::uint32_t, std::uint64_t, std::uint64_t>> keys;
+  for (const auto& tl : lookup(table_, c).layout.tiles) {
+    needs.push_back({tl.second.rank, bias, Rect{0, 1, tl.first.colStart, tl.first.colEnd()}, {}});
+    keys.emplace_back(tl.second.rank, tl.first.rowStart, tl.first.colStart);
+  }
+  std::vector<Xfer> xs;
+  std::vector<std::pair<Worker*, void*>> temps;
+  resolveReads(needs, c, xs, temps);
+  if (!xs.empty() || !temps.empty()) throw Error("fused gemm/biasAdd/relu: bias not readable in place");
+  FusedBiasRelu f;
+  f.act = act;
+  for (std::size_t i = 0; i < needs.size(); ++i)
+    if (isLocal(needs[i].worker)) f.bias[keys[i]] = needs[i].view.ptr;
+  // relu's write of act moves into the GEMM: its earlier readers finish first.
+  forEachLocal([&](Worker& w) {
+    if (!w.tiles.count(act)) return;
+    w.beforeMutation(act, w.compute);
+    auto rr = remoteReaders_.find(act);
+    if (rr != remoteReaders_.end())
+      for (const auto& rd : rr->second)
+        ipcWait(w.compute, peerFlags_[rd.first.first] + kSlots * (1 + rd.first.second) + slotOf(act), rd.second);
+  });
+  issue(g);
+  fused_ = &f;
+  try {
+    execGemm(g);
+  } catch (...) {
+    fused_ = nullptr;
+    throw;
+  }
+  fused_ = nullptr;
+  // The bias and relu ops' metadata (versions, replica / cache invalidation,
+  // publication of their writes) as if they had run after the GEMM.
+  issue(bo);
+  issue(ro);
 }
 
 // ---------------------------------------------------------------- replication

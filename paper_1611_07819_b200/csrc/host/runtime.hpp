@@ -345,6 +345,16 @@ class Session {
   // Issues a Gemm op (gemm() below wraps it). sync: wait for completion
   // like the reference's acked gemm(); otherwise stream-ordered only.
   void runGemm(const OpDescriptor& op, bool sync);
+  // Replay peephole: gemm(C) -> biasAdd(C, b) -> relu(C -> act), all bf16,
+  // runs as one GEMM whose epilogue adds the bias and writes act (the three
+  // ops' metadata, versions and hazards are applied as if run one by one).
+  struct FusedBiasRelu {
+    std::uint64_t act = 0;
+    std::map<std::tuple<std::uint32_t, std::uint64_t, std::uint64_t>, const void*> bias;  // (rank, row0, col0)
+  };
+  const FusedBiasRelu* fused_ = nullptr;
+  bool fusableBiasRelu(const std::vector<OpDescriptor>& ops, std::size_t i) const;
+  void runGemmBiasRelu(const OpDescriptor& g, const OpDescriptor& bo, const OpDescriptor& ro);
   // FC-layer neighbours on device (reference session.cpp:547-609,
   // kernels.cpp:435-815): SetConst, EwUnary, EwBinary, AddRowColSum.
   // Same sync contract as runGemm.

@@ -11,10 +11,8 @@ from paper_1611_07819_b200 import gridmath as G
 pytestmark = pytest.mark.gpu
 
 
-def build(s, p):
+def build(s, p, S=G.Precision.Single, batch=192, fin=256, fout=160):
     grp = list(range(p))
-    S = G.Precision.Single
-    batch, fin, fout = 192, 256, 160
     m = dict(
         X=s.createMatrix(batch, fin, S, G.makeRowBlockLayout(batch, fin, grp)),
         W=s.createMatrix(fin, fout, S, G.makeColBlockLayout(fin, fout, grp)),
@@ -56,11 +54,21 @@ def snapshot(s, m):
     return {k: (s.getDataRaw(v), v.version()) for k, v in m.items()}
 
 
-@pytest.mark.parametrize("p", [1, 4])
-def test_replay_equals_eager(p):
+@pytest.mark.parametrize("p,prec,shape", [
+    (1, G.Precision.Single, (192, 256, 160)),
+    (4, G.Precision.Single, (192, 256, 160)),
+    # bf16: replay runs gemm -> biasAdd -> relu as one GEMM with the fused
+    # epilogue; eager runs the three ops. Bitwise equal either way.
+    (1, G.Precision.BF16, (192, 256, 160)),
+    (4, G.Precision.BF16, (192, 256, 160)),
+    (2, G.Precision.BF16, (200, 96, 136)),
+    (3, G.Precision.BF16, (515, 320, 1000)),
+])
+def test_replay_equals_eager(p, prec, shape):
     k = 3
+    batch, fin, fout = shape
     with G.Session(workers=p) as s:
-        m = build(s, p)
+        m = build(s, p, prec, batch, fin, fout)
         pid = s.beginRecord()
         step(s, m)
         s.endRecord()
@@ -69,7 +77,7 @@ def test_replay_equals_eager(p):
         s.verifyMetadataConsistency()
         got = snapshot(s, m)
     with G.Session(workers=p) as s:
-        m = build(s, p)
+        m = build(s, p, prec, batch, fin, fout)
         for _ in range(k + 1):
             step(s, m)
         want = snapshot(s, m)
@@ -115,3 +123,61 @@ def test_recording_errors_like_reference():
         G.setConst(s, m["R"], 0.0)
         s.replay(pid)
         assert np.all(s.getDataRaw(m["R"]) == np.float32(2.5))
+
+
+def test_replay_fuses_bias_relu_into_the_gemm():
+    # The bf16 step's replay launches two kernels fewer than the eager step
+    # (biasAdd and relu ride in the forward GEMM's epilogue); Single does not fuse.
+    counts = {}
+    for prec in (G.Precision.BF16, G.Precision.Single):
+        with G.Session(workers=1) as s:
+            m = build(s, 1, prec)
+            pid = s.beginRecord()
+            step(s, m)
+            s.endRecord()
+            s.synchronize()
+            n0 = G.kernel_launches()
+            step(s, m)
+            s.synchronize()
+            n1 = G.kernel_launches()
+            s.replay(pid)
+            n2 = G.kernel_launches()
+            counts[prec] = (n1 - n0, n2 - n1)
+    eager, replayed = counts[G.Precision.BF16]
+    assert replayed == eager - 2, counts
+    eager, replayed = counts[G.Precision.Single]
+    assert replayed == eager, counts
+
+
+def test_fused_epilogue_not_used_when_bias_needs_a_transfer():
+    # Z row-block over 2 workers, bias col-block and not replicated: each
+    # worker's Z tile needs bias columns the other owns, so replay keeps the
+    # three ops (and still matches eager).
+    def run(record):
+        with G.Session(workers=2) as s:
+            P = G.Precision.BF16
+            grp = [0, 1]
+            X = s.createMatrix(64, 96, P, G.makeRowBlockLayout(64, 96, grp))
+            W = s.createMatrix(96, 80, P, G.makeColBlockLayout(96, 80, grp))
+            B = s.createMatrix(1, 80, P, G.makeColBlockLayout(1, 80, grp))
+            Z = s.createMatrix(64, 80, P, G.makeRowBlockLayout(64, 80, grp))
+            A = s.createMatrix(64, 80, P, G.makeRowBlockLayout(64, 80, grp))
+            s.fillUniform(X, 1)
+            s.fillUniform(W, 2)
+            s.fillUniform(B, 3)
+            def fwd():
+                G.gemm(s, X, W, Z, 1.0, 0.0)
+                G.biasAdd(s, Z, B)
+                G.relu(s, Z, A)
+            if record:
+                pid = s.beginRecord()
+                fwd()
+                s.endRecord()
+                s.replay(pid)
+            else:
+                fwd()
+                fwd()
+            return s.getDataRaw(Z), s.getDataRaw(A), Z.version(), A.version()
+    got, want = run(True), run(False)
+    for g, w in zip(got, want):
+        assert np.array_equal(np.asarray(g), np.asarray(w))

@@ -154,14 +154,16 @@ def run(transport, nccl_id):
             ok = ok and good
         # FC train step (reference Trainer order) recorded once and replayed,
         # vs the same pipeline on one process with `world` workers on one GPU
-        fc = fc_steps(s, 3)
-        if rank == 0:
-            with G.Session(workers=world, devices=[local]) as s1:
-                ref = fc_steps(s1, 3)
-            good = all(np.array_equal(fc[k].view(np.uint8), ref[k].view(np.uint8)) for k in fc)
-            say(f"[rank0 {plane}] FC step record/replay (gemm, biasAdd, relu, reluGrad, rowcolsum, axpy, "
-                f"replication) bitwise_vs_1process={good}")
-            ok = ok and good
+        # (bf16: the replay runs gemm -> biasAdd -> relu as one fused GEMM on every rank)
+        for fprec in (G.Precision.Single, G.Precision.BF16):
+            fc = fc_steps(s, 3, fprec)
+            if rank == 0:
+                with G.Session(workers=world, devices=[local]) as s1:
+                    ref = fc_steps(s1, 3, fprec)
+                good = all(np.array_equal(fc[k].view(np.uint8), ref[k].view(np.uint8)) for k in fc)
+                say(f"[rank0 {plane}] FC step {fprec.name} record/replay (gemm, biasAdd, relu, reluGrad, rowcolsum, "
+                    f"axpy, replication) bitwise_vs_1process={good}")
+                ok = ok and good
         # chunked async host streaming: upload A/B, gemm, download C
         n = 1024
         lay = G.makeGridLayout(n, n, pr, pc, g)
@@ -218,8 +220,7 @@ def _fresh_id():
     return obj[0]
 
 
-def fc_steps(s, steps):
-    S = G.Precision.Single
+def fc_steps(s, steps, S=G.Precision.Single):
     batch, fin, fout = 256, 384, 192
     M = dict(X=(batch, fin, G.makeRowBlockLayout), W=(fin, fout, G.makeColBlockLayout),
              B=(1, fout, G.makeColBlockLayout), Z=(batch, fout, G.makeRowBlockLayout),
