@@ -181,3 +181,49 @@ def test_fused_epilogue_not_used_when_bias_needs_a_transfer():
     got, want = run(True), run(False)
     for g, w in zip(got, want):
         assert np.array_equal(np.asarray(g), np.asarray(w))
+
+
+@pytest.mark.parametrize("p,batch,fin,fout", [(2, 128, 192, 256), (3, 100, 64, 264)])
+def test_fused_epilogue_on_column_blocks(p, batch, fin, fout):
+    # Z / act / bias column blocks with the same split: every worker holds the
+    # bias columns of its Z tile, so each worker's GEMM carries the epilogue.
+    def run(record):
+        with G.Session(workers=p) as s:
+            P = G.Precision.BF16
+            grp = list(range(p))
+            X = s.createMatrix(batch, fin, P, G.makeSingleTileLayout(batch, fin, 0))
+            W = s.createMatrix(fin, fout, P, G.makeColBlockLayout(fin, fout, grp))
+            B = s.createMatrix(1, fout, P, G.makeColBlockLayout(1, fout, grp))
+            Z = s.createMatrix(batch, fout, P, G.makeColBlockLayout(batch, fout, grp))
+            A = s.createMatrix(batch, fout, P, G.makeColBlockLayout(batch, fout, grp))
+            s.fillUniform(X, 5)
+            s.fillUniform(W, 6, -0.2, 0.2)
+            s.fillUniform(B, 7, -0.3, 0.3)
+
+            def fwd():
+                G.gemm(s, X, W, Z, 1.0, 0.0)
+                G.biasAdd(s, Z, B)
+                G.relu(s, Z, A)
+            s.synchronize()
+            n0 = G.kernel_launches()
+            if record:
+                pid = s.beginRecord()
+                fwd()
+                s.endRecord()
+                s.synchronize()
+                n0 = G.kernel_launches()
+                s.replay(pid)
+            else:
+                fwd()
+                s.synchronize()
+                n0 = G.kernel_launches()
+                fwd()
+            s.synchronize()
+            n = G.kernel_launches() - n0
+            return [s.getDataRaw(Z), s.getDataRaw(A), Z.version(), A.version()], n
+    (got, n_rep), (want, n_eager) = run(True), run(False)
+    for g, w in zip(got, want):
+        assert np.array_equal(np.asarray(g), np.asarray(w))
+    assert n_rep == n_eager - 2 * p, (n_rep, n_eager)
+    a = got[1].view(np.uint16)
+    assert (a != 0).any() and not (a & 0x8000).any()  # relu output: non-trivial, no negatives
