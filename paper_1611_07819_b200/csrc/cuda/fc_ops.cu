@@ -220,7 +220,10 @@ __global__ void __launch_bounds__(kLsThreads) line_sums_kernel(EwView a, uint64_
 //   by cols: stage = 128 rows x 32 elements (lane o reads column o).
 // Zero padding is exact: a chain that starts at +0 never holds -0, so adding
 // +0 leaves it unchanged.
-constexpr int kAsStep = 128, kAsThreads = 128;
+constexpr int kAsThreads = 128;
+// Elements per chain per stage: 256 for 16-bit storage (one barrier per 256
+// folds; 6 x 16.5 KB ring, two CTAs per SM), 128 for wider elements.
+constexpr int as_step(int elem_bytes) { return elem_bytes <= 2 ? 256 : 128; }
 // Ring depth: the folding warp eats a chunk in ~512 cycles, so keep ~5 chunks
 // in flight to cover HBM latency (4 for 8-byte elements: smem).
 constexpr int as_stages(int elem_bytes) { return elem_bytes >= 8 ? 4 : 6; }
@@ -242,6 +245,7 @@ __global__ void __launch_bounds__(kAsThreads) line_sums_async_kernel(const void*
   using S = typename Stor<P>::type;
   constexpr int E = sizeof(S), VE = 16 / E;
   constexpr int kAsStages = as_stages(E);
+  constexpr int kAsStep = as_step(E);
   constexpr int kPitchR = kAsStep * E + 16, kStageR = 32 * kPitchR;
   constexpr int kPitchC = 32 * E, kStageC = kAsStep * kPitchC;
   constexpr int kStage = kStageR > kStageC ? kStageR : kStageC;
@@ -253,12 +257,22 @@ __global__ void __launch_bounds__(kAsThreads) line_sums_async_kernel(const void*
   const uint64_t nchunks = (len + kAsStep - 1) / kAsStep;
   const unsigned char* ab = static_cast<const unsigned char*>(a);
   const int tid = threadIdx.x;
+  // The folding warp: row-sum CTAs use warp 0, column-sum CTAs warp 2. The
+  // two directions run concurrently (two streams) and share SMs, so their
+  // folding warps sit on different SM sub-partitions instead of contending
+  // for one scheduler's issue slots.
+  const int fw = by_rows ? 0 : 2;
+  const bool folder = (tid >> 5) == fw;
+  const int lane = tid & 31;
 
   auto issue = [&](uint64_t chunk) {
     const uint32_t st = ring_s + static_cast<uint32_t>((chunk % kAsStages) * kStage);
     const uint64_t s0 = chunk * kAsStep;
     constexpr int kVecs = 32 * kAsStep / VE;  // 16-byte copies per stage
-    for (int q = tid; q < kVecs; q += kAsThreads) {
+    // The three other warps copy; the folding warp only folds.
+    if (folder) return;
+    const int ptid = tid - (tid >= fw * 32 ? 32 : 0);
+    for (int q = ptid; q < kVecs; q += kAsThreads - 32) {
       uint64_t r, c;
       uint32_t soff;
       if (by_rows) {
@@ -295,10 +309,10 @@ __global__ void __launch_bounds__(kAsThreads) line_sums_async_kernel(const void*
     __syncthreads();
     if (i + kAsStages - 1 < nchunks) issue(i + kAsStages - 1);
     cp_async_commit();
-    if (tid < 32) {
+    if (folder) {
       const unsigned char* st = ring + (i % kAsStages) * kStage;
       if (by_rows) {
-        const unsigned char* row = st + tid * kPitchR;
+        const unsigned char* row = st + lane * kPitchR;
 #pragma unroll 4
         for (int v = 0; v < kAsStep / VE; ++v) {
           union {
@@ -310,15 +324,15 @@ __global__ void __launch_bounds__(kAsThreads) line_sums_async_kernel(const void*
           for (int k = 0; k < VE; ++k) sum = add_rn(sum, widen<P, T>(w.e[k]));
         }
       } else {
-        const S* col = reinterpret_cast<const S*>(st) + tid;
+        const S* col = reinterpret_cast<const S*>(st) + lane;
 #pragma unroll 16
         for (int sr = 0; sr < kAsStep; ++sr) sum = add_rn(sum, widen<P, T>(col[sr * 32]));
       }
     }
   }
   cp_async_wait<0>();
-  if (tid < 32 && o0 + tid < outs) {
-    const uint64_t idx = (o0 + tid) * acc_stride;
+  if (folder && o0 + lane < outs) {
+    const uint64_t idx = (o0 + lane) * acc_stride;
     const T cur = load_as<T>(acc, acc_prec, idx);
     store_as(acc, acc_prec, idx, add_rn(cur, mul_rn(alpha, sum)));
   }
@@ -329,6 +343,7 @@ cudaError_t launch_sums_async(EwView band, uint64_t rows, uint64_t cols, int by_
                               uint64_t acc_stride, int acc_prec, T alpha, cudaStream_t s) {
   using S = typename Stor<P>::type;
   constexpr int E = sizeof(S);
+  constexpr int kAsStep = as_step(E);
   constexpr int kStageR = 32 * (kAsStep * E + 16), kStageC = kAsStep * 32 * E;
   constexpr size_t smem = static_cast<size_t>(as_stages(E)) * (kStageR > kStageC ? kStageR : kStageC);
   // Per device (the attribute lives in each device's context).
