@@ -237,6 +237,30 @@ def test_row_col_sums_vs_c_restatement(prec, lay):
         assert same_bits(got_r, want_r, prec) and same_bits(got_c, want_c, prec), (prec, lay, det)
 
 
+@pytest.mark.parametrize("prec", [3, 1])
+@pytest.mark.parametrize("shape", [(600, 1000), (4096, 264), (33, 4104)])
+def test_row_col_sums_aligned_rows_vs_c_restatement(prec, shape):
+    """16-byte aligned rows take the cp.async ring (256-element stages for
+    16-bit storage, 128 for Single): chains that end mid-stage and output
+    counts that are not multiples of 32, bit-for-bit."""
+    rows, cols = shape
+    a = O.fill_uniform(rows, cols, prec, 41).reshape(rows, cols)
+    r = O.fill_uniform(rows, 1, prec, 42).reshape(rows, 1)
+    c = O.fill_uniform(1, cols, prec, 43).reshape(1, cols)
+    want_r, want_c = O.rowcolsum_c(1.0, a, prec, r, prec, c, prec)
+    with G.Session(workers=1) as s:
+        one = lambda rr, cc: G.makeSingleTileLayout(rr, cc, 0)
+        A = s.createMatrix(rows, cols, G.Precision(prec), one(rows, cols))
+        R = s.createMatrix(rows, 1, G.Precision(prec), one(rows, 1))
+        C = s.createMatrix(1, cols, G.Precision(prec), one(1, cols))
+        for M, img in ((A, a), (R, r), (C, c)):
+            s.setDataRaw(M, img)
+        G.addRowColSum(s, A, R, C, 1.0, True)
+        got_r = s.getDataRaw(R).reshape(rows, 1)
+        got_c = s.getDataRaw(C).reshape(1, cols)
+    assert same_bits(got_r, want_r, prec) and same_bits(got_c, want_c, prec), (prec, shape)
+
+
 @pytest.mark.parametrize("prec,value", [(0, 65520.0), (1, 1.0 / 3.0), (2, np.pi), (3, -1.0 / 3.0), (3, 1e39)])
 def test_set_const(prec, value):
     rows, cols, p = 130, 77, 3
