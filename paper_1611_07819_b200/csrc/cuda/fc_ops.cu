@@ -313,7 +313,7 @@ __global__ void __launch_bounds__(kAsThreads) line_sums_async_kernel(const void*
       const unsigned char* st = ring + (i % kAsStages) * kStage;
       if (by_rows) {
         const unsigned char* row = st + lane * kPitchR;
-#pragma unroll 4
+#pragma unroll 16
         for (int v = 0; v < kAsStep / VE; ++v) {
           union {
             uint4 u;
@@ -325,7 +325,7 @@ __global__ void __launch_bounds__(kAsThreads) line_sums_async_kernel(const void*
         }
       } else {
         const S* col = reinterpret_cast<const S*>(st) + lane;
-#pragma unroll 16
+#pragma unroll 64
         for (int sr = 0; sr < kAsStep; ++sr) sum = add_rn(sum, widen<P, T>(col[sr * 32]));
       }
     }
