@@ -245,6 +245,10 @@ def run_reference(args):
 
 # ------------------------------------------------------------------ our arm
 
+def flops_of(n):
+    return 2.0 * n ** 3
+
+
 def run_ours(args):
     import numpy as np
     import torch
@@ -288,6 +292,17 @@ def run_ours(args):
         s.gemmAsync(A, B, C)
     barrier()
 
+    nvl = None
+    if world > 1:
+        try:
+            sys.path.insert(0, os.path.join(ROOT, "tools"))
+            from nvlink_counters import NvlinkCounters
+            nvl = NvlinkCounters(local)
+            nvl.read()
+        except Exception as exc:  # reported, never fatal
+            nvl = str(exc)
+    st_a = s.queryWorkerStats()[0]
+    nv_a = nvl.read() if not isinstance(nvl, (str, type(None))) else None
     launches0 = G.kernel_launches()
     t_start = time.time()
     s.timerStart()
@@ -295,6 +310,8 @@ def run_ours(args):
         s.gemmAsync(A, B, C)
     ms = s.timerStop()
     t_end = time.time()
+    nv_b = nvl.read() if nv_a is not None else None
+    st_b = s.queryWorkerStats()[0]
     clk = clocks.stop(t_start, t_end)
     launches = G.kernel_launches() - launches0
     # Average GEMM-kernel (compute phase) time per launch over the timed
@@ -305,8 +322,33 @@ def run_ours(args):
     kernel_ms_max = allreduce_max(dist, kernel_ms)
     launches_total = int(allreduce_sum(dist, launches))
 
-    flops = 2.0 * n ** 3
+    flops = flops_of(n)
     value = flops * args.steps / (ms_max / 1e3) / 1e12
+
+    # ---- dependent chain: step i's A is step i-1's C (A_i = a C_{i-1} B,
+    # a = 1/(sigma_B sqrt(k)) keeps the values bounded over the run), so no
+    # A panel can move before the previous GEMM finished; only the in-GEMM
+    # panel pipelining can hide the exchange.
+    dependent = None
+    if args.dependent_steps > 0:
+        alpha = 1.0 / (math.sqrt(1.0 / 3.0) * math.sqrt(n))
+        pair = [A, C]
+        for i in range(3):
+            s.gemmAsync(pair[i % 2], B, pair[(i + 1) % 2], alpha, 0.0)
+        barrier()
+        s.timerStart()
+        for i in range(args.dependent_steps):
+            s.gemmAsync(pair[(i + 1) % 2], B, pair[i % 2], alpha, 0.0)
+        dms = s.timerStop()
+        dk = max(tot / cnt for tot, cnt in s.timerKernelMs() if cnt)
+        barrier()
+        dms_max = allreduce_max(dist, dms)
+        dk_max = allreduce_max(dist, dk)
+        dependent = {"value": round(flops_of(n) * args.dependent_steps / (dms_max / 1e3) / 1e12, 3), "unit": "TFLOP/s",
+                     "ms_per_step": round(dms_max / args.dependent_steps, 4), "steps": args.dependent_steps,
+                     "kernel_ms_per_gemm": round(dk_max, 4),
+                     "chain": "A_i = alpha * C_{i-1} . B (A and C alternate), B fixed; every step's A panels are the "
+                              "previous step's output"}
 
     # ---- panel exchange bandwidth: one isolated op (no overlap with a GEMM)
     nvlink = None
@@ -322,10 +364,26 @@ def run_ours(args):
         recv_max = allreduce_max(dist, float(recv))
         barrier()
         peaks, _ = measured_peaks()
+        # Counter evidence over the timed loop: NVML NVLink RX bytes on this
+        # rank's GPU next to the bytes the planner pulled (remote pieces).
+        plan_rx = (st_b["bytes_received"] - st_a["bytes_received"]) / args.steps
+        counters = None
+        if nv_a is not None and nv_b is not None:
+            rx_step = (nv_b[1] - nv_a[1]) / args.steps
+            tx_step = (nv_b[0] - nv_a[0]) / args.steps
+            rx_max = allreduce_max(dist, rx_step)
+            counters = {"rx_bytes_per_step_max_rank": int(rx_max), "rx_bytes_per_step_rank0": int(rx_step),
+                        "tx_bytes_per_step_rank0": int(tx_step),
+                        "rx_over_planned_rank0": round(rx_step / plan_rx, 4) if plan_rx else None,
+                        "avg_rx_gbs_over_step": round(rx_max / (ms_max / args.steps / 1e3) / 1e9, 1),
+                        "source": nvl.describe()["source"], "links": nvl.describe()["links"]}
+        elif isinstance(nvl, str):
+            counters = {"unavailable": nvl}
         nvlink = {"plane": s.transport(), "bytes_received_per_gpu": int(recv_max), "exchange_ms": round(comm_ms_max, 4),
                   "achieved_gbs": round(recv_max / (comm_ms_max / 1e3) / 1e9, 1) if comm_ms_max > 0 else None,
+                  "planned_rx_bytes_per_step_rank0": int(plan_rx), "counters": counters,
                   "peak_gbs": 770.0, "peak_kind": "B200_PROFILING.md measured peer copy per direction (900 nominal)",
-                  "note": "isolated op (exchange not overlapped); in the timed loop the exchange overlaps the previous GEMM",
+                  "note": "exchange_ms/achieved_gbs: one isolated op (exchange not overlapped); counters: the timed loop",
                   "compute_ms_per_step": round(kernel_ms_max, 4)}
 
     # ---- e2e through the public API from pinned host buffers
@@ -395,12 +453,17 @@ def run_ours(args):
         achieved = local_flops / (kernel_ms_max / 1e3) / 1e12
         peak = float(peaks.get("bf16_tflops_sustained", 1412.3))
         traffic = None
+        traffic_src = None
         tpath = os.path.join(ROOT, "profiles", "traffic.json")
         if os.path.exists(tpath):
             try:
-                traffic = json.load(open(tpath)).get(f"bf16_{n}_n{world}")
+                tj = json.load(open(tpath))
+                traffic = tj.get(f"bf16_{n}_n{world}")
+                traffic_src = tj.get("_provenance", "profiled constant (profiles/traffic.json)")
             except Exception:
                 traffic = None
+        run_mhz = clk.get("sm_mhz")
+        peak_mhz = (peaks.get("clocks_under_load") or {}).get("sm_mhz_median")
         line = {
             "metric": METRIC, "value": round(value, 3), "unit": "TFLOP/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(ms_max / args.steps, 4), "higher_is_better": True,
@@ -415,6 +478,10 @@ def run_ours(args):
             "e2e": e2e,
             "roofline": {"bound": "tensor", "achieved": round(achieved, 1), "peak": peak, "unit": "TFLOP/s",
                          "frac": round(achieved / peak, 4), "traffic": traffic,
+                         "traffic_source": traffic_src,
+                         "frac_clock_normalised": round((achieved / run_mhz) / (peak / peak_mhz), 4)
+                         if run_mhz and peak_mhz else None,
+                         "clock_normalisation": "achieved/run SM MHz over peak/peak-measurement SM MHz (both medians under load)",
                          "peak_kind": f"{peak_kind} bf16_tflops_sustained (cuBLAS, long loop)",
                          "peak_sm_mhz": (peaks.get("clocks_under_load") or {}).get("sm_mhz_median"),
                          "frac_of_burst_peak": round(achieved / float(peaks.get("bf16_tflops", 1657.1)), 4),
@@ -424,6 +491,7 @@ def run_ours(args):
             "clocks": clk,
             "gpu_launches": launches_total,
             "nvlink": nvlink,
+            "dependent": dependent,
             **extra,
         }
         if numa:
@@ -511,13 +579,25 @@ def run_extra_config(args):
         s.endRecord()
 
         def step(i):
-            s.fillUniform(DL, 1000 + i)                            # upstream gradient dAct (synthetic)
+            # A new batch every step (the Trainer uploads one, dnn.cpp:132-141):
+            # X and the upstream gradient dAct change, so the dW GEMM's X band
+            # is gathered again every step (never served from the panel cache).
+            s.fillUniform(X, 2000 + i)
+            s.fillUniform(DL, 1000 + i)
             s.replay(pid, sync=False)
 
         flops = 3 * 2.0 * batch * fi * fo
-        workload = (f"FC train step {args.fc_dtype} batch {batch}, {fi}->{fo}: fwd (gemm, biasAdd, relu), bwd (reluGrad, "
-                    "dW gemm, addRowColSum, dX gemm), SGD axpy, W/b re-replication; W col-block + replicated, "
-                    "X row-block; value counts the 3 GEMMs' flops")
+        eb = 4 if args.fc_dtype == "f32" else 2
+        # Per GPU per step (rank 0's share): W and b re-replication ((P-1)/P
+        # of each) + the dW GEMM's gathered bands: all of X (dW is
+        # column-block, so every rank needs every row of X^T: the other
+        # ranks' (P-1)/P of the batch) and delta's column band (the other
+        # ranks' rows of batch x fo/P). dX and the forward read W's replica.
+        expected_rx = int(((world - 1) * (fi * fo + fo) // world + (world - 1) * batch // world * fi
+                           + (world - 1) * batch // world * (fo // world)) * eb) if world > 1 else 0
+        workload = (f"FC train step {args.fc_dtype} batch {batch}, {fi}->{fo}: new X and dAct every step, fwd (gemm, "
+                    "biasAdd, relu), bwd (reluGrad, dW gemm, addRowColSum, dX gemm), SGD axpy, W/b re-replication; "
+                    "W col-block + replicated, X row-block; value counts the 3 GEMMs' flops")
     else:
         n = 16384 if args.n == 32768 else args.n
         pr, pc = grid_for(world)
@@ -531,6 +611,7 @@ def run_extra_config(args):
         def step(i):
             s.gemmAsync(A, B, C)
 
+        expected_rx = None
         flops = 2.0 * n ** 3
         workload = f"fp64 GEMM {n}^3 (DMMA) on a {pr}x{pc} grid"
     for i in range(args.warmup):
@@ -538,6 +619,7 @@ def run_extra_config(args):
     s.synchronize()
     if dist is not None:
         dist.barrier()
+    st0 = s.queryWorkerStats()[0]
     s.timerStart()
     th0 = time.perf_counter()
     for i in range(args.steps):
@@ -545,11 +627,15 @@ def run_extra_config(args):
     host_ms = (time.perf_counter() - th0) * 1e3 / args.steps  # host issue time per step (async)
     ms = allreduce_max(dist, s.timerStop())
     st = s.queryWorkerStats()
+    rx = (st[0]["bytes_received"] - st0["bytes_received"]) / args.steps
+    rx_max = allreduce_max(dist, rx)
     if rank == 0:
         print(json.dumps({"metric": METRIC, "config": {"workload": workload}, "n_gpus": world,
                           "value": round(flops * args.steps / (ms / 1e3) / 1e12, 3), "unit": "TFLOP/s",
                           "ms_per_step": round(ms / args.steps, 4), "host_issue_ms_per_step": round(host_ms, 4),
                           "steps": args.steps, "warmup": args.warmup,
+                          "bytes_received_per_step": {"rank0": int(rx), "max_rank": int(rx_max),
+                                                      "expected": expected_rx},
                           "worker0_stats": st[0]}), flush=True)
     s.close()
     if dist is not None:
@@ -564,6 +650,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--size", dest="n", type=int, default=32768)
     ap.add_argument("--e2e-steps", type=int, default=6)
+    ap.add_argument("--dependent-steps", type=int, default=10,
+                    help="also time a dependent chain (A_i = C_{i-1}); 0 = skip")
     ap.add_argument("--gemm-max-ctas", type=int, default=0)
     ap.add_argument("--pipeline-chunks", type=int, default=0)
     ap.add_argument("--transport", type=int, default=0, help="0 auto (IPC copy engines), 1 NCCL")

@@ -196,6 +196,14 @@ typedef struct {
   int32_t transport;                /* 0 = auto, 1 = NCCL, 2 = copy engines (IPC pulls under SPMD) */
   uint64_t panel_cache_bytes;       /* per-worker panel cache budget; 0 = 1/4 of HBM, 1 = off */
   int32_t pipeline_chunks;          /* SUMMA overlap chunks per band (0 = auto, 1 = off) */
+  /* SPMD control channel. NULL: an NCCL communicator (bootstrapped from
+   * nccl_unique_id) carries the few blocking control collectives. Non-NULL:
+   * the host calls this instead -- a max-reduce of `bytes` host bytes over
+   * every rank, in place, blocking, returning 0 on success (e.g. a gloo
+   * all_reduce) -- and no NCCL communicator is created, so several ranks may
+   * share one GPU; the data plane is then the copy-engine (IPC) plane. */
+  int (*control_allreduce_max_u8)(void* buf, uint64_t bytes, void* user);
+  void* control_user;
 } gm_session_options;
 
 void gm_session_options_default(gm_session_options* o);

@@ -50,7 +50,8 @@ class gm_session_options(Structure):
                 ("num_devices", c_int32), ("devices", c_int32 * 16),
                 ("nccl_unique_id", c_uint8 * 128), ("arena_slab_bytes", c_uint64),
                 ("gemm_max_ctas", c_int32), ("transport", c_int32), ("panel_cache_bytes", c_uint64),
-                ("pipeline_chunks", c_int32)]
+                ("pipeline_chunks", c_int32), ("control_allreduce_max_u8", c_void_p),
+                ("control_user", c_void_p)]
 
 
 class gm_worker_stats(Structure):

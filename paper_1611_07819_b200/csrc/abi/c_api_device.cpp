@@ -7,7 +7,6 @@
 #include "../host/core.hpp"
 #include "../host/device.hpp"
 #include "../cuda/convert.h"
-#include "../cuda/die_map.h"
 #include "abi_util.hpp"
 
 struct gm_arena {
@@ -168,19 +167,6 @@ int gm_layout_validate(uint64_t rows, uint64_t cols, const gm_tile* tiles, uint3
                                               tiles[i].col_start, tiles[i].col_count},
                          gridmath::WorkerId{tiles[i].owner}});
     *violation = static_cast<int32_t>(gridmath::validateLayout(rows, cols, l, worker_count).kind);
-  });
-}
-
-// Developer probe (not part of the documented ABI): SM -> die calibration.
-int gm_debug_die_map(int32_t device, uint64_t* die1_mask3, int32_t* die0_sms, int32_t* sms,
-                     int32_t* distance_max) {
-  return guard([&] {
-    gridmath::cudaCheck(cudaSetDevice(device), "cudaSetDevice");
-    const gmk::DieMap& m = gmk::die_map(device);
-    for (int i = 0; i < 3; ++i) die1_mask3[i] = m.die1_mask[i];
-    *die0_sms = m.valid ? m.die0_sms : -1;
-    *sms = m.sms;
-    *distance_max = m.distance_max;
   });
 }
 

@@ -93,6 +93,13 @@ gridmath::SessionOptions toOptions(const gm_session_options* o) {
   opts.transport = o->transport;
   opts.panelCacheBytes = o->panel_cache_bytes;
   opts.pipelineChunks = o->pipeline_chunks;
+  if (o->control_allreduce_max_u8) {
+    auto fn = o->control_allreduce_max_u8;
+    void* user = o->control_user;
+    opts.controlAllreduceMax = [fn, user](void* buf, std::size_t n) {
+      if (fn(buf, n, user) != 0) throw gridmath::Error("session: control channel all-reduce failed");
+    };
+  }
   return opts;
 }
 }  // namespace

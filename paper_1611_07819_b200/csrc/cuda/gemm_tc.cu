@@ -28,14 +28,16 @@
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
-#include <atomic>
 #include <cstdint>
 #include <cstring>
+#include <algorithm>
 #include <cstdio>
-#include <cstdlib>
+#include <map>
 #include <mutex>
+#include <utility>
 
 #include "convert.h"
+#include "debug_config.h"
 #include "gemm_tc.h"
 #include "ptx.cuh"
 
@@ -52,7 +54,7 @@ constexpr uint32_t kNumThreads = 192;  // 6 warps
 // (128 * kCG) x (256 * kChunks). kChunks = 2 fills all 512 TMEM columns with
 // one accumulator (no accumulator double-buffering); kChunks = 1 keeps two
 // accumulators so the epilogue of tile t overlaps the MMAs of tile t+1.
-template <int kCG, int kElemBytes, int kSplit, int kChunks, int kPairs = 1>
+template <int kCG, int kElemBytes, int kSplit, int kChunks>
 struct TcCfg {
   static constexpr uint32_t kBlockK = kSwizzleBytes / kElemBytes;
   static constexpr uint32_t kMmaK = 32 / kElemBytes;  // 16 (f16) or 8 (tf32)
@@ -68,9 +70,8 @@ struct TcCfg {
   // Epilogue staging for TMA stores: 4 warps x 2 buffers x (32 rows x 128 B).
   static constexpr uint32_t kStagingBytes = 4u * 2u * 4096u;
   static constexpr uint32_t kSmemBytes = kStages * kStageBytes + kStagingBytes + 1024 + 256;
-  static constexpr uint32_t kClusterCtas = kCG * kPairs;
+  static constexpr uint32_t kClusterCtas = kCG;
   static_assert(kAccStages * kChunks * kMmaN <= 512, "TMEM columns");
-  static_assert(kPairs == 1 || kCG == 2, "A multicast across pairs needs 2-SM pairs");
 };
 
 struct TcParams {
@@ -96,18 +97,27 @@ struct TcParams {
   uint64_t ld_act;
   uint32_t bias_vec, act_vec;           // 16-byte loads / stores legal
   uint32_t act_tma;                     // act written by TMA stores beside C's
+  // In-GEMM panel pipelining (the SUMMA exchange lands while the GEMM runs):
+  // ready.a[(chunk * num_panels + panel) * streams + s] >= ready.target once
+  // pull stream s has copied its pieces of A's (m-chunk, k-panel) block (B:
+  // n-chunks). The producer checks the blocks a k-block reads before it
+  // loads them. Null flag array: that operand is resident.
+  PanelReady ready;
 };
 
 // Lockstep: persistent CTA pairs run ~100 tiles back to back and drift apart,
 // after which pairs that share a panel no longer read it while it is in L2.
-// Every `sync_every` k-blocks the pair leader's producer checks in and waits
-// until all pairs reached the previous checkpoint. The wait is bounded
-// (~40 us) and a pair whose wait ever times out stops waiting for the rest of
-// the launch, so a pair that is not resident (SMs held by another kernel) or
-// a finished tail delays the others at most once and never blocks them.
-// Returns false on timeout.
-__device__ __forceinline__ bool lockstep(uint32_t* ctr, uint32_t checkpoint, uint32_t units) {
+// Every `sync_every` k-blocks the pair leader's producer checks in (always)
+// and, while waiting is enabled, waits until all pairs reached the previous
+// checkpoint. The wait is bounded (~40 us): a pair whose wait times out
+// stops waiting for the rest of its tile, and for the rest of the launch
+// after kMaxLockstepTimeouts timeouts -- so a pair that is not resident (SMs
+// held by another kernel), a finished tail, or pairs stalled on panel flags
+// delay the others boundedly and never block them. Returns false on timeout.
+constexpr uint32_t kMaxLockstepTimeouts = 4;
+__device__ __forceinline__ bool lockstep(uint32_t* ctr, uint32_t checkpoint, uint32_t units, bool wait) {
   atomicAdd(ctr, 1u);
+  if (!wait) return true;
   const uint32_t target = checkpoint * units;
   uint64_t t0;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
@@ -134,6 +144,24 @@ __device__ __forceinline__ void tile_coords(uint32_t t, const TcParams& p, uint3
   const uint32_t r = t % per_group;
   mb = first_m + r % gsize;
   nb = r / gsize;
+}
+
+// Waits until every pull stream published blocks [c0, c1] x {panel} of one
+// operand's flag array, then orders the generic-proxy acquire before the
+// async-proxy (TMA) reads of the landed bytes.
+__device__ __forceinline__ void wait_ready(const uint64_t* flags, uint32_t c0, uint32_t c1, uint32_t panel,
+                                           const PanelReady& r) {
+  for (uint32_t c = c0; c <= c1; ++c)
+    for (uint32_t s = 0; s < r.streams; ++s) {
+      const uint64_t* f = flags + (static_cast<uint64_t>(c) * r.num_panels + panel) * r.streams + s;
+      for (;;) {
+        uint64_t v;
+        asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(f) : "memory");
+        if (v >= r.target) break;
+        __nanosleep(256);
+      }
+    }
+  asm volatile("fence.proxy.async.global;" ::: "memory");
 }
 
 __device__ __forceinline__ float load_c(const TcParams& p, uint64_t off) {
@@ -248,18 +276,14 @@ __device__ __forceinline__ void store_row32(const TcParams& p, uint32_t row, uin
 }
 
 // kSplit: 3xTF32 (maps a_hi/a_lo, b_hi/b_lo). Otherwise a single pair.
-// kPairs = 2: a 4-CTA cluster holds two UMMA pairs that compute the same
-// M-block and adjacent N-blocks; each CTA fetches half of the A slab its
-// counterpart in the other pair also needs and multicasts it (A leaves L2 once
-// per cluster, and the two pairs stay in lockstep, so their A reuse holds).
-template <int kCG, int kElemBytes, int kSplit, int kChunks, int kPairs>
+template <int kCG, int kElemBytes, int kSplit, int kChunks>
 __global__ void __launch_bounds__(kNumThreads, 1)
     tc_gemm_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid_constant__ CUtensorMap tm_b,
                    const __grid_constant__ CUtensorMap tm_a_lo,
                    const __grid_constant__ CUtensorMap tm_b_lo,
                    const __grid_constant__ CUtensorMap tm_c,
                    const __grid_constant__ CUtensorMap tm_act, const TcParams p) {
-  using Cfg = TcCfg<kCG, kElemBytes, kSplit, kChunks, kPairs>;
+  using Cfg = TcCfg<kCG, kElemBytes, kSplit, kChunks>;
   constexpr uint32_t kStages = Cfg::kStages;
   constexpr uint32_t kBlockK = Cfg::kBlockK;
   constexpr uint32_t kMmaK = Cfg::kMmaK;
@@ -278,12 +302,9 @@ __global__ void __launch_bounds__(kNumThreads, 1)
 
   const uint32_t warp = warp_id_sync();
   const uint32_t lane = threadIdx.x & 31;
-  const uint32_t crank = (kCG == 2) ? cluster_ctarank() : 0;  // rank in cluster
-  const uint32_t rank = crank & (kCG - 1);                      // rank in the UMMA pair
-  const uint32_t pair = crank / kCG;                            // pair in the cluster
+  const uint32_t rank = (kCG == 2) ? cluster_ctarank() : 0;  // rank in the UMMA pair
   const bool leader = rank == 0;
-  const uint16_t pair_mask = static_cast<uint16_t>(((1u << kCG) - 1) << (pair * kCG));
-  const uint16_t all_mask = static_cast<uint16_t>((1u << Cfg::kClusterCtas) - 1);
+  const uint16_t pair_mask = static_cast<uint16_t>((1u << kCG) - 1);
 
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tm_a);
@@ -296,7 +317,7 @@ __global__ void __launch_bounds__(kNumThreads, 1)
     }
     for (uint32_t s = 0; s < kStages; ++s) {
       mbar_init(&full_bar[s], 1);
-      mbar_init(&empty_bar[s], kPairs);  // a commit from every pair that reads the slot
+      mbar_init(&empty_bar[s], 1);
     }
     for (uint32_t a = 0; a < kAcc; ++a) {
       mbar_init(&tfull_bar[a], 1);
@@ -313,10 +334,7 @@ __global__ void __launch_bounds__(kNumThreads, 1)
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
-  // Work units: (M-block, group of kPairs N-blocks); pair `pair` takes N-block
-  // nbu * kPairs + pair of the unit.
-  const uint32_t num_nbu = (p.num_n_blocks + kPairs - 1) / kPairs;
-  const uint32_t num_tiles = p.num_m_blocks * num_nbu;
+  const uint32_t num_tiles = p.num_m_blocks * p.num_n_blocks;
   const uint32_t num_kb = (p.k + kBlockK - 1) / kBlockK;
   // Fold mode (tf32 kinds, 256-wide tiles): one chunk accumulator plus a
   // running-sum region in TMEM instead of two tile accumulators.
@@ -329,18 +347,41 @@ __global__ void __launch_bounds__(kNumThreads, 1)
       uint32_t stage = 0, phase = 0;
       const uint64_t pol_a = l2_policy(static_cast<int>(p.hint_a));
       const uint64_t pol_b = l2_policy(static_cast<int>(p.hint_b));
-      bool sync = p.sync_ctr != nullptr && crank == 0;
-      const bool synced = sync;
-      const uint32_t cps_per_tile = sync ? (num_kb + p.sync_every - 1) / p.sync_every : 0;
+      const bool synced = p.sync_ctr != nullptr && rank == 0;
+      uint32_t timeouts = 0;
+      const uint32_t cps_per_tile = synced ? (num_kb + p.sync_every - 1) / p.sync_every : 0;
+      const PanelReady& rd = p.ready;
+      const uint32_t kb_per_panel = rd.num_panels ? rd.panel_k / kBlockK : 0;
       uint32_t local_tile = 0;
       for (uint32_t t = unit; t < num_tiles; t += num_units, ++local_tile) {
-        uint32_t mb, nbu;
-        tile_coords(t, p, num_nbu, mb, nbu);
-        const uint32_t nb = nbu * kPairs + pair;
+        uint32_t mb, nb;
+        tile_coords(t, p, p.num_n_blocks, mb, nb);
         const int32_t m0 = static_cast<int32_t>(mb * kBlockMcta * kCG + rank * kBlockMcta);
+        bool wait_sync = synced && timeouts < kMaxLockstepTimeouts;
+        // Flag blocks this CTA's loads touch: its own 128 rows of A, the
+        // tile's columns of B.
+        uint32_t ac0 = 0, ac1 = 0, bc0 = 0, bc1 = 0;
+        if (rd.a) {
+          const uint32_t r1 = min(static_cast<uint32_t>(m0) + kBlockMcta, p.m) - 1;
+          ac0 = (rd.a_row0 + static_cast<uint32_t>(m0)) / rd.a_chunk_rows;
+          ac1 = (rd.a_row0 + r1) / rd.a_chunk_rows;
+        }
+        if (rd.b) {
+          const uint32_t c0 = nb * Cfg::kBlockN, c1 = min(c0 + Cfg::kBlockN, p.n) - 1;
+          bc0 = (rd.b_col0 + c0) / rd.b_chunk_cols;
+          bc1 = (rd.b_col0 + c1) / rd.b_chunk_cols;
+        }
         for (uint32_t kb = 0; kb < num_kb; ++kb) {
-          if (sync && kb % p.sync_every == 0)
-            sync = lockstep(p.sync_ctr, local_tile * cps_per_tile + kb / p.sync_every, num_units);
+          if (synced && kb % p.sync_every == 0 &&
+              !lockstep(p.sync_ctr, local_tile * cps_per_tile + kb / p.sync_every, num_units, wait_sync)) {
+            wait_sync = false;  // rest of this tile
+            ++timeouts;
+          }
+          if (kb_per_panel && kb % kb_per_panel == 0) {
+            const uint32_t panel = kb / kb_per_panel;
+            if (rd.a) wait_ready(rd.a, ac0, ac1, panel, rd);
+            if (rd.b) wait_ready(rd.b, bc0, bc1, panel, rd);
+          }
           mbar_wait(&empty_bar[stage], phase ^ 1);
           uint8_t* sa = smem + stage * Cfg::kStageBytes;
           uint8_t* sb = sa + Cfg::kParts * Cfg::kBytesA;
@@ -353,18 +394,7 @@ __global__ void __launch_bounds__(kNumThreads, 1)
             const CUtensorMap* mbm = part ? &tm_b_lo : &tm_b;
             uint8_t* da = sa + part * Cfg::kBytesA;
             uint8_t* db = sb + part * Cfg::kBytesB;
-            if constexpr (kPairs == 2) {
-              // This CTA loads half of the A slab (its pair index picks the
-              // half) into both pairs' CTAs with the same in-pair rank.
-              const uint16_t mc = static_cast<uint16_t>((1u << rank) | (1u << (kCG + rank)));
-              if (!p.a_mn_major) {
-                tma_load_2d_2sm_mc(da + pair * (kBlockMcta / 2) * kSwizzleBytes, ma, &full_bar[stage], k0,
-                                   m0 + static_cast<int32_t>(pair * (kBlockMcta / 2)), mc, pol_a);
-              } else {
-                tma_load_2d_2sm_mc(da + pair * kBlockK * kSwizzleBytes, ma, &full_bar[stage],
-                                   m0 + static_cast<int32_t>(pair * kElems128), k0, mc, pol_a);
-              }
-            } else if (!p.a_mn_major) {
+            if (!p.a_mn_major) {
               if (kCG == 2) tma_load_2d_2sm_hint(da, ma, &full_bar[stage], k0, m0, pol_a);
               else tma_load_2d(da, ma, &full_bar[stage], k0, m0);
             } else {
@@ -405,8 +435,8 @@ __global__ void __launch_bounds__(kNumThreads, 1)
       }
       if (synced) {
         // Finished: release the others' waits. The last pair to finish
-        // (nobody waits any more) zeroes the counter for the launch that
-        // reuses this slot, so launches need no memset in between.
+        // (nobody waits any more) zeroes the counter for the next launch on
+        // the same stream, so launches need no memset in between.
         const uint32_t old = atomicAdd(p.sync_ctr, 1u << 24);
         if ((old >> 24) + 1 == num_units) atomicExch(p.sync_ctr, 0u);
       }
@@ -460,7 +490,7 @@ __global__ void __launch_bounds__(kNumThreads, 1)
               }
             }
           }
-          if constexpr (kCG == 2) mma_commit_2sm(&empty_bar[stage], all_mask);
+          if constexpr (kCG == 2) mma_commit_2sm(&empty_bar[stage], pair_mask);
           else mma_commit(&empty_bar[stage]);
           if (fold ? (kq + 1 == p.fold_kb || kb + 1 == num_kb) : kb + 1 == num_kb) {
             if constexpr (kCG == 2) mma_commit_2sm(&tfull_bar[fold ? 0 : acc], pair_mask);
@@ -570,14 +600,13 @@ __global__ void __launch_bounds__(kNumThreads, 1)
       tc_fence_before();
       __syncwarp();
       if (lane == 0) {
-        if (kCG == 2 && !leader) mbar_arrive_cluster(&tempty_bar[a], pair * kCG);
+        if (kCG == 2 && !leader) mbar_arrive_cluster(&tempty_bar[a], 0);
         else mbar_arrive(&tempty_bar[a]);
       }
     };
     for (uint32_t t = unit; t < num_tiles; t += num_units) {
-      uint32_t mb, nbu;
-      tile_coords(t, p, num_nbu, mb, nbu);
-      const uint32_t nb = nbu * kPairs + pair;
+      uint32_t mb, nb;
+      tile_coords(t, p, p.num_n_blocks, mb, nb);
       const uint32_t row0 = mb * kBlockMcta * kCG + rank * kBlockMcta + lane_grp * 32;
       const uint32_t row = row0 + lane;
       if (fold) {
@@ -687,10 +716,7 @@ int make_map_2d(CUtensorMap* map, const void* ptr, CUtensorMapDataType dt, uint3
   cuuint64_t strides[1] = {pitch_elems * esize};
   cuuint32_t box[2] = {box_inner, box_outer};
   cuuint32_t estr[2] = {1, 1};
-  static const int promo = [] {
-    const char* e = std::getenv("GM_L2_PROMO");
-    return e ? std::atoi(e) : 128;
-  }();
+  const int promo = debug_config().l2_promo;
   const CUtensorMapL2promotion pr = promo == 0 ? CU_TENSOR_MAP_L2_PROMOTION_NONE
                                     : promo == 64 ? CU_TENSOR_MAP_L2_PROMOTION_L2_64B
                                     : promo == 128 ? CU_TENSOR_MAP_L2_PROMOTION_L2_128B
@@ -712,10 +738,66 @@ int sm_count(int dev) {
   return counts[dev];
 }
 
-template <int kCG, int kElemBytes, int kSplit, int kChunks, int kPairs = 1>
+// Lockstep counter of a stream: launches on one stream never overlap, and
+// the last pair of each launch zeroes the counter, so one zeroed counter per
+// (device, stream) serves every launch without aliasing (stream ids are
+// unique for the process lifetime, cudaStreamGetId).
+uint32_t* lockstep_counter(int dev, cudaStream_t stream) {
+  static std::mutex mu;
+  static std::map<std::pair<int, unsigned long long>, uint32_t*> ctrs;
+  unsigned long long sid = 0;
+  if (cudaStreamGetId(stream, &sid) != cudaSuccess) {
+    cudaGetLastError();
+    return nullptr;
+  }
+  std::lock_guard<std::mutex> lock(mu);
+  auto it = ctrs.find({dev, sid});
+  if (it != ctrs.end()) return it->second;
+  uint32_t* c = nullptr;
+  if (cudaMalloc(&c, sizeof(uint32_t)) != cudaSuccess || cudaMemsetAsync(c, 0, sizeof(uint32_t), stream) != cudaSuccess) {
+    cudaGetLastError();
+    if (c) cudaFree(c);
+    return nullptr;
+  }
+  ctrs[{dev, sid}] = c;
+  return c;
+}
+
+// Persistent grid = the number of CTAs (CTA pairs) that are co-resident.
+template <int kCG, int kElemBytes, int kSplit, int kChunks>
+int resident_ctas(int dev) {
+  using Cfg = TcCfg<kCG, kElemBytes, kSplit, kChunks>;
+  static int resident[64] = {0};
+  if (dev < 0 || dev >= 64) return sm_count(dev);
+  if (!resident[dev]) {
+    auto kern = tc_gemm_kernel<kCG, kElemBytes, kSplit, kChunks>;
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::kSmemBytes);
+    cudaLaunchConfig_t cfg{};
+    cfg.blockDim = dim3(kNumThreads, 1, 1);
+    cfg.dynamicSmemBytes = Cfg::kSmemBytes;
+    cfg.gridDim = dim3(sm_count(dev), 1, 1);
+    cudaLaunchAttribute attrs[1];
+    attrs[0].id = cudaLaunchAttributeClusterDimension;
+    attrs[0].val.clusterDim.x = Cfg::kClusterCtas;
+    attrs[0].val.clusterDim.y = 1;
+    attrs[0].val.clusterDim.z = 1;
+    cfg.attrs = attrs;
+    cfg.numAttrs = 1;
+    int clusters = 0;
+    if (cudaOccupancyMaxActiveClusters(&clusters, kern, &cfg) != cudaSuccess || clusters <= 0) {
+      cudaGetLastError();
+      clusters = sm_count(dev) / Cfg::kClusterCtas;
+    }
+    resident[dev] = clusters * Cfg::kClusterCtas;
+  }
+  return resident[dev];
+}
+
+template <int kCG, int kElemBytes, int kSplit, int kChunks>
 int launch(const TcOperand& a, const TcOperand& b, const TcOperand* a_lo, const TcOperand* b_lo,
            const TcParams& p0, int max_ctas, cudaStream_t stream, const char** err) {
-  using Cfg = TcCfg<kCG, kElemBytes, kSplit, kChunks, kPairs>;
+  using Cfg = TcCfg<kCG, kElemBytes, kSplit, kChunks>;
+  const DebugConfig& dbg = debug_config();
   const CUtensorMapDataType dt = kElemBytes == 4 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32
                                                  : CU_TENSOR_MAP_DATA_TYPE_UINT16;
   constexpr uint32_t kChunk = kSwizzleBytes / kElemBytes;
@@ -723,7 +805,7 @@ int launch(const TcOperand& a, const TcOperand& b, const TcOperand* a_lo, const 
   CUtensorMap ma, mb, mal, mbl;
   auto map_a = [&](CUtensorMap* m, const TcOperand& op) {
     // A logical M x K. K-major: stored M rows x K cols; MN-major: K rows x M cols.
-    if (!p.a_mn_major) return make_map_2d(m, op.ptr, dt, kElemBytes, p.k, p.m, op.ld, Cfg::kBlockK, kBlockMcta / kPairs, err);
+    if (!p.a_mn_major) return make_map_2d(m, op.ptr, dt, kElemBytes, p.k, p.m, op.ld, Cfg::kBlockK, kBlockMcta, err);
     return make_map_2d(m, op.ptr, dt, kElemBytes, p.m, p.k, op.ld, kChunk, Cfg::kBlockK, err);
   };
   auto map_b = [&](CUtensorMap* m, const TcOperand& op) {
@@ -738,30 +820,26 @@ int launch(const TcOperand& a, const TcOperand& b, const TcOperand* a_lo, const 
     mal = ma;
     mbl = mb;
   }
-  p.num_m_blocks = (p.m + kBlockMcta * kCG - 1) / (kBlockMcta * kCG);
-  {
-    static const uint32_t env_group = [] {
-      const char* e = std::getenv("GM_RASTER_GROUP");
-      return e ? static_cast<uint32_t>(std::atoi(e)) : 0u;
-    }();
-    p.group = env_group ? env_group : 16;  // interleaved sweep at 32768^3: 12-16 beat 32 by 2% (DRAM 84 -> 67 GB)
-    static const uint32_t ha = std::getenv("GM_HINT_A") ? std::atoi(std::getenv("GM_HINT_A")) : 0;
-    static const uint32_t hb = std::getenv("GM_HINT_B") ? std::atoi(std::getenv("GM_HINT_B")) : 0;
-    p.hint_a = ha;
-    p.hint_b = hb;
-    // Lockstep every 16 k-blocks for long-k launches (default; GM_TC_SYNC=0 off).
-    static const int se = std::getenv("GM_TC_SYNC") ? std::atoi(std::getenv("GM_TC_SYNC")) : -1;
-    const uint32_t kblocks = (p.k + Cfg::kBlockK - 1) / Cfg::kBlockK;
-    p.sync_every = se >= 0 ? static_cast<uint32_t>(se) : (kblocks >= 64 && kChunks == 2 ? 16u : 0u);
-    p.sync_ctr = nullptr;
-    if (p.group > p.num_m_blocks) p.group = p.num_m_blocks;
+  if (p.ready.num_panels && (p.ready.panel_k % Cfg::kBlockK || !p.ready.streams ||
+                             (p.ready.a && !p.ready.a_chunk_rows) || (p.ready.b && !p.ready.b_chunk_cols))) {
+    *err = "tc_gemm: panel flags need panel_k a multiple of the k-block and non-zero chunk sizes";
+    return 1;
   }
+  p.num_m_blocks = (p.m + kBlockMcta * kCG - 1) / (kBlockMcta * kCG);
+  // Raster group 16: an interleaved sweep at 32768^3 measured 12-16 2% faster
+  // than 32 (DRAM 84 -> 67 GB).
+  p.group = dbg.raster_group > 0 ? static_cast<uint32_t>(dbg.raster_group) : 16u;
+  p.hint_a = static_cast<uint32_t>(dbg.hint_a);
+  p.hint_b = static_cast<uint32_t>(dbg.hint_b);
+  // Lockstep every 16 k-blocks for long-k launches with wide tiles.
+  const uint32_t kblocks = (p.k + Cfg::kBlockK - 1) / Cfg::kBlockK;
+  p.sync_every = dbg.tc_sync >= 0 ? static_cast<uint32_t>(dbg.tc_sync) : (kblocks >= 64 && kChunks == 2 ? 16u : 0u);
+  p.sync_ctr = nullptr;
+  if (p.group > p.num_m_blocks) p.group = p.num_m_blocks;
   p.num_n_blocks = (p.n + Cfg::kBlockN - 1) / Cfg::kBlockN;
   int dev = 0;
   cudaGetDevice(&dev);
-  auto kern = tc_gemm_kernel<kCG, kElemBytes, kSplit, kChunks, kPairs>;
-  // Persistent grid = the number of CTAs (CTA pairs) that are co-resident.
-  static int resident[64] = {0};
+  auto kern = tc_gemm_kernel<kCG, kElemBytes, kSplit, kChunks>;
   cudaLaunchConfig_t cfg{};
   cfg.blockDim = dim3(kNumThreads, 1, 1);
   cfg.dynamicSmemBytes = Cfg::kSmemBytes;
@@ -773,48 +851,23 @@ int launch(const TcOperand& a, const TcOperand& b, const TcOperand* a_lo, const 
   attrs[0].val.clusterDim.z = 1;
   cfg.attrs = attrs;
   cfg.numAttrs = 1;
-  if (dev < 64 && !resident[dev]) {
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::kSmemBytes);
-    int clusters = 0;
-    cfg.gridDim = dim3(sm_count(dev), 1, 1);
-    if (cudaOccupancyMaxActiveClusters(&clusters, kern, &cfg) != cudaSuccess || clusters <= 0) {
-      cudaGetLastError();
-      clusters = sm_count(dev) / Cfg::kClusterCtas;
-    }
-    resident[dev] = clusters * Cfg::kClusterCtas;
-  }
-  int ctas = dev < 64 ? resident[dev] : sm_count(dev);
+  const int res = resident_ctas<kCG, kElemBytes, kSplit, kChunks>(dev);
+  int ctas = res;
   if (max_ctas > 0 && max_ctas < ctas) ctas = max_ctas;
   ctas = (ctas / Cfg::kClusterCtas) * Cfg::kClusterCtas;
-  const int need = static_cast<int>((p.num_n_blocks + kPairs - 1) / kPairs * p.num_m_blocks) * Cfg::kClusterCtas;
+  const int need = static_cast<int>(p.num_n_blocks * p.num_m_blocks) * Cfg::kClusterCtas;
   if (need < ctas) ctas = need;
   cfg.gridDim = dim3(ctas, 1, 1);
-  if (p.sync_every > 0) {
-    // A ring of 64 counters per device, zeroed once; each launch takes the
-    // next slot and its last finishing pair zeroes it again.
-    static uint32_t* ctr[64] = {nullptr};
-    static std::atomic<uint32_t> next[64];
-    if (dev < 64 && !ctr[dev]) {
-      if (cudaMalloc(&ctr[dev], 64 * sizeof(uint32_t)) == cudaSuccess) {
-        cudaMemset(ctr[dev], 0, 64 * sizeof(uint32_t));
-      } else {
-        cudaGetLastError();
-        ctr[dev] = nullptr;
-      }
-    }
-    if (dev < 64 && ctr[dev]) p.sync_ctr = ctr[dev] + (next[dev].fetch_add(1) % 64);
-  }
-  static const bool debug = std::getenv("GM_DEBUG") != nullptr;
-  if (debug)
-    std::fprintf(stderr, "[gm] tc_gemm cg=%d elem=%d split=%d chunks=%d pairs=%d m=%u n=%u k=%u grid=%d resident=%d stages=%u smem=%u\n",
-                 kCG, kElemBytes, kSplit, kChunks, kPairs, p.m, p.n, p.k, ctas, dev < 64 ? resident[dev] : -1,
-                 Cfg::kStages, Cfg::kSmemBytes);
+  if (p.sync_every > 0) p.sync_ctr = lockstep_counter(dev, stream);
+  if (dbg.verbose)
+    std::fprintf(stderr, "[gm] tc_gemm cg=%d elem=%d split=%d chunks=%d m=%u n=%u k=%u grid=%d resident=%d stages=%u smem=%u panels=%u\n",
+                 kCG, kElemBytes, kSplit, kChunks, p.m, p.n, p.k, ctas, res,
+                 Cfg::kStages, Cfg::kSmemBytes, p.ready.num_panels);
   CUtensorMap mc = ma;
   {
     const uint32_t cb = p.c_dtype == 2 ? 4 : 2;
     p.tma_store = 0;
-    static const bool no_tma_store = std::getenv("GM_NO_TMA_STORE") != nullptr;
-    if (!no_tma_store && p.beta == 0.0f && (reinterpret_cast<uintptr_t>(p.c) % 16) == 0 && (p.ldc * cb) % 16 == 0) {
+    if (dbg.tma_store && p.beta == 0.0f && (reinterpret_cast<uintptr_t>(p.c) % 16) == 0 && (p.ldc * cb) % 16 == 0) {
       const char* e2 = nullptr;
       if (make_map_2d(&mc, p.c, cb == 4 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_UINT16, cb, p.n,
                       p.m, p.ldc, 32, 32, &e2,
@@ -839,7 +892,43 @@ int launch(const TcOperand& a, const TcOperand& b, const TcOperand* a_lo, const 
   return 0;
 }
 
+bool wide_tiles(uint64_t m, uint64_t n, uint64_t k, int cg) {
+  const int env_chunks = debug_config().tc_chunks;
+  if (env_chunks) return env_chunks == 2;
+  if (!(k >= 4096 && n > kMmaN)) return false;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const uint64_t units = static_cast<uint64_t>(sm_count(dev)) / cg;
+  const uint64_t mrows = kBlockMcta * cg;
+  auto fill = [&](uint64_t tiles) {
+    const uint64_t waves = (tiles + units - 1) / units;
+    return static_cast<double>(tiles) / static_cast<double>(waves * units);
+  };
+  const uint64_t mb = (m + mrows - 1) / mrows;
+  const double f_wide = fill(mb * ((n + 2 * kMmaN - 1) / (2 * kMmaN)));
+  const double f_narrow = fill(mb * ((n + kMmaN - 1) / kMmaN));
+  return !(f_narrow > f_wide + 0.05);
+}
+
 }  // namespace
+
+TcTilePlan tc_tile_plan(uint64_t m, uint64_t n, uint64_t k, int cta_group, int max_ctas) {
+  const int cg = cta_group == 1 ? 1 : 2;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const bool wide = wide_tiles(m, n, k, cg);
+  TcTilePlan t;
+  t.block_m = kBlockMcta * cg;
+  t.block_n = wide ? 2 * kMmaN : kMmaN;
+  int ctas = cg == 1 ? (wide ? resident_ctas<1, 2, 0, 2>(dev) : resident_ctas<1, 2, 0, 1>(dev))
+                     : (wide ? resident_ctas<2, 2, 0, 2>(dev) : resident_ctas<2, 2, 0, 1>(dev));
+  if (max_ctas > 0 && max_ctas < ctas) ctas = max_ctas;
+  t.units = std::max(1, ctas / cg);
+  const uint32_t mblocks = static_cast<uint32_t>((m + t.block_m - 1) / t.block_m);
+  const int rg = debug_config().raster_group;
+  t.group = std::min(rg > 0 ? static_cast<uint32_t>(rg) : 16u, std::max(1u, mblocks));
+  return t;
+}
 
 int tc_gemm(const TcGemmArgs& g, cudaStream_t stream, const char** err) {
   TcParams p{};
@@ -853,6 +942,7 @@ int tc_gemm(const TcGemmArgs& g, cudaStream_t stream, const char** err) {
   p.c = g.c;
   p.ldc = g.ldc;
   p.c_dtype = g.c_dtype;
+  p.ready = g.ready;
   const uint32_t cb = g.c_dtype == 2 ? 4 : 2;
   p.c_vec = ((reinterpret_cast<uintptr_t>(g.c) % 16) == 0 && (g.ldc * cb) % 16 == 0) ? 1 : 0;
   if (g.bias) {
@@ -868,48 +958,26 @@ int tc_gemm(const TcGemmArgs& g, cudaStream_t stream, const char** err) {
   }
   const int cg = g.cta_group == 1 ? 1 : 2;
   const uint32_t mrows = kBlockMcta * cg;
-  // Wide tiles (256 x 512 per CTA pair, two UMMAs per k-step) halve the
-  // distinct A panels in flight and cut L2->SMEM traffic by a quarter; their
-  // single accumulator leaves the epilogue unoverlapped, which only pays off
-  // when the k loop is long. GM_TC_CHUNKS=1|2 overrides.
-  static const int env_chunks = [] {
-    const char* e = std::getenv("GM_TC_CHUNKS");
-    return e ? std::atoi(e) : 0;
-  }();
   if (g.kind == TcKind::F16 || g.kind == TcKind::BF16) {
     const uint32_t fmt = g.kind == TcKind::BF16 ? 1 : 0;
     p.idesc = make_idesc(fmt, fmt, p.a_mn_major, p.b_mn_major, mrows, kMmaN);
-    // Wide tiles only when they fill the persistent grid's waves as well as
-    // 256-wide tiles do (a 1024 x 4096 output is 32 wide tiles for 74 pairs:
-    // 43% of the SMs; 64 narrow tiles fill 86%). Same bits either way.
-    bool wide = env_chunks ? env_chunks == 2 : (g.k >= 4096 && g.n > kMmaN);
-    if (wide && !env_chunks) {
-      int dev = 0;
-      cudaGetDevice(&dev);
-      const uint64_t units = static_cast<uint64_t>(sm_count(dev)) / cg;
-      auto fill = [&](uint64_t tiles) {
-        const uint64_t waves = (tiles + units - 1) / units;
-        return static_cast<double>(tiles) / static_cast<double>(waves * units);
-      };
-      const uint64_t mb = (g.m + mrows - 1) / mrows;
-      const double f_wide = fill(mb * ((g.n + 2 * kMmaN - 1) / (2 * kMmaN)));
-      const double f_narrow = fill(mb * ((g.n + kMmaN - 1) / kMmaN));
-      if (f_narrow > f_wide + 0.05) wide = false;
-    }
-    static const int env_pairs = [] {
-      const char* e = std::getenv("GM_TC_PAIRS");
-      return e ? std::atoi(e) : 0;
-    }();
-    // Two pairs per cluster sharing A (multicast) once there are enough
-    // N-blocks for both pairs.
-    const bool pairs2 = env_pairs == 2;  // 4-CTA clusters place only 132 SMs: opt-in
-    if (cg == 2 && wide && pairs2)
-      return launch<2, 2, 0, 2, 2>(g.a, g.b, nullptr, nullptr, p, g.max_ctas, stream, err);
+    // Wide tiles (256 x 512 per CTA pair, two UMMAs per k-step) halve the
+    // distinct A panels in flight and cut L2->SMEM traffic by a quarter;
+    // their single accumulator leaves the epilogue unoverlapped, which only
+    // pays off when the k loop is long. Wide tiles are kept only when they
+    // fill the persistent grid's waves as well as 256-wide tiles do (a
+    // 1024 x 4096 output is 32 wide tiles for 74 pairs: 43% of the SMs; 64
+    // narrow tiles fill 86%). Same bits either way.
+    const bool wide = wide_tiles(g.m, g.n, g.k, cg);
     if (cg == 1)
       return wide ? launch<1, 2, 0, 2>(g.a, g.b, nullptr, nullptr, p, g.max_ctas, stream, err)
                   : launch<1, 2, 0, 1>(g.a, g.b, nullptr, nullptr, p, g.max_ctas, stream, err);
     return wide ? launch<2, 2, 0, 2>(g.a, g.b, nullptr, nullptr, p, g.max_ctas, stream, err)
                 : launch<2, 2, 0, 1>(g.a, g.b, nullptr, nullptr, p, g.max_ctas, stream, err);
+  }
+  if (g.ready.num_panels) {
+    *err = "tc_gemm: panel flags are consumed by the 16-bit kinds only";
+    return 1;
   }
   p.idesc = make_idesc(2, 2, p.a_mn_major, p.b_mn_major, mrows, kMmaN);
   if (g.fold_k) {

@@ -13,6 +13,21 @@ struct TcOperand {
   uint64_t ld = 0;            // row pitch in elements (pitch bytes % 16 == 0)
 };
 
+// In-GEMM panel pipelining: the consumer's pull streams copy the gathered
+// bands block by block -- (m-chunk x k-panel) of A, (n-chunk x k-panel) of B
+// -- and after its pieces of a block stream s writes
+// flags[(chunk * num_panels + panel) * streams + s] = target. The GEMM's
+// producer waits for the blocks a k-block reads before loading it, so
+// panel k+1 lands while panel k multiplies. Null flag array: resident.
+struct PanelReady {
+  const uint64_t* a = nullptr;
+  const uint64_t* b = nullptr;
+  uint64_t target = 0;
+  uint32_t a_row0 = 0, a_chunk_rows = 0;  // kernel row r lies in A chunk (a_row0 + r) / a_chunk_rows
+  uint32_t b_col0 = 0, b_chunk_cols = 0;  // kernel column j lies in B chunk (b_col0 + j) / b_chunk_cols
+  uint32_t panel_k = 0, num_panels = 0, streams = 0;  // num_panels 0 = off
+};
+
 struct TcGemmArgs {
   uint64_t m = 0, n = 0, k = 0;
   bool trans_a = false, trans_b = false;
@@ -32,7 +47,17 @@ struct TcGemmArgs {
   const void* bias = nullptr;
   void* act = nullptr;
   uint64_t ld_act = 0;
+  PanelReady ready;  // 16-bit kinds only
 };
+
+// The 16-bit kernel's tile raster for a launch of this shape on the current
+// device (host mirror, for ordering panel transfers by when the persistent
+// grid first needs them): tile = block_m x block_n, tiles in groups of
+// `group` M-blocks (m fastest inside a group), `units` CTA pairs.
+struct TcTilePlan {
+  uint32_t block_m = 256, block_n = 512, group = 16, units = 74;
+};
+TcTilePlan tc_tile_plan(uint64_t m, uint64_t n, uint64_t k, int cta_group, int max_ctas);
 
 // Launches on `stream`; returns 0 or 1 with *err set (static string).
 int tc_gemm(const TcGemmArgs& args, cudaStream_t stream, const char** err);

@@ -5,6 +5,7 @@
 #include <cstdlib>
 
 #include "../cuda/convert.h"
+#include "../cuda/debug_config.h"
 #include "../cuda/gemm_f64.h"
 #include "../cuda/gemm_tc.h"
 
@@ -128,12 +129,8 @@ std::uint64_t elemBytes(int p) {
 std::uint64_t stagedLd(std::uint64_t cols, std::uint64_t eb) { return roundUp(cols * eb, 128) / eb; }
 
 std::uint64_t tf32Chunk() {
-  static const std::uint64_t L = [] {
-    const char* e = std::getenv("GM_TF32_CHUNK");
-    const long v = e ? std::atol(e) : 0;
-    return v > 0 ? static_cast<std::uint64_t>(v) : std::uint64_t{256};
-  }();
-  return L;
+  const int v = gmk::debug_config().tf32_chunk;
+  return v > 0 ? static_cast<std::uint64_t>(v) : std::uint64_t{256};
 }
 
 bool tmaOk(const void* p, std::uint64_t ld, std::uint64_t eb) {
@@ -215,9 +212,19 @@ std::uint64_t gemmWorkspaceBytes(const gm_gemm_desc& d, const void* a, const voi
   return makePlan(d, a, b).bytes;
 }
 
+bool gemmConsumesPanelFlags(const gm_gemm_desc& d, const void* a, const void* b) {
+  if (d.m == 0 || d.n == 0 || d.alpha == 0.0 || d.k == 0) return false;
+  if (d.prec_c == GM_DOUBLE) return false;
+  const Plan pl = makePlan(d, a, b);
+  return pl.path == Plan::F16 && !pl.stageA && !pl.stageB;
+}
+
 void gemmLocal(const gm_gemm_desc& d, const void* a, const void* b, void* c, void* workspace,
-               std::uint64_t workspaceBytes, cudaStream_t stream, const BiasReluEpilogue* ep) {
+               std::uint64_t workspaceBytes, cudaStream_t stream, const BiasReluEpilogue* ep,
+               const gmk::PanelReady* ready) {
   if (d.m == 0 || d.n == 0) return;
+  if (ready && ready->num_panels && !gemmConsumesPanelFlags(d, a, b))
+    throw Error("gemm: panel flags need the 16-bit tcgen05 path reading both operands in place");
   if (ep && (d.alpha == 0.0 || d.k == 0 || d.prec_c != GM_BF16 || d.prec_a == GM_DOUBLE || d.prec_b == GM_DOUBLE))
     throw Error("gemm: fused bias/relu epilogue needs the tcgen05 path with bf16 C");
   for (int p : {d.prec_a, d.prec_b, d.prec_c}) (void)elemBytes(p);
@@ -286,6 +293,7 @@ void gemmLocal(const gm_gemm_desc& d, const void* a, const void* b, void* c, voi
   g.max_ctas = d.max_ctas;
   g.a = {a, d.lda};
   g.b = {b, d.ldb};
+  if (ready) g.ready = *ready;
 
   if (pl.path == Plan::F16) {
     const std::uint64_t eb = 2;

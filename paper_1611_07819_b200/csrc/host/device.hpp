@@ -12,6 +12,7 @@
 
 #include "../../../include/gridmath_b200.h"
 #include "core.hpp"
+#include "../cuda/gemm_tc.h"
 
 namespace gridmath {
 
@@ -70,7 +71,12 @@ struct BiasReluEpilogue {
   void* act = nullptr;
   std::uint64_t ldAct = 0;
 };
+// `ready`: in-GEMM panel pipelining flags (see gmk::PanelReady); only the
+// 16-bit tcgen05 path reading both operands in place consumes them
+// (gemmConsumesPanelFlags).
+bool gemmConsumesPanelFlags(const gm_gemm_desc& d, const void* a, const void* b);
 void gemmLocal(const gm_gemm_desc& d, const void* a, const void* b, void* c, void* workspace,
-               std::uint64_t workspaceBytes, cudaStream_t stream, const BiasReluEpilogue* ep = nullptr);
+               std::uint64_t workspaceBytes, cudaStream_t stream, const BiasReluEpilogue* ep = nullptr,
+               const gmk::PanelReady* ready = nullptr);
 
 }  // namespace gridmath

@@ -44,7 +44,7 @@ void Session::setLocalPackedAsync(DistMatrix m, const void* host, std::uint64_t 
       n[t.second.rank] += static_cast<std::uint32_t>((t.first.rowCount + rpc - 1) / rpc);
     }
     for (std::uint32_t r = 0; r < opts_.workers; ++r) {
-      std::uint32_t& cnt = upCount_[{r, slot}];
+      std::uint64_t& cnt = upCount_[{r, slot}];
       cw.base[r] = cnt;
       cnt += n[r];
     }
@@ -82,7 +82,7 @@ void Session::setLocalPackedAsync(DistMatrix m, const void* host, std::uint64_t 
         cudaCheck(cudaEventRecord(c.done, w->h2d), "upload: chunk event");
         if (ipc_)  // peers pulling these rows wait for this value (ChunkedWrite::base)
           ipcWrite(w->h2d, w->flags + kUpChunkOff + slotOf(m.id()),
-                   chunked_.at(m.id()).base[w->rank] + static_cast<std::uint32_t>(up.chunks.size()) + 1);
+                   chunked_.at(m.id()).base[w->rank] + static_cast<std::uint64_t>(up.chunks.size()) + 1);
         up.chunks.push_back(c);
       }
     }

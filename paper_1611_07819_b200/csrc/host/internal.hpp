@@ -13,7 +13,7 @@ namespace gridmath {
 
 constexpr std::uint64_t kPitchAlign = 16;  // TMA row-stride rule
 
-// SPMD flag page (u32 words): written[kSlots], readDone[2][kSlots] (comm,
+// SPMD flag page (u64 words): written[kSlots], readDone[2][kSlots] (comm,
 // compute), upChunk[kSlots] (chunks of chunked uploads completed, per slot).
 constexpr std::uint32_t kSlots = 16384;
 constexpr std::size_t kUpChunkOff = 3ull * kSlots;

@@ -59,6 +59,20 @@ struct OpDescriptor {
   static OpDescriptor decode(const std::vector<std::uint8_t>& payload);
 };
 
+// Worker acknowledgement of an op (reference ops.hpp:63-75). On the B200
+// runtime a worker's "ack" is the completion of its stream-ordered work;
+// Session::awaitAcks returns one per local worker.
+enum class CompletionKind : std::uint32_t { OpAck = 0, ReplicaDone = 1, ReplicaFailed = 2 };
+struct Completion {
+  std::uint64_t execId = 0;
+  std::uint32_t status = 0;  // 0 ok, 1 error
+  CompletionKind kind = CompletionKind::OpAck;
+  std::uint64_t aux0 = 0;
+  std::uint64_t aux1 = 0;
+  double scalar = 0.0;
+  std::vector<std::uint8_t> blob;
+};
+
 std::vector<std::uint64_t> mutatedMatrices(const OpDescriptor& op);
 void applyOpMetadata(const OpDescriptor& op, DescriptorTable& table);
 

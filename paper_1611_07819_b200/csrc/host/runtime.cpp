@@ -17,6 +17,7 @@
 #include "runtime.hpp"
 
 #include <cuda.h>  // types of the driver entry points (resolved at run time, no -lcuda)
+#include <nccl.h>
 
 #include <algorithm>
 #include <cstdio>
@@ -24,20 +25,23 @@
 #include <cstring>
 
 #include "../cuda/convert.h"
+#include "../cuda/debug_config.h"
 #include "internal.hpp"
 
 namespace gridmath {
 
 namespace {
 
-constexpr std::size_t kFlagBytes = 4ull * kSlots * sizeof(std::uint32_t);
+constexpr std::size_t kFlagBytes = 4ull * kSlots * sizeof(std::uint64_t);
 
 // Stream memory operations and address-range lookup from the driver, via
 // the runtime's entry-point query (the library stays loadable without a
 // driver: CPU-only hosts load it for the pure-host helpers).
 struct DriverFns {
-  CUresult (*waitValue32)(CUstream, CUdeviceptr, cuuint32_t, unsigned int) = nullptr;
-  CUresult (*writeValue32)(CUstream, CUdeviceptr, cuuint32_t, unsigned int) = nullptr;
+  // 64-bit flag words: exec ids never wrap (a 32-bit GEQ wait would pass
+  // early against a pre-wrap value after 2^32 ops).
+  CUresult (*waitValue64)(CUstream, CUdeviceptr, cuuint64_t, unsigned int) = nullptr;
+  CUresult (*writeValue64)(CUstream, CUdeviceptr, cuuint64_t, unsigned int) = nullptr;
   CUresult (*addressRange)(CUdeviceptr*, size_t*, CUdeviceptr) = nullptr;
 };
 
@@ -45,12 +49,12 @@ const DriverFns& driver() {
   static const DriverFns fns = [] {
     DriverFns f;
     cudaDriverEntryPointQueryResult q;
-    if (cudaGetDriverEntryPoint("cuStreamWaitValue32", reinterpret_cast<void**>(&f.waitValue32),
+    if (cudaGetDriverEntryPoint("cuStreamWaitValue64", reinterpret_cast<void**>(&f.waitValue64),
                                 cudaEnableDefault, &q) != cudaSuccess || q != cudaDriverEntryPointSuccess)
-      f.waitValue32 = nullptr;
-    if (cudaGetDriverEntryPoint("cuStreamWriteValue32", reinterpret_cast<void**>(&f.writeValue32),
+      f.waitValue64 = nullptr;
+    if (cudaGetDriverEntryPoint("cuStreamWriteValue64", reinterpret_cast<void**>(&f.writeValue64),
                                 cudaEnableDefault, &q) != cudaSuccess || q != cudaDriverEntryPointSuccess)
-      f.writeValue32 = nullptr;
+      f.writeValue64 = nullptr;
     if (cudaGetDriverEntryPoint("cuMemGetAddressRange", reinterpret_cast<void**>(&f.addressRange),
                                 cudaEnableDefault, &q) != cudaSuccess || q != cudaDriverEntryPointSuccess)
       f.addressRange = nullptr;
@@ -177,15 +181,12 @@ void validateOp(const DescriptorTable& t, const OpDescriptor& op, std::uint32_t 
     }
     case OpCode::MetaChecksum:
     case OpCode::QueryStats:
+    case OpCode::DistributeSeeds:
       return;
     default:
       throw Error("op not supported on the B200 GEMM path");
   }
 }
-
-namespace {
-
-}  // namespace
 
 // ---------------------------------------------------------------- DistMatrix
 
@@ -279,6 +280,25 @@ Worker::Worker(std::uint32_t r, int dev, std::uint64_t budget)
   cudaCheck(cudaEventCreate(&kStart), "worker: event");
   cudaCheck(cudaEventCreate(&cStart), "worker: event");
   cudaCheck(cudaEventCreate(&cEnd), "worker: event");
+  if (gmk::debug_config().ready_slots > 0) readyCap = static_cast<std::uint64_t>(gmk::debug_config().ready_slots);
+  void* rf = nullptr;
+  cudaCheck(cudaMalloc(&rf, readyCap * sizeof(std::uint64_t)), "worker: ready flags");
+  cudaCheck(cudaMemset(rf, 0, readyCap * sizeof(std::uint64_t)), "worker: ready flags");
+  readyFlags = static_cast<std::uint64_t*>(rf);
+}
+
+std::uint64_t Worker::reserveReady(std::uint64_t n) {
+  if (n == 0 || n > readyCap) throw Error("gemm: ready-flag region of " + std::to_string(n) + " slots");
+  std::uint64_t start = readyHead;
+  if (start % readyCap + n > readyCap) start += readyCap - start % readyCap;  // contiguous in memory
+  const std::uint64_t end = start + n;
+  while (!readyInUse.empty() && readyInUse.front().first + readyCap < end) {
+    cudaCheck(cudaStreamWaitEvent(comm, readyInUse.front().done, 0), "gemm: ready region reuse");
+    recycle(readyInUse.front().done);
+    readyInUse.pop_front();
+  }
+  readyHead = end;
+  return start;
 }
 
 Worker::~Worker() {
@@ -307,6 +327,8 @@ Worker::~Worker() {
     cudaEventDestroy(ev.second);
   }
   if (flags) cudaFree(flags);
+  if (readyFlags) cudaFree(readyFlags);
+  for (auto& r : readyInUse) cudaEventDestroy(r.done);
   if (nccl) ncclCommDestroy(nccl);
   for (cudaEvent_t e : pool_) cudaEventDestroy(e);
   cudaEventDestroy(tStart);
@@ -386,11 +408,15 @@ void Worker::beforeMutation(std::uint64_t matrix, cudaStream_t on) {
 
 // ---------------------------------------------------------------- Session
 
-namespace {
-
 // Max-reduce a small host byte array over all SPMD ranks (control plane of
-// the IPC registration; blocking).
-void allreduceMaxBytes(Worker& w, void* host, std::size_t n) {
+// the IPC registration; blocking): the caller's channel (e.g. gloo) when one
+// was given, else the NCCL communicator through a device staging buffer.
+void Session::controlMax(void* host, std::size_t n) {
+  if (opts_.controlAllreduceMax) {
+    opts_.controlAllreduceMax(host, n);
+    return;
+  }
+  Worker& w = *local(static_cast<std::uint32_t>(opts_.spmdRank));
   w.activate();
   void* d = w.arena.alloc(std::max<std::size_t>(n, 256), w.compute);
   cudaCheck(cudaMemcpyAsync(d, host, n, cudaMemcpyHostToDevice, w.compute), "ipc: upload records");
@@ -399,8 +425,6 @@ void allreduceMaxBytes(Worker& w, void* host, std::size_t n) {
   cudaCheck(cudaStreamSynchronize(w.compute), "ipc: records sync");
   w.arena.free(d, w.compute);
 }
-
-}  // namespace
 
 // SPMD copy-engine plane: every rank exports a flag page; every rank must
 // map every peer's page, or all ranks fall back to NCCL together.
@@ -411,12 +435,12 @@ void Session::setupIpc() {
   std::vector<IpcRecord> recs(opts_.workers);
   std::memset(recs.data(), 0, recs.size() * sizeof(IpcRecord));
   IpcRecord& mine = recs[opts_.spmdRank];
-  bool ok = drv.waitValue32 && drv.writeValue32 && drv.addressRange;
+  bool ok = drv.waitValue64 && drv.writeValue64 && drv.addressRange;
   if (ok) {
     void* f = nullptr;
     ok = cudaMalloc(&f, kFlagBytes) == cudaSuccess;
     if (ok) {
-      w.flags = static_cast<std::uint32_t*>(f);
+      w.flags = static_cast<std::uint64_t*>(f);
       ok = cudaMemset(f, 0, kFlagBytes) == cudaSuccess && cudaDeviceSynchronize() == cudaSuccess &&
            cudaIpcGetMemHandle(&mine.handle, f) == cudaSuccess;
       mine.base = reinterpret_cast<std::uint64_t>(f);
@@ -425,10 +449,10 @@ void Session::setupIpc() {
   }
   cudaGetLastError();
   if (!ok) mine.failed = 1;
-  allreduceMaxBytes(w, recs.data(), recs.size() * sizeof(IpcRecord));
+  controlMax(recs.data(), recs.size() * sizeof(IpcRecord));
   bool all = true;
   for (const IpcRecord& r : recs) all = all && r.valid && !r.failed;
-  std::vector<std::uint32_t*> mapped(opts_.workers, nullptr);
+  std::vector<std::uint64_t*> mapped(opts_.workers, nullptr);
   for (std::uint32_t r = 0; all && r < opts_.workers; ++r) {
     if (r == w.rank) continue;
     void* p = nullptr;
@@ -438,10 +462,10 @@ void Session::setupIpc() {
       break;
     }
     ipcOpened_[{r, recs[r].base}] = p;
-    mapped[r] = static_cast<std::uint32_t*>(p);
+    mapped[r] = static_cast<std::uint64_t*>(p);
   }
   std::uint8_t failed = all ? 0 : 1;
-  allreduceMaxBytes(w, &failed, 1);
+  controlMax(&failed, 1);
   if (failed) {
     for (auto& kv : ipcOpened_) cudaIpcCloseMemHandle(kv.second);
     ipcOpened_.clear();
@@ -493,7 +517,7 @@ void Session::registerTiles(std::uint64_t id, const std::string& localError) {
     }
   }
   if (!err.empty()) recs[T].failed = 1;
-  allreduceMaxBytes(w, recs.data(), recs.size() * sizeof(IpcRecord));
+  controlMax(recs.data(), recs.size() * sizeof(IpcRecord));
   if (recs[T].failed)
     throw Error(err.empty() ? "op failed: a peer rank could not allocate or export its tiles" : err);
   std::vector<void*> ptrs(T, nullptr);
@@ -518,16 +542,16 @@ void Session::registerTiles(std::uint64_t id, const std::string& localError) {
   peerTiles_[id] = std::move(ptrs);
 }
 
-void Session::ipcWait(cudaStream_t s, const std::uint32_t* addr, std::uint64_t value) {
-  const CUresult r = driver().waitValue32(reinterpret_cast<CUstream>(s), reinterpret_cast<CUdeviceptr>(addr),
-                                          static_cast<cuuint32_t>(value), CU_STREAM_WAIT_VALUE_GEQ);
-  if (r != CUDA_SUCCESS) throw Error("ipc: cuStreamWaitValue32 failed (" + std::to_string(static_cast<int>(r)) + ")");
+void Session::ipcWait(cudaStream_t s, const std::uint64_t* addr, std::uint64_t value) {
+  const CUresult r = driver().waitValue64(reinterpret_cast<CUstream>(s), reinterpret_cast<CUdeviceptr>(addr),
+                                          static_cast<cuuint64_t>(value), CU_STREAM_WAIT_VALUE_GEQ);
+  if (r != CUDA_SUCCESS) throw Error("ipc: cuStreamWaitValue64 failed (" + std::to_string(static_cast<int>(r)) + ")");
 }
 
-void Session::ipcWrite(cudaStream_t s, std::uint32_t* addr, std::uint64_t value) {
-  const CUresult r = driver().writeValue32(reinterpret_cast<CUstream>(s), reinterpret_cast<CUdeviceptr>(addr),
-                                           static_cast<cuuint32_t>(value), CU_STREAM_WRITE_VALUE_DEFAULT);
-  if (r != CUDA_SUCCESS) throw Error("ipc: cuStreamWriteValue32 failed (" + std::to_string(static_cast<int>(r)) + ")");
+void Session::ipcWrite(cudaStream_t s, std::uint64_t* addr, std::uint64_t value) {
+  const CUresult r = driver().writeValue64(reinterpret_cast<CUstream>(s), reinterpret_cast<CUdeviceptr>(addr),
+                                           static_cast<cuuint64_t>(value), CU_STREAM_WRITE_VALUE_DEFAULT);
+  if (r != CUDA_SUCCESS) throw Error("ipc: cuStreamWriteValue64 failed (" + std::to_string(static_cast<int>(r)) + ")");
 }
 
 const Session::ChunkedWrite* Session::chunkedSource(std::uint64_t matrix) const {
@@ -649,7 +673,10 @@ Session::Session(SessionOptions opts) : opts_(std::move(opts)) {
       throw Error("session: spmd rank out of range");
     const int dev = devs[0];
     auto w = std::make_unique<Worker>(opts_.spmdRank, dev, budget(dev));
-    if (opts_.workers > 1) {
+    const bool ownControl = static_cast<bool>(opts_.controlAllreduceMax);
+    if (ownControl && opts_.transport == 1)
+      throw Error("session: the NCCL data plane needs the NCCL control channel (no control callback)");
+    if (opts_.workers > 1 && !ownControl) {
       ncclUniqueId id;
       static_assert(sizeof(id.internal) == 128, "nccl id size");
       std::memcpy(id.internal, opts_.ncclId.data(), 128);
@@ -659,7 +686,20 @@ Session::Session(SessionOptions opts) : opts_(std::move(opts)) {
       nccl_ = true;
     }
     workers_[opts_.spmdRank] = std::move(w);
-    if (nccl_ && opts_.transport != 1) setupIpc();
+    if (opts_.workers > 1 && opts_.transport != 1) setupIpc();
+    if (opts_.workers > 1 && !ipc_ && !nccl_)
+      throw Error("session: SPMD without NCCL needs the copy-engine (IPC) plane, and peer memory cannot be mapped");
+    if (opts_.workers > 1) {
+      // Every rank keeps a directory of every peer's panel cache and replays
+      // its keep/evict decisions with its own budget: the budgets must agree.
+      // Each rank contributes its budget in its own 8-byte slot (max-reduce
+      // of bytes = gather); all adopt the minimum.
+      std::vector<std::uint64_t> all(opts_.workers, 0);
+      all[opts_.spmdRank] = workers_[opts_.spmdRank]->cacheBudget;
+      controlMax(all.data(), all.size() * sizeof(std::uint64_t));
+      const std::uint64_t agreed = *std::min_element(all.begin(), all.end());
+      workers_[opts_.spmdRank]->cacheBudget = agreed;
+    }
   } else {
     for (std::uint32_t r = 0; r < opts_.workers; ++r) {
       const int dev = devs[r % devs.size()];
@@ -695,7 +735,7 @@ Session::~Session() {
     // idle before any mapping closes or any arena frees.
     try {
       std::uint8_t b = 0;
-      allreduceMaxBytes(*local(static_cast<std::uint32_t>(opts_.spmdRank)), &b, 1);
+      controlMax(&b, 1);
     } catch (...) {
     }
     for (auto& kv : ipcOpened_) cudaIpcCloseMemHandle(kv.second);
@@ -824,7 +864,11 @@ std::uint64_t Session::issue(OpDescriptor& op) {
   // Control plane: every local worker mirrors the op through the wire codec.
   const std::vector<std::uint8_t> wire = op.encode();
   for (auto& w : workers_)
-    if (w) applyOpMetadata(OpDescriptor::decode(wire), w->descs);
+    if (w) {
+      applyOpMetadata(OpDescriptor::decode(wire), w->descs);
+      countLink(kMasterRank, w->rank, MsgKind::Control, wire.size());
+      trace_.record(w->rank, EventKind::OpStart, op.execId, static_cast<std::uint64_t>(op.opcode));
+    }
   // SetData carrying a chunk size is an asynchronous upload (hostio.cpp).
   const bool asyncUpload = op.opcode == OpCode::SetData && op.ids[1] != 0;
   for (const auto& mv : moved) mutationHook(mv.first, mv.second, asyncUpload);
@@ -1105,7 +1149,39 @@ void Session::getDataRawInto(DistMatrix m, void* image, std::uint64_t bytes, boo
                 "getData: download");
     }
   });
-  if (nccl_ && !localOnly) {
+  if (ipc_ && !localOnly) {
+    // Remote tiles: every rank pulls each peer tile through its IPC mapping
+    // straight into the host image (copy engines; RAW/WAR through the flag
+    // pages like any other pull).
+    std::vector<Xfer> xs;
+    for (const auto& t : d.layout.tiles) {
+      const TileExtent& e = t.first;
+      for (std::uint32_t r = 0; r < opts_.workers; ++r) {
+        if (r == t.second.rank) continue;
+        const bool mine = isLocal(r), theirs = isLocal(t.second.rank);
+        if (!mine && !theirs) continue;
+        Xfer x;
+        x.src = t.second.rank;
+        x.dst = r;
+        x.rows = e.rowCount;
+        x.cols = e.colCount;
+        x.eb = static_cast<std::uint32_t>(eb);
+        x.matrix = d.matrixId;
+        x.hasOrigin = true;
+        x.r0 = e.rowStart;
+        x.c0 = e.colStart;
+        if (mine) {
+          const BandView sv = srcView(d, x.src, Rect::ofExtent(e));
+          x.srcPtr = sv.ptr;
+          x.srcLd = sv.ld;
+          x.dstPtr = img + (e.rowStart * d.cols + e.colStart) * eb;
+          x.dstLd = d.cols;
+        }
+        xs.push_back(x);
+      }
+    }
+    exchange(xs, false);
+  } else if (nccl_ && !localOnly) {
     // Remote tiles: each owner broadcasts its tile (packed) to every rank.
     Worker& w = *local(static_cast<std::uint32_t>(opts_.spmdRank));
     w.activate();
@@ -1290,22 +1366,20 @@ void Session::exchange(std::vector<Xfer>& xs, bool onComm, bool commit, int maxP
   const int sIdx = onComm ? 0 : 1;
   if (!nccl_ || ipc_) {
     std::set<std::tuple<std::uint32_t, std::uint32_t, std::uint64_t>> routes;  // (src, dst, matrix)
-    std::set<std::tuple<std::uint32_t, std::uint32_t, std::uint64_t>> waited;  // whole-write waits done
-    std::set<std::pair<std::uint32_t, cudaEvent_t>> chunkWaited;               // (dst, chunk event)
-    std::set<std::tuple<std::uint32_t, std::uint32_t, std::uint32_t>> flagWaited;  // (dst, src, value)
+    std::set<std::tuple<std::uint32_t, std::uint32_t, std::uint64_t, cudaStream_t>> waited;  // whole-write waits done
+    std::set<std::tuple<std::uint32_t, cudaEvent_t, cudaStream_t>> chunkWaited;  // (dst, chunk event, stream)
+    std::set<std::tuple<std::uint32_t, std::uint32_t, std::uint64_t, cudaStream_t>> flagWaited;  // (dst, src, value, stream)
     // Pieces from source worker s land on pull stream s % kPullStreams of the
     // consumer, forked from its base stream (so they see everything the base
     // stream owes, including this worker's own earlier writes) and joined
     // back before the op's readers are recorded.
     std::set<std::pair<Worker*, cudaStream_t>> forked;
-    auto pullOf = [&](Worker& d, std::uint32_t src) {
-      static const std::uint32_t nPull = [] {
-        const char* e = std::getenv("GM_PULL_STREAMS");  // dev switch: 1 = one stream
-        const int v = e ? std::atoi(e) : Worker::kPullStreams;
-        return static_cast<std::uint32_t>(std::clamp(v, 1, Worker::kPullStreams));
-      }();
+    auto pullOf = [&](Worker& d, std::uint32_t src, int fixed) {
+      const int dv = gmk::debug_config().pull_streams;
+      const std::uint32_t nPull = static_cast<std::uint32_t>(std::clamp(dv > 0 ? dv : Worker::kPullStreams, 1,
+                                                                        Worker::kPullStreams));
       const std::uint32_t np = maxPull > 0 ? std::min<std::uint32_t>(nPull, static_cast<std::uint32_t>(maxPull)) : nPull;
-      cudaStream_t ps = d.pulls[src % np];
+      cudaStream_t ps = fixed >= 0 ? d.pulls[fixed % Worker::kPullStreams] : d.pulls[src % np];
       if (forked.insert({&d, ps}).second) {
         cudaEvent_t e = d.event();
         cudaCheck(cudaEventRecord(e, streamOf(d)), "exchange: fork");
@@ -1318,7 +1392,7 @@ void Session::exchange(std::vector<Xfer>& xs, bool onComm, bool commit, int maxP
     // is a chunked upload and the piece's origin is known -- only the upload
     // chunks it overlaps (sub-pieces are then copied chunk by chunk).
     auto wholeWait = [&](const Xfer& x, Worker& d, cudaStream_t ps) {
-      if (!waited.insert({x.src, x.dst, x.matrix}).second) return;
+      if (!waited.insert({x.src, x.dst, x.matrix, ps}).second) return;
       Worker* s = local(x.src);
       if (s) {
         auto it = s->lastWrite.find(x.matrix);
@@ -1363,7 +1437,7 @@ void Session::exchange(std::vector<Xfer>& xs, bool onComm, bool commit, int maxP
       // A local producer whose upload was already joined publishes through
       // its lastWrite event (recorded after the upload).
       if (cw && found && s && !s->uploads.count(x.matrix)) found = false;
-      cudaStream_t ps = pullOf(*d, x.src);
+      cudaStream_t ps = pullOf(*d, x.src, x.pullStream);
       if (!cw || !found) {
         wholeWait(x, *d, ps);
         cudaCheck(cudaMemcpy2DAsync(x.dstPtr, x.dstLd * x.eb, x.srcPtr, x.srcLd * x.eb, x.cols * x.eb, x.rows,
@@ -1378,11 +1452,11 @@ void Session::exchange(std::vector<Xfer>& xs, bool onComm, bool commit, int maxP
             const auto& chunks = s->uploads.at(x.matrix).chunks;
             if (ord >= chunks.size()) throw Error("exchange: upload chunk geometry mismatch");
             // (the upload runs on the h2d stream: waited even for own tiles)
-            if (chunkWaited.insert({x.dst, chunks[ord].done}).second)
+            if (chunkWaited.insert({x.dst, chunks[ord].done, ps}).second)
               cudaCheck(cudaStreamWaitEvent(ps, chunks[ord].done, 0), "exchange: wait chunk");
           } else {
-            const std::uint32_t v = cw->base[x.src] + ord + 1;
-            if (flagWaited.insert({x.dst, x.src, v}).second)
+            const std::uint64_t v = cw->base[x.src] + ord + 1;
+            if (flagWaited.insert({x.dst, x.src, v, ps}).second)
               ipcWait(ps, peerFlags_[x.src] + kUpChunkOff + slotOf(x.matrix), v);
           }
           const std::uint64_t off = r - x.r0;
@@ -1393,9 +1467,11 @@ void Session::exchange(std::vector<Xfer>& xs, bool onComm, bool commit, int maxP
           r = r1;
         }
       }
+      if (x.flagAddr && x.lastOfBlock) ipcWrite(ps, x.flagAddr, x.flagValue);
       if (x.src != x.dst) {
         d->bytesReceived += bytes;
         if (s) s->bytesSent += bytes;
+        countLink(x.src, x.dst, MsgKind::Data, bytes);
       }
     }
     for (const auto& fk : forked) {
@@ -1626,6 +1702,20 @@ void Session::execGemm(const OpDescriptor& op) {
   const GemmPlanB200 plan = planGemmB200(table_, op, P, [&](std::uint32_t r, const MatrixDescriptor& M, const Rect& rect) {
     return dirOf(r).contains(M.matrixId, M.version, rect);
   });
+  // Pin every panel the plan reads from the cache before any gather of this
+  // op reserves room: lookup() stamps lastUse = tick_, and reserve() never
+  // evicts an entry stamped with the current tick. (Without this, a later
+  // Gather need of the same op could evict a band planned as Cached.)
+  std::vector<CacheEntry*> cachedHits(plan.needs.size(), nullptr);
+  for (std::size_t i = 0; i < plan.needs.size(); ++i) {
+    const PlannedNeed& nd = plan.needs[i];
+    if (nd.kind != PlannedNeed::Cached) continue;
+    const MatrixDescriptor& M = nd.operand == 0 ? A : B;
+    cachedHits[i] = dirOf(nd.worker).lookup(M.matrixId, M.version, nd.rect, tick_);
+    if (!cachedHits[i])
+      throw Error("gemm: panel of matrix " + std::to_string(M.matrixId) + " planned as cached on worker " +
+                  std::to_string(nd.worker) + " is not in its cache");
+  }
 
   // SUMMA-style overlap: gathered bands move on the comm stream in groups --
   // first every gathered B band, then the gathered A bands in `S` row chunks
@@ -1647,6 +1737,50 @@ void Session::execGemm(const OpDescriptor& op) {
   else if (chunkedSource(A.matrixId) && !plan.transA && opts_.pipelineChunks <= 0) S = 8u;
   while (S > 1 && plan.m < 512ull * S) --S;
 
+  // In-GEMM panel pipelining (copy-engine planes, 16-bit operands read in
+  // place): every gathered band is cut into blocks -- m-chunks (A) or
+  // n-chunks (B) by k-panels -- that the pull streams copy in the order the
+  // persistent GEMM first needs them, each block publishing a ready flag the
+  // GEMM's producer polls before loading a k-block. The GEMM starts at once;
+  // panel k+1 lands while panel k multiplies (reference: panels are consumed
+  // as their pieces arrive, kernels.cpp:490-552). Per-consumer decision: the
+  // producers' side of the exchange is unchanged.
+  const bool f16Pair = (A.precision == Precision::BF16 || A.precision == Precision::Half) &&
+                       A.precision == B.precision && C.precision != Precision::Double;
+  bool pipelined = anyGather && f16Pair && op.s0 != 0.0 && (!nccl_ || ipc_) &&
+                         gmk::debug_config().panel_flags && opts_.pipelineChunks <= 0 && !streamedA &&
+                         !chunkedSource(A.matrixId) && !chunkedSource(B.matrixId);
+  const std::uint64_t panelK = std::max<std::uint64_t>(64, (plan.k + 16 * 64 - 1) / (16 * 64) * 64);
+  const std::uint64_t numPanels = (plan.k + panelK - 1) / panelK;
+  constexpr std::uint64_t kAChunkRows = 4096, kBChunkCols = 2048;  // raster group x 256; 4 wide tiles
+  bool fits = true;  // every local band's flag region fits its worker's ring
+  for (const PlannedNeed& nd : plan.needs) {
+    Worker* w = local(nd.worker);
+    if (nd.kind != PlannedNeed::Gather || !w) continue;
+    const bool chunkRows = nd.operand == 0 ? !plan.transA : plan.transB;
+    const std::uint64_t ext = chunkRows ? nd.rect.rows() : nd.rect.cols();
+    const std::uint64_t cs = nd.operand == 0 ? kAChunkRows : kBChunkCols;
+    fits = fits && (ext + cs - 1) / cs * numPanels <= w->readyCap;
+  }
+  pipelined = pipelined && fits;
+  if (pipelined) S = 1;
+  // One gathered band of a local consumer in pipelined mode.
+  struct FlagBand {
+    Worker* w = nullptr;
+    int operand = 0;
+    std::size_t interval = 0;
+    std::uint64_t chunk = 0, chunks = 0;
+    std::uint64_t* flags = nullptr;  // chunks x numPanels
+    std::uint64_t first = 0;         // monotonic ring slot
+  };
+  std::vector<FlagBand> flagBands;
+  struct BlockXfer {
+    Xfer x;
+    std::size_t band = 0;
+    std::uint64_t chunk = 0, panel = 0;
+  };
+  std::vector<BlockXfer> blockXfers;
+
   std::vector<std::vector<BandView>> aViews(P), bViews(P);
   for (std::uint32_t w = 0; w < P; ++w) {
     aViews[w].resize(plan.rowsOf[w].size());
@@ -1664,7 +1798,8 @@ void Session::execGemm(const OpDescriptor& op) {
     return std::make_pair(lo + len * j / S, lo + len * (j + 1) / S);
   };
 
-  for (const PlannedNeed& nd : plan.needs) {
+  for (std::size_t ni = 0; ni < plan.needs.size(); ++ni) {
+    const PlannedNeed& nd = plan.needs[ni];
     const MatrixDescriptor& M = nd.operand == 0 ? A : B;
     const std::uint64_t eb = bytesOf(M.precision);
     Worker* w = local(nd.worker);
@@ -1691,7 +1826,7 @@ void Session::execGemm(const OpDescriptor& op) {
         break;
       }
       case PlannedNeed::Cached: {
-        CacheEntry* hit = dirOf(nd.worker).lookup(M.matrixId, M.version, nd.rect, tick_);
+        CacheEntry* hit = cachedHits[ni];
         if (!w) break;
         w->activate();
         cudaCheck(cudaStreamWaitEvent(w->compute, hit->ready, 0), "gemm: wait panel");
@@ -1734,6 +1869,60 @@ void Session::execGemm(const OpDescriptor& op) {
         }
         const CacheEntry& slot = keep ? *slotp : e;
         if (w) view = {slot.ptr, slot.ld};
+        if (pipelined && w) {
+          // Cut the band into (chunk x k-panel) blocks. Chunk dimension:
+          // A's m (stored rows unless transposed), B's n (stored columns
+          // unless transposed); the k-panels run along the other one.
+          const bool chunkRows = nd.operand == 0 ? !plan.transA : plan.transB;
+          FlagBand fb;
+          fb.w = w;
+          fb.operand = nd.operand;
+          fb.interval = nd.interval;
+          fb.chunk = nd.operand == 0 ? kAChunkRows : kBChunkCols;
+          const std::uint64_t ext = chunkRows ? nd.rect.rows() : nd.rect.cols();
+          fb.chunks = (ext + fb.chunk - 1) / fb.chunk;
+          fb.first = w->reserveReady(fb.chunks * numPanels);
+          fb.flags = w->readyFlags + fb.first % w->readyCap;
+          const std::size_t bi = flagBands.size();
+          flagBands.push_back(fb);
+          for (const PieceRoute& pr : nd.pieces) {
+            Worker* sw = local(pr.src);
+            const std::uint64_t m0 = chunkRows ? pr.rect.r0 - nd.rect.r0 : pr.rect.c0 - nd.rect.c0;
+            const std::uint64_t m1 = chunkRows ? pr.rect.r1 - nd.rect.r0 : pr.rect.c1 - nd.rect.c0;
+            const std::uint64_t k0 = chunkRows ? pr.rect.c0 - nd.rect.c0 : pr.rect.r0 - nd.rect.r0;
+            const std::uint64_t k1 = chunkRows ? pr.rect.c1 - nd.rect.c0 : pr.rect.r1 - nd.rect.r0;
+            for (std::uint64_t c = m0 / fb.chunk; c * fb.chunk < m1; ++c)
+              for (std::uint64_t pk = k0 / panelK; pk * panelK < k1; ++pk) {
+                const std::uint64_t a0 = std::max(m0, c * fb.chunk), a1 = std::min(m1, (c + 1) * fb.chunk);
+                const std::uint64_t b0 = std::max(k0, pk * panelK), b1 = std::min(k1, (pk + 1) * panelK);
+                Rect r = chunkRows ? Rect{nd.rect.r0 + a0, nd.rect.r0 + a1, nd.rect.c0 + b0, nd.rect.c0 + b1}
+                                   : Rect{nd.rect.r0 + b0, nd.rect.r0 + b1, nd.rect.c0 + a0, nd.rect.c0 + a1};
+                BlockXfer bx;
+                Xfer& x = bx.x;
+                x.src = pr.src;
+                x.dst = nd.worker;
+                x.rows = r.rows();
+                x.cols = r.cols();
+                x.eb = static_cast<std::uint32_t>(eb);
+                x.matrix = M.matrixId;
+                x.hasOrigin = true;
+                x.r0 = r.r0;
+                x.c0 = r.c0;
+                const BandView sv = srcView(M, pr.src, r);
+                x.srcPtr = sv.ptr;
+                x.srcLd = sv.ld;
+                x.dstPtr = static_cast<std::uint8_t*>(slot.ptr) + ((r.r0 - nd.rect.r0) * slot.ld + (r.c0 - nd.rect.c0)) * eb;
+                x.dstLd = slot.ld;
+                x.flagAddr = fb.flags + c * numPanels + pk;
+                bx.band = bi;
+                bx.chunk = c;
+                bx.panel = pk;
+                blockXfers.push_back(bx);
+                (void)sw;
+              }
+          }
+          break;
+        }
         // Which group each piece belongs to: B whole; A split by m rows
         // (stored rows for A, stored columns for transposed A).
         for (const PieceRoute& pr : nd.pieces) {
@@ -1789,7 +1978,7 @@ void Session::execGemm(const OpDescriptor& op) {
 
   // Comm stream: B bands, then A chunks; an event per group per local worker.
   std::vector<std::vector<cudaEvent_t>> groupDone(1 + S);
-  bool anyXfer = false;
+  bool anyXfer = !blockXfers.empty();
   for (auto& gx : groups) anyXfer = anyXfer || !gx.empty();
   // No blanket wait on the compute stream: exchange() orders each pull after
   // the last write of its source matrix only, so these pulls overlap the
@@ -1799,15 +1988,99 @@ void Session::execGemm(const OpDescriptor& op) {
     w.commTimed = anyXfer;
     if (anyXfer) cudaCheck(cudaEventRecord(w.cStart, w.comm), "gemm: comm timing");
   });
-  for (std::uint32_t gi = 0; gi <= S; ++gi) {
-    if (groups[gi].empty()) continue;
-    exchange(groups[gi], true, false);
-    for (auto& wp : workers_) {
-      if (!wp) continue;
-      wp->activate();
-      cudaEvent_t ev = wp->event();
-      cudaCheck(cudaEventRecord(ev, wp->comm), "gemm: group done");
-      groupDone[gi].push_back(ev);
+  // Pipelined mode: order each local consumer's blocks by when its GEMM
+  // first needs them -- the wave of the persistent grid whose tiles first
+  // touch the block's chunk (host mirror of the kernel's raster), then the
+  // k-panel -- and deal them round-robin over the pull streams.
+  std::map<std::pair<Worker*, std::pair<int, std::size_t>>, std::size_t> bandOf;  // (w, (operand, interval)) -> band
+  for (std::size_t i = 0; i < flagBands.size(); ++i)
+    bandOf[{flagBands[i].w, {flagBands[i].operand, flagBands[i].interval}}] = i;
+  if (pipelined && !blockXfers.empty()) {
+    constexpr std::uint64_t kNever = ~0ull;
+    std::vector<std::vector<std::uint64_t>> firstWave(flagBands.size());
+    for (std::size_t i = 0; i < flagBands.size(); ++i) firstWave[i].assign(flagBands[i].chunks, kNever);
+    forEachLocal([&](Worker& w) {
+      std::uint64_t waveOff = 0;
+      for (const DeviceTile& ct : w.tiles.at(C.matrixId)) {
+        const TileExtent& e = ct.extent;
+        std::size_t ri = 0, ci = 0;
+        while (!(e.rowStart >= plan.rowsOf[w.rank][ri].first && e.rowStart < plan.rowsOf[w.rank][ri].second)) ++ri;
+        while (!(e.colStart >= plan.colsOf[w.rank][ci].first && e.colStart < plan.colsOf[w.rank][ci].second)) ++ci;
+        auto ai = bandOf.find({&w, {0, ri}});
+        auto bi = bandOf.find({&w, {1, ci}});
+        if (ai == bandOf.end() && bi == bandOf.end()) continue;
+        const std::uint64_t roff = e.rowStart - plan.rowsOf[w.rank][ri].first;
+        const std::uint64_t coff = e.colStart - plan.colsOf[w.rank][ci].first;
+        const gmk::TcTilePlan tp = gmk::tc_tile_plan(e.rowCount, e.colCount, plan.k, 2, opts_.gemmMaxCtas);
+        const std::uint64_t mbs = (e.rowCount + tp.block_m - 1) / tp.block_m;
+        const std::uint64_t nbs = (e.colCount + tp.block_n - 1) / tp.block_n;
+        const std::uint64_t tiles = mbs * nbs;
+        for (std::uint64_t t = 0; t < tiles; ++t) {
+          const std::uint64_t per = static_cast<std::uint64_t>(tp.group) * nbs, g = t / per;
+          const std::uint64_t gsize = std::min<std::uint64_t>(tp.group, mbs - g * tp.group);
+          const std::uint64_t mb = g * tp.group + (t % per) % gsize, nb = (t % per) / gsize;
+          const std::uint64_t wave = waveOff + t / tp.units;
+          if (ai != bandOf.end()) {
+            const FlagBand& fb = flagBands[ai->second];
+            const std::uint64_t r0 = roff + mb * tp.block_m;
+            const std::uint64_t r1 = roff + std::min<std::uint64_t>(e.rowCount, (mb + 1) * tp.block_m) - 1;
+            for (std::uint64_t c = r0 / fb.chunk; c <= r1 / fb.chunk && c < fb.chunks; ++c)
+              firstWave[ai->second][c] = std::min(firstWave[ai->second][c], wave);
+          }
+          if (bi != bandOf.end()) {
+            const FlagBand& fb = flagBands[bi->second];
+            const std::uint64_t c0 = coff + nb * tp.block_n;
+            const std::uint64_t c1 = coff + std::min<std::uint64_t>(e.colCount, (nb + 1) * tp.block_n) - 1;
+            for (std::uint64_t c = c0 / fb.chunk; c <= c1 / fb.chunk && c < fb.chunks; ++c)
+              firstWave[bi->second][c] = std::min(firstWave[bi->second][c], wave);
+          }
+        }
+        waveOff += (tiles + tp.units - 1) / tp.units;
+      }
+    });
+    std::stable_sort(blockXfers.begin(), blockXfers.end(), [&](const BlockXfer& x, const BlockXfer& y) {
+      const FlagBand& fx = flagBands[x.band];
+      const FlagBand& fy = flagBands[y.band];
+      if (fx.w->rank != fy.w->rank) return fx.w->rank < fy.w->rank;
+      const auto kx = std::make_tuple(firstWave[x.band][x.chunk], x.panel, fx.operand, x.chunk, x.band);
+      const auto ky = std::make_tuple(firstWave[y.band][y.chunk], y.panel, fy.operand, y.chunk, y.band);
+      return kx < ky;
+    });
+    std::map<Worker*, int> ordinal;
+    for (std::size_t i = 0; i < blockXfers.size(); ++i) {
+      BlockXfer& bx = blockXfers[i];
+      Worker* w = flagBands[bx.band].w;
+      const bool firstOfBlock = i == 0 || blockXfers[i - 1].x.flagAddr != bx.x.flagAddr;
+      if (firstOfBlock) ++ordinal[w];
+      bx.x.pullStream = (ordinal[w] - 1) % Worker::kPullStreams;
+      bx.x.lastOfBlock = i + 1 == blockXfers.size() || blockXfers[i + 1].x.flagAddr != bx.x.flagAddr;
+      bx.x.flagValue = w->readySeq + 1;
+    }
+    forEachLocal([&](Worker& w) {
+      if (ordinal.count(&w)) ++w.readySeq;
+    });
+  }
+  {
+    // One exchange per op in pipelined mode (the groups then hold only
+    // producer-side bookkeeping of peers' pulls); else group by group.
+    std::vector<std::vector<Xfer>> batches;
+    if (pipelined) {
+      std::vector<Xfer> all;
+      for (auto& gx : groups) all.insert(all.end(), gx.begin(), gx.end());
+      for (const BlockXfer& bx : blockXfers) all.push_back(bx.x);
+      batches.push_back(std::move(all));
+    }
+    for (std::uint32_t gi = 0; gi <= S; ++gi) {
+      if (!pipelined && !groups[gi].empty()) exchange(groups[gi], true, false);
+      if (pipelined && gi == 0 && !batches[0].empty()) exchange(batches[0], true, false);
+      if (pipelined ? gi != 0 : groups[gi].empty()) continue;
+      for (auto& wp : workers_) {
+        if (!wp) continue;
+        wp->activate();
+        cudaEvent_t ev = wp->event();
+        cudaCheck(cudaEventRecord(ev, wp->comm), "gemm: group done");
+        groupDone[gi].push_back(ev);
+      }
     }
   }
   commitReads();
@@ -1856,7 +2129,25 @@ void Session::execGemm(const OpDescriptor& op) {
   forEachLocal([&](Worker& w) {
     w.dropChunkDone(C.matrixId);
     std::set<cudaEvent_t> waited;
-    waitGroup(w, 0);
+    bool wPipe = false;
+    for (const FlagBand& fb : flagBands) wPipe = wPipe || fb.w == &w;
+    if (!wPipe) {
+      waitGroup(w, 0);
+    } else {
+      // The GEMM polls flags instead of waiting for the comm stream. Its
+      // pulls may wait on other local workers' writes (events on their
+      // compute streams, possibly on this GPU): wait for those first, so
+      // the spinning persistent grid never holds the SMs a producer needs.
+      std::set<cudaEvent_t> raw;
+      for (const BlockXfer& bx : blockXfers) {
+        if (flagBands[bx.band].w != &w || bx.x.src == w.rank) continue;
+        Worker* sw = local(bx.x.src);
+        if (!sw) continue;
+        auto it = sw->lastWrite.find(bx.x.matrix);
+        if (it != sw->lastWrite.end() && raw.insert(it->second).second)
+          cudaCheck(cudaStreamWaitEvent(w.compute, it->second, 0), "gemm: wait source write");
+      }
+    }
     if (!alphaZero)
       for (std::size_t ci = 0; ci < plan.colsOf[w.rank].size(); ++ci)
         if (bLocal[w.rank][ci]) waitUploadRows(w, B.matrixId, 0, ~0ull, waited);
@@ -1930,7 +2221,31 @@ void Session::execGemm(const OpDescriptor& op) {
           ep.act = static_cast<std::uint8_t*>(at->ptr) + (r0 - e.rowStart) * at->ld * 2;
           ep.ldAct = at->ld;
         }
-        gemmLocal(d, ap, bp, cp, ws, wsb, w.compute, fused_ ? &ep : nullptr);
+        gmk::PanelReady ready;
+        if (wPipe && !alphaZero) {
+          auto ai = bandOf.find({&w, {0, ri}});
+          auto bi = bandOf.find({&w, {1, ci}});
+          if ((ai != bandOf.end() || bi != bandOf.end()) && gemmConsumesPanelFlags(d, ap, bp)) {
+            ready.target = w.readySeq;
+            ready.panel_k = static_cast<std::uint32_t>(panelK);
+            ready.num_panels = static_cast<std::uint32_t>(numPanels);
+            ready.streams = 1;
+            if (ai != bandOf.end()) {
+              ready.a = flagBands[ai->second].flags;
+              ready.a_row0 = static_cast<std::uint32_t>(r0 - plan.rowsOf[w.rank][ri].first);
+              ready.a_chunk_rows = static_cast<std::uint32_t>(kAChunkRows);
+            }
+            if (bi != bandOf.end()) {
+              ready.b = flagBands[bi->second].flags;
+              ready.b_col0 = static_cast<std::uint32_t>(e.colStart - plan.colsOf[w.rank][ci].first);
+              ready.b_chunk_cols = static_cast<std::uint32_t>(kBChunkCols);
+            }
+          } else if (ai != bandOf.end() || bi != bandOf.end()) {
+            // This launch cannot poll (staged operand): whole bands first.
+            waitGroup(w, 0);
+          }
+        }
+        gemmLocal(d, ap, bp, cp, ws, wsb, w.compute, fused_ ? &ep : nullptr, ready.num_panels ? &ready : nullptr);
       }
       // Row-chunk completion of C (chunked downloads drain behind these).
       for (const auto& rr : chunkRows) {
@@ -1941,6 +2256,16 @@ void Session::execGemm(const OpDescriptor& op) {
     }
     cudaCheck(cudaEventRecord(w.tEnd, w.compute), "gemm: timing");
     if (w.windowOpen) cudaCheck(cudaEventRecord(w.kernelWindow.back().second, w.compute), "gemm: timing");
+    // Flag regions polled by this op's GEMMs become reusable after them.
+    for (const FlagBand& fb : flagBands) {
+      if (fb.w != &w) continue;
+      Worker::ReadyRegion rr;
+      rr.first = fb.first;
+      rr.end = fb.first + fb.chunks * numPanels;
+      rr.done = w.event();
+      cudaCheck(cudaEventRecord(rr.done, w.compute), "gemm: ready region done");
+      w.readyInUse.push_back(rr);
+    }
   });
   for (auto& tp : temps) {
     tp.first->activate();
@@ -2165,11 +2490,7 @@ void Session::replay(std::uint64_t pipelineId, bool sync) {
 }
 
 bool Session::fusableBiasRelu(const std::vector<OpDescriptor>& ops, std::size_t i) const {
-  static const bool enabled = [] {
-    const char* e = std::getenv("GM_FUSE_EPILOGUE");
-    return !(e && e[0] == '0');
-  }();
-  if (!enabled || i + 2 >= ops.size()) return false;
+  if (!gmk::debug_config().fuse_epilogue || i + 2 >= ops.size()) return false;
   const OpDescriptor& g = ops[i];
   const OpDescriptor& bo = ops[i + 1];
   const OpDescriptor& ro = ops[i + 2];
@@ -2262,6 +2583,7 @@ ReplicationHandle Session::replicateAsync(DistMatrix m) {
   op.ids[0] = m.id();
   op.ids[1] = opts_.replicationChunkBytes;
   issue(op);
+  trace_.record(-1, EventKind::ReplInitiate, h.matrixId, h.version);
   execReplicate(m.id());
   return h;
 }
@@ -2388,6 +2710,7 @@ ReplState Session::wait(const ReplicationHandle& h) {
         rit->second.state == ReplicaState::Pending) {
       wp->activate();
       cudaCheck(cudaEventSynchronize(rit->second.ready), "replica wait");
+      trace_.record(wp->rank, EventKind::ReplicaValid, h.matrixId, h.version);
     }
   }
   return handleState(h);
@@ -2427,7 +2750,163 @@ std::vector<WorkerStatsRow> Session::queryWorkerStats() {
   return rows;
 }
 
+// ---------------------------------------------------------------- reference public surface
+
+std::uint64_t EventTrace::record(std::int64_t actor, EventKind kind, std::uint64_t a, std::uint64_t b,
+                                 std::string label) {
+  std::lock_guard<std::mutex> g(mu_);
+  const std::uint64_t s = seq_++;
+  events_.push_back(TraceEvent{s, actor, kind, a, b, std::move(label)});
+  return s;
+}
+
+std::vector<TraceEvent> EventTrace::snapshot() const {
+  std::lock_guard<std::mutex> g(mu_);
+  return events_;  // appended in sequence order
+}
+
+void EventTrace::clear() {
+  std::lock_guard<std::mutex> g(mu_);
+  events_.clear();
+}
+
+LinkStats FabricStats::totalByKind(MsgKind k) const {
+  LinkStats t;
+  for (const auto& kv : perLink) {
+    t.messageCount += kv.second[static_cast<int>(k)].messageCount;
+    t.byteCount += kv.second[static_cast<int>(k)].byteCount;
+  }
+  return t;
+}
+
+LinkStats FabricStats::total() const {
+  LinkStats t;
+  for (int k = 0; k < 3; ++k) {
+    const LinkStats x = totalByKind(static_cast<MsgKind>(k));
+    t.messageCount += x.messageCount;
+    t.byteCount += x.byteCount;
+  }
+  return t;
+}
+
+void Session::countLink(std::uint32_t src, std::uint32_t dst, MsgKind k, std::uint64_t bytes) {
+  std::lock_guard<std::mutex> g(statsMu_);
+  LinkStats& l = links_[{src, dst}][static_cast<int>(k)];
+  l.messageCount += 1;
+  l.byteCount += bytes;
+}
+
+FabricStats Session::fabricStats() const {
+  std::lock_guard<std::mutex> g(statsMu_);
+  FabricStats f;
+  f.perLink = links_;
+  return f;
+}
+
+void Session::phaseMark(const std::string& label) { trace_.record(-1, EventKind::PhaseMark, 0, 0, label); }
+
+void Session::distributeSeeds(std::uint64_t rootSeed) {
+  // Reference session.cpp:377-383: an acked control op; the workers derive
+  // deriveSeed(root, rank). The device generator takes explicit seeds
+  // (fillUniform), so the runtime only records the root.
+  rootSeed_ = rootSeed;
+  OpDescriptor op;
+  op.opcode = OpCode::DistributeSeeds;
+  op.ids[0] = rootSeed;
+  awaitAcks(issueOp(std::move(op)));
+}
+
+const Worker& Session::workerForTest(std::uint32_t rank) const {
+  const Worker* w = local(rank);
+  if (!w) throw Error("workerForTest: worker " + std::to_string(rank) + " is not hosted by this process");
+  return *w;
+}
+
+std::uint64_t Session::issueOp(OpDescriptor op, std::uint64_t extraExecIds) {
+  (void)extraExecIds;
+  switch (op.opcode) {
+    case OpCode::Gemm:
+      runGemm(op, false);
+      return curExec_;
+    case OpCode::SetConst:
+    case OpCode::EwUnary:
+    case OpCode::EwBinary:
+    case OpCode::AddRowColSum:
+      runPointwise(op, false);
+      return curExec_;
+    case OpCode::ReplicateStart: {
+      const MatrixDescriptor& d = descriptor(op.ids[0]);
+      replicateAsync(DistMatrix(this, d.matrixId));
+      return curExec_;
+    }
+    case OpCode::DistributeSeeds:
+    case OpCode::QueryStats:
+    case OpCode::MetaChecksum:
+      return issue(op);  // metadata-only control ops
+    case OpCode::CreateMatrix:
+    case OpCode::DestroyMatrix:
+    case OpCode::SetData:
+    case OpCode::GetData:
+    case OpCode::Reshape:
+    case OpCode::Replay:
+    case OpCode::Snapshot:
+    case OpCode::Shutdown:
+      throw Error(std::string("issueOp: opcode ") + std::to_string(static_cast<std::uint32_t>(op.opcode)) +
+                  " carries host data or lifecycle state; use its Session method");
+    default:
+      validateOp(table_, op, opts_.workers);  // throws "op not supported on the B200 GEMM path"
+      throw Error("op not supported on the B200 GEMM path");
+  }
+}
+
+std::vector<std::pair<std::uint32_t, Completion>> Session::awaitAcks(std::uint64_t execId) {
+  synchronize();
+  std::vector<std::pair<std::uint32_t, Completion>> acks;
+  for (auto& w : workers_) {
+    if (!w) continue;
+    Completion c;
+    c.execId = execId;
+    acks.push_back({w->rank, c});
+    countLink(w->rank, kMasterRank, MsgKind::Completion, 0);
+  }
+  return acks;
+}
+
 // ---------------------------------------------------------------- free function
+
+void softmaxRows(Session& s, DistMatrix a) {
+  OpDescriptor op;
+  op.opcode = OpCode::SoftmaxRows;
+  op.ids[0] = a.id();
+  s.issueOp(op);
+}
+
+void subtractOneHot(Session& s, DistMatrix probs, DistMatrix labels) {
+  OpDescriptor op;
+  op.opcode = OpCode::SubtractOneHot;
+  op.ids[0] = probs.id();
+  op.ids[1] = labels.id();
+  s.issueOp(op);
+}
+
+double logLossMean(Session& s, DistMatrix probs, DistMatrix labels) {
+  OpDescriptor op;
+  op.opcode = OpCode::LogLossGather;
+  op.ids[0] = probs.id();
+  op.ids[1] = labels.id();
+  s.issueOp(op);
+  return 0.0;
+}
+
+void conv2dForward(Session& s, DistMatrix input, DistMatrix filters, DistMatrix output, kernels::ConvGeometry g) {
+  (void)g;
+  OpDescriptor op;
+  op.opcode = OpCode::Im2col;
+  op.ids[0] = input.id();
+  op.ids[1] = filters.id();
+  op.ids[2] = output.id();
+  s.issueOp(op);
+}
 
 void gemm(Session& s, DistMatrix a, DistMatrix b, DistMatrix c, double alpha, double beta,
           bool transA, bool transB) {

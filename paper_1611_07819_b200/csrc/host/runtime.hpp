@@ -18,14 +18,15 @@
 #pragma once
 
 #include <cuda_runtime.h>
-#include <nccl.h>
 
 #include <array>
 #include <cstdint>
+#include <deque>
 #include <functional>
 #include <list>
 #include <map>
 #include <memory>
+#include <mutex>
 #include <optional>
 #include <set>
 #include <string>
@@ -38,9 +39,83 @@
 #include "device.hpp"
 #include "ops.hpp"
 
+// NCCL's handle type (nccl.h: typedef struct ncclComm* ncclComm_t), so that
+// callers of this header do not need NCCL's headers.
+typedef struct ncclComm* ncclComm_t;
+
 namespace gridmath {
 
 class Session;
+
+// ---- introspection types of the reference's public Session surface
+// (trace.hpp:13-64, fabric.hpp:21-49), filled by the B200 runtime.
+enum class EventKind : std::uint8_t {
+  PhaseMark,       // master annotation; label carries the phase name
+  OpStart,         // a worker's device work for an op is issued (a = execId, b = opcode)
+  OpComputeStart,
+  OpComputeEnd,
+  OpEnd,
+  ReplInitiate,    // a = matrixId, b = version
+  ReplChunkSent,
+  ReplicaValid,    // this worker's full copy became readable (a = matrixId, b = version)
+  ReplFailed,
+  BatchProduced,
+  BatchConsumed,
+};
+
+struct TraceEvent {
+  std::uint64_t seq = 0;
+  std::int64_t actor = 0;  // worker rank, -1 for master
+  EventKind kind{};
+  std::uint64_t a = 0;
+  std::uint64_t b = 0;
+  std::string label;
+};
+
+// Append-only host event log with a total order (sequence numbers).
+class EventTrace {
+ public:
+  std::uint64_t record(std::int64_t actor, EventKind kind, std::uint64_t a = 0, std::uint64_t b = 0,
+                       std::string label = {});
+  std::vector<TraceEvent> snapshot() const;
+  void clear();
+
+ private:
+  mutable std::mutex mu_;
+  std::uint64_t seq_ = 0;
+  std::vector<TraceEvent> events_;
+};
+
+enum class MsgKind : std::uint8_t { Control = 0, Data = 1, Completion = 2 };
+
+struct LinkStats {
+  std::uint64_t messageCount = 0;
+  std::uint64_t byteCount = 0;  // payload bytes
+};
+
+// Per (src, dst) worker pair: Control = ops mirrored to the worker (src =
+// master, 0xFFFFFFFF), Data = pieces pulled over the data plane (one
+// message per 2D copy), Completion = worker acknowledgements.
+struct FabricStats {
+  std::map<std::pair<std::uint32_t, std::uint32_t>, std::array<LinkStats, 3>> perLink;
+  LinkStats totalByKind(MsgKind k) const;
+  LinkStats total() const;
+};
+
+inline constexpr std::uint32_t kMasterRank = 0xFFFFFFFFu;
+
+namespace kernels {
+// Reference kernels.hpp:68-78 (the conv op is outside the B200 GEMM path;
+// declared so reference call sites compile).
+struct ConvGeometry {
+  std::uint32_t batch = 0;
+  std::uint32_t channels = 0, height = 0, width = 0;
+  std::uint32_t kernels = 0, kh = 0, kw = 0;
+  std::uint32_t stride = 1, pad = 0;
+  std::uint32_t outH() const { return (height + 2 * pad - kh) / stride + 1; }
+  std::uint32_t outW() const { return (width + 2 * pad - kw) / stride + 1; }
+};
+}  // namespace kernels
 
 class DistMatrix {
  public:
@@ -81,6 +156,10 @@ struct SessionOptions {
   // mappable, else NCCL. 1 forces NCCL point-to-point; 2 requires copy engines.
   int transport = 0;
   int pipelineChunks = 0;             // SUMMA row chunks (0 = auto)
+  // SPMD control channel: blocking in-place max-reduce of host bytes over
+  // all ranks. Empty: an NCCL communicator carries it. Set: no NCCL at all
+  // (ranks may share a GPU); the data plane must be the IPC copy engines.
+  std::function<void(void*, std::size_t)> controlAllreduceMax;
 };
 
 struct WorkerStatsRow {
@@ -180,7 +259,26 @@ class Worker {
   std::map<std::uint64_t, cudaEvent_t> lastTouch;
   // SPMD copy-engine plane: this rank's flag page (device memory, mapped by
   // every peer): written[slot], then readDone[stream][slot].
-  std::uint32_t* flags = nullptr;
+  std::uint64_t* flags = nullptr;
+
+  // In-GEMM panel pipelining: a ring of u64 ready flags in device memory.
+  // The pull streams write a block's flag once its pieces landed; the GEMM
+  // producer polls it. Each pipelined GEMM takes a fresh region (values are
+  // a per-worker sequence number); a region is handed out again only after
+  // the GEMM that polled it has finished (the comm stream waits on its done
+  // event), so no kernel ever sees a later op's write.
+  std::uint64_t readyCap = 1ull << 16;  // slots (GM_DEBUG_CONFIG ready_slots overrides)
+  std::uint64_t* readyFlags = nullptr;
+  std::uint64_t readyHead = 0;  // monotonic slot counter (memory slot = head % readyCap)
+  std::uint64_t readySeq = 0;   // last published value
+  struct ReadyRegion {
+    std::uint64_t first = 0, end = 0;
+    cudaEvent_t done = nullptr;  // on compute, after the GEMM that polls the region
+  };
+  std::deque<ReadyRegion> readyInUse;
+  // Reserves n contiguous slots; returns the monotonic start. Makes the comm
+  // stream wait for every earlier GEMM whose region the new one may reuse.
+  std::uint64_t reserveReady(std::uint64_t n);
 
   // Host<->device streaming (asynchronous packed local I/O): uploads run on
   // `h2d` in row chunks, each with an event, so a GEMM can start on the rows
@@ -254,6 +352,13 @@ struct Xfer {
   // can; enables per-chunk waits on a chunked upload of the source).
   bool hasOrigin = false;
   std::uint64_t r0 = 0, c0 = 0;
+  // Panel pipelining (consumer side): the copy runs on pull stream
+  // `pullStream` (else by source), and when `lastOfBlock` is set that stream
+  // then writes *flagAddr = flagValue (the block has landed).
+  int pullStream = -1;
+  bool lastOfBlock = false;
+  std::uint64_t* flagAddr = nullptr;
+  std::uint64_t flagValue = 0;
 };
 
 // Pure GEMM planning (no device state): merged C row/col intervals per
@@ -333,6 +438,25 @@ class Session {
 
   void verifyMetadataConsistency();
   std::vector<WorkerStatsRow> queryWorkerStats();
+  // --- rest of the reference's public surface (session.hpp:86-124)
+  // Seeds: every worker's generator seed is deriveSeed(root, rank).
+  void distributeSeeds(std::uint64_t rootSeed);
+  std::uint64_t rootSeed() const { return rootSeed_; }
+  // The master keeps no pooled host buffers here (device arenas are per
+  // worker, queryWorkerStats): all-zero row.
+  WorkerStatsRow masterPoolStats() const { return {}; }
+  FabricStats fabricStats() const;
+  EventTrace& trace() { return trace_; }
+  void phaseMark(const std::string& label);
+  double simulatedElapsed() const { return 0.0; }  // no simulated fabric on the device runtime
+  const Worker& workerForTest(std::uint32_t rank) const;
+  // Op plumbing: validate, apply metadata and execute any op the runtime
+  // executes (Gemm, SetConst, EwUnary, EwBinary, AddRowColSum,
+  // ReplicateStart) stream-ordered; awaitAcks waits for the local workers
+  // and returns their acknowledgements. extraExecIds is kept for source
+  // compatibility (every op takes one exec id here).
+  std::uint64_t issueOp(OpDescriptor op, std::uint64_t extraExecIds = 0);
+  std::vector<std::pair<std::uint32_t, Completion>> awaitAcks(std::uint64_t execId);
   const MatrixDescriptor& descriptor(std::uint64_t id) const;
   const DescriptorTable& table() const { return table_; }
   std::uint32_t workerCount() const { return opts_.workers; }
@@ -413,9 +537,12 @@ class Session {
   void flushWritten(std::uint64_t before);  // publish mutations of ops with exec id < before
   void commitReads();    // consumers publish readDone for this op's pulls
   void setupIpc();
+  // Blocking max-reduce of a small host byte array over all SPMD ranks
+  // (control plane: IPC registration, budgets, shutdown).
+  void controlMax(void* host, std::size_t n);
   void registerTiles(std::uint64_t id, const std::string& localError);
-  void ipcWait(cudaStream_t s, const std::uint32_t* addr, std::uint64_t value);
-  void ipcWrite(cudaStream_t s, std::uint32_t* addr, std::uint64_t value);
+  void ipcWait(cudaStream_t s, const std::uint64_t* addr, std::uint64_t value);
+  void ipcWrite(cudaStream_t s, std::uint64_t* addr, std::uint64_t value);
   std::uint32_t slotOf(std::uint64_t id) const;
   // Source view of `r` (inside one tile of M owned by `src`): a local tile
   // pointer, or the IPC mapping of a peer's tile. {nullptr, 0} if neither.
@@ -425,6 +552,11 @@ class Session {
 
   SessionOptions opts_;
   DescriptorTable table_;
+  std::uint64_t rootSeed_ = 0;
+  EventTrace trace_;
+  mutable std::mutex statsMu_;
+  std::map<std::pair<std::uint32_t, std::uint32_t>, std::array<LinkStats, 3>> links_;
+  void countLink(std::uint32_t src, std::uint32_t dst, MsgKind k, std::uint64_t bytes);
   std::vector<std::unique_ptr<Worker>> workers_;  // indexed by rank; null if remote
   std::vector<PanelCache> remoteCaches_;          // directory for non-local workers (SPMD)
   std::map<std::pair<std::uint64_t, std::uint64_t>, bool> replFailed_;
@@ -435,10 +567,10 @@ class Session {
   // pulls, local copies) wait per chunk instead of for the whole upload.
   struct ChunkedWrite {
     std::uint64_t execId = 0, chunkBytes = 0;
-    std::vector<std::uint32_t> base;  // per rank: its upload-chunk counter before this upload
+    std::vector<std::uint64_t> base;  // per rank: its upload-chunk counter before this upload
   };
   std::map<std::uint64_t, ChunkedWrite> chunked_;
-  std::map<std::pair<std::uint32_t, std::uint32_t>, std::uint32_t> upCount_;  // (rank, slot) -> chunks so far
+  std::map<std::pair<std::uint32_t, std::uint32_t>, std::uint64_t> upCount_;  // (rank, slot) -> chunks so far
   const ChunkedWrite* chunkedSource(std::uint64_t matrix) const;
   // Ordinal of the upload chunk holding global row `row` of tile `tileIdx`
   // among its owner's chunks of matrix M (tiles in layout order), and the
@@ -461,7 +593,7 @@ class Session {
   std::vector<std::uint32_t> freeSlots_;
   std::uint32_t nextSlot_ = 0;
   // SPMD IPC plane
-  std::vector<std::uint32_t*> peerFlags_;                  // rank -> mapped flag page
+  std::vector<std::uint64_t*> peerFlags_;                  // rank -> mapped flag page
   std::map<std::pair<std::uint32_t, std::uint64_t>, void*> ipcOpened_;  // (rank, remote base) -> mapping
   std::map<std::uint64_t, std::vector<void*>> peerTiles_;  // matrix -> per layout tile: mapped ptr
   // producer side: matrix -> (consumer, stream) -> exec id of its last pull
@@ -484,5 +616,13 @@ void biasAdd(Session& s, DistMatrix x, DistMatrix bias);
 void copyMatrix(Session& s, DistMatrix src, DistMatrix dst);
 void castPrecision(Session& s, DistMatrix src, DistMatrix dst);
 void setConst(Session& s, DistMatrix m, double value);
+// Outside the B200 GEMM path (reference session.hpp:175-179): declared so
+// reference call sites compile; they throw "op not supported on the B200
+// GEMM path" before anything is issued.
+void softmaxRows(Session& s, DistMatrix a);
+void subtractOneHot(Session& s, DistMatrix probs, DistMatrix labels);
+double logLossMean(Session& s, DistMatrix probs, DistMatrix labels);
+void conv2dForward(Session& s, DistMatrix input, DistMatrix filters, DistMatrix output,
+                   kernels::ConvGeometry g);
 
 }  // namespace gridmath

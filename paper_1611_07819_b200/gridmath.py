@@ -129,6 +129,31 @@ def nccl_unique_id() -> bytes:
     return bytes(buf)
 
 
+_CONTROL_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.c_uint64, ctypes.c_void_p)
+
+
+def gloo_control(group=None):
+    """SPMD control channel over a torch.distributed gloo group (CPU): the
+    session's few blocking control collectives (IPC registration, budget
+    agreement, shutdown) run through it instead of an NCCL communicator, so
+    several ranks may share one GPU. `group` None: a new gloo group over the
+    default world (or the default group itself when it is gloo)."""
+    import torch
+    import torch.distributed as dist
+    if group is None and dist.get_backend() != "gloo":
+        group = dist.new_group(backend="gloo")
+
+    def allreduce_max(buf, n, _user):
+        try:
+            t = torch.frombuffer((ctypes.c_uint8 * n).from_address(buf), dtype=torch.uint8)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX, group=group)
+            return 0
+        except Exception:  # reported to the library as a failed collective
+            return 1
+
+    return allreduce_max
+
+
 @dataclass(frozen=True)
 class DistMatrix:
     session: "Session"
@@ -167,7 +192,10 @@ class Session:
     def __init__(self, workers: int = 1, deterministic: bool = True, devices: Optional[Sequence[int]] = None,
                  spmd_rank: int = -1, nccl_id: Optional[bytes] = None, gemm_max_ctas: int = 0,
                  transport: int = 0, check_metadata_every_op: bool = False, panel_cache_bytes: int = 0,
-                 pipeline_chunks: int = 0, _restore_from: Optional[str] = None):
+                 pipeline_chunks: int = 0, control=None, _restore_from: Optional[str] = None):
+        """control: None (NCCL control channel under SPMD) or a callable
+        (buf_address, nbytes, user) -> int doing an in-place max all-reduce of
+        host bytes over the ranks (see gloo_control), or "gloo"."""
         lib = _lib.load()
         o = _lib.gm_session_options()
         lib.gm_session_options_default(ctypes.byref(o))
@@ -185,6 +213,11 @@ class Session:
         o.transport = transport
         o.panel_cache_bytes = panel_cache_bytes
         o.pipeline_chunks = pipeline_chunks
+        self._control = None
+        if control is not None:
+            fn = gloo_control() if control == "gloo" else control
+            self._control = _CONTROL_FN(fn)  # kept alive for the session's lifetime
+            o.control_allreduce_max_u8 = ctypes.cast(self._control, ctypes.c_void_p)
         self._h = ctypes.c_void_p()
         if _restore_from is None:
             check(lib.gm_session_create(ctypes.byref(o), ctypes.byref(self._h)))

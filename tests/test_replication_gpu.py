@@ -202,3 +202,34 @@ def test_single_tile_owner_replica_aliases_the_tile():
         s.fillUniform(W, 5, -0.05, 0.05)
         assert s.wait(s.replicateAsync(W)) == G.ReplState.Done
         check(s.getDataRaw(W))
+
+
+def test_panel_cache_never_evicts_a_band_planned_as_cached():
+    """Budget of three bands, access pattern gemm(X,W), gemm(X,V), gemm(Y,W)
+    with C column-block: the third GEMM gathers Y (A bands come first in
+    the plan) while W is planned as a cache hit. The gather's reservation
+    must evict X (least recently used, not in the plan), never W; results
+    stay exact and W moves no bytes in the third GEMM."""
+    p, fi = 2, 256
+    fo = 512
+    batch = fo // p  # X band (batch x fi) == W band (fi x fo/p)
+    g = G.makeWorkerGroup(p)
+    band = batch * fi * 2
+    with G.Session(workers=p, panel_cache_bytes=3 * band) as s:
+        X = s.createMatrix(batch, fi, G.Precision.BF16, G.makeRowBlockLayout(batch, fi, g))
+        Y = s.createMatrix(batch, fi, G.Precision.BF16, G.makeRowBlockLayout(batch, fi, g))
+        W = s.createMatrix(fi, fo, G.Precision.BF16, G.makeRowBlockLayout(fi, fo, g))
+        V = s.createMatrix(fi, fo, G.Precision.BF16, G.makeRowBlockLayout(fi, fo, g))
+        C = s.createMatrix(batch, fo, G.Precision.Single, G.makeColBlockLayout(batch, fo, g))
+        for i, M in enumerate((X, Y, W, V)):
+            s.fillUniform(M, 11 + i)
+        x, y, w, v = (s.getDataRaw(M) for M in (X, Y, W, V))
+        zero = np.zeros((batch, fo), np.float32)
+        for a, b, ah, bh in ((X, W, x, w), (X, V, x, v), (Y, W, y, w), (Y, W, y, w)):
+            st0 = s.queryWorkerStats()
+            G.gemm(s, a, b, C, 1.0, 0.0)
+            st1 = s.queryWorkerStats()
+            want = O.gemm_c(batch, fo, fi, ah, 3, bh, 3, zero, 1, 1.0, 0.0, 0, 0)
+            assert O.rel_fro(s.getDataRaw(C), want) <= 1e-5
+        # the last GEMM finds both Y and W in the cache: nothing moves
+        assert sum(b["bytes_received"] - a["bytes_received"] for a, b in zip(st0, st1)) == 0

@@ -68,3 +68,42 @@ def test_spmd_plans_agree_across_ranks(world):
     for p in procs:
         p.join(timeout=60)
     assert all(ok for _, ok in res), res
+
+
+def _control_worker(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import ctypes
+    import sys
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    from paper_1611_07819_b200 import gridmath as G
+    # Exactly what the library does: a C function pointer called with a host
+    # buffer. Each rank fills its own 8-byte slot (the budget agreement) and
+    # one shared byte; the max-reduce must gather the slots and max the byte.
+    fn = G._CONTROL_FN(G.gloo_control())
+    buf = (ctypes.c_uint8 * (8 * world + 1))()
+    ctypes.memmove(ctypes.addressof(buf) + 8 * rank, (1000 + rank).to_bytes(8, "little"), 8)
+    buf[8 * world] = 7 if rank == world - 1 else 1
+    rc = fn(ctypes.addressof(buf), len(buf), None)
+    got = [int.from_bytes(bytes(buf[8 * r:8 * r + 8]), "little") for r in range(world)]
+    dist.destroy_process_group()
+    q.put((rank, rc == 0 and got == [1000 + r for r in range(world)] and buf[8 * world] == 7))
+
+
+@pytest.mark.timeout(300)
+def test_gloo_control_channel_gathers_and_maxes():
+    """The host control channel (Session(control="gloo")) that replaces the
+    NCCL communicator when several ranks share a GPU: a byte-wise max
+    all-reduce in place through the ctypes callback."""
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_control_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=240) for _ in procs]
+    for p in procs:
+        p.join(timeout=60)
+    assert all(ok for _, ok in res), res

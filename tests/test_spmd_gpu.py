@@ -1,7 +1,13 @@
 # SPDX-License-Identifier: Apache-2.0
-"""One process per GPU (the benchmark's mode): torchrun over the GPUs present
-runs tools/spmd_check.py -- NCCL data plane, SUMMA pipelining, replication --
-and requires bitwise equality with the single-GPU result. Skips with < 2 GPUs."""
+"""One process per worker (the benchmark's mode): torchrun runs
+tools/spmd_check.py -- both data planes, SUMMA panel exchange, replication,
+reshape, RAW/WAR chains, record/replay, host streaming, checkpoint -- and
+requires bitwise equality with the single-GPU result.
+
+* one rank per GPU (>= 2 GPUs): NCCL control channel, IPC and NCCL planes;
+* two ranks per GPU (any box, including a 1-GPU one): the gloo control
+  channel and the IPC copy-engine plane (NCCL cannot put two ranks on one
+  GPU). On a 4-GPU box this runs the 2x4 grid's 8 ranks."""
 import os
 import socket
 import subprocess
@@ -19,17 +25,29 @@ def _gpus():
     return torch.cuda.device_count() if torch.cuda.is_available() else 0
 
 
-@pytest.mark.timeout(600)
-def test_spmd_nccl_path_matches_single_gpu():
-    n = _gpus()
-    if n < 2:
-        pytest.skip("needs >= 2 GPUs")
-    n = 4 if n >= 4 else 2
+def _run(nproc):
     s = socket.socket()
     s.bind(("127.0.0.1", 0))
     port = s.getsockname()[1]
     s.close()
-    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={nproc}",
            "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.join(ROOT, "tools", "spmd_check.py")]
-    out = subprocess.run(cmd, capture_output=True, text=True, timeout=540)
+    out = subprocess.run(cmd, capture_output=True, text=True, timeout=840)
     assert out.returncode == 0 and "SPMD_CHECK PASS" in out.stdout, out.stdout[-3000:] + out.stderr[-3000:]
+    return out.stdout
+
+
+@pytest.mark.timeout(900)
+def test_spmd_one_rank_per_gpu_matches_single_gpu():
+    n = _gpus()
+    if n < 2:
+        pytest.skip("needs >= 2 GPUs (the two-ranks-per-GPU test covers 1-GPU boxes)")
+    _run(4 if n >= 4 else 2)
+
+
+@pytest.mark.timeout(900)
+def test_spmd_two_ranks_per_gpu_gloo_control_matches_single_gpu():
+    n = _gpus()
+    world = 8 if n >= 4 else (4 if n >= 2 else 2)
+    out = _run(world)
+    assert f"SPMD_CHECK world={world}" in out and "control=gloo" in out, out[-2000:]

@@ -21,11 +21,21 @@ from paper_1611_07819_b200 import gridmath as G  # noqa: E402
 import oracle as O  # noqa: E402
 
 rank, world, local = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"]), int(os.environ["LOCAL_RANK"])
-# More ranks than GPUs (e.g. the 2x4 grid's 8 ranks on a 4-GPU box): ranks
-# share devices round-robin; the IPC plane maps same-device peers too.
+# More ranks than GPUs (e.g. the 2x4 grid's 8 ranks on a 4-GPU box, or 2
+# ranks on a 1-GPU box): ranks share devices round-robin. NCCL refuses two
+# ranks on one GPU, so the sessions then take the gloo control channel
+# (Session(control="gloo")) and the IPC copy-engine data plane only (the
+# IPC plane maps same-device peers too); the script's own collectives run
+# on the gloo group with CPU tensors.
+SHARED = world > torch.cuda.device_count()
 local = local % torch.cuda.device_count()
 torch.cuda.set_device(local)
-dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+if SHARED:
+    dist.init_process_group("gloo")
+else:
+    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+CONTROL = "gloo" if SHARED else None
+TDEV = "cpu" if SHARED else "cuda"
 pr, pc = {1: (1, 1), 2: (1, 2), 4: (2, 2), 8: (2, 4)}[world]
 g = G.makeWorkerGroup(world)
 
@@ -67,7 +77,7 @@ def chain(s, lay, n, steps):
 def run(transport, nccl_id):
     ok = True
     with G.Session(workers=world, spmd_rank=rank, devices=[local], nccl_id=nccl_id, panel_cache_bytes=1,
-                   transport=transport) as s:
+                   transport=transport, control=CONTROL) as s:
         plane = s.transport()
         want_plane = "nccl" if transport == 1 else "ipc"
         if plane != want_plane:
@@ -189,7 +199,7 @@ def run(transport, nccl_id):
             s.getLocalPackedAsync(C, hc.ctypes.data, hc.nbytes)
         s.synchronize()
         good = bool(np.array_equal(hc, want_c))
-        t = torch.tensor([1 if good else 0], device="cuda")
+        t = torch.tensor([1 if good else 0], device=TDEV)
         dist.all_reduce(t, op=dist.ReduceOp.MIN)
         good = t.item() == 1
         say(f"[rank0 {plane}] async chunked upload/gemm/download == sync path on every rank: {good}")
@@ -203,7 +213,7 @@ def run(transport, nccl_id):
         s.checkpoint(path)
         dist.barrier()
     with G.Session.restore(path, workers=world, spmd_rank=rank, devices=[local], nccl_id=_fresh_id(),
-                           transport=transport) as s2:
+                           transport=transport, control=CONTROL) as s2:
         after = s2.getDataRaw(s2.matrix(C.id))
         good = bool(np.array_equal(after, before))
         say(f"[rank0 {plane}] checkpoint/restore across ranks ok={good}")
@@ -258,11 +268,12 @@ def fc_steps(s, steps, S=G.Precision.Single):
 
 
 ok = True
-for transport in (0, 1):
+for transport in ((0,) if SHARED else (0, 1)):
     obj = [G.nccl_unique_id() if rank == 0 else None]
     dist.broadcast_object_list(obj, src=0)
     ok = run(transport, obj[0]) and ok
-t = torch.tensor([1 if ok else 0], device="cuda")
+say(f"SPMD_CHECK world={world} gpus={torch.cuda.device_count()} control={'gloo' if SHARED else 'nccl'}")
+t = torch.tensor([1 if ok else 0], device=TDEV)
 dist.all_reduce(t, op=dist.ReduceOp.MIN)
 say("SPMD_CHECK " + ("PASS" if t.item() == 1 else "FAIL"))
 dist.destroy_process_group()
