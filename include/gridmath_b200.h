@@ -340,6 +340,11 @@ int gm_session_local_workers(gm_session* s, uint32_t* ranks, uint32_t cap, uint3
 #define GM_TRANSPORT_NCCL 1
 #define GM_TRANSPORT_IPC 2
 int gm_session_transport(gm_session* s, int32_t* kind);
+/* In-GEMM panel pipelining (default on): gathered bands land block by block
+ * while the GEMM runs, its producer polling per-block ready flags. 0 turns
+ * it off for later GEMMs of this session (they wait for whole bands). Local
+ * to this process (SPMD ranks may differ). */
+int gm_session_set_panel_pipelining(gm_session* s, int32_t on);
 /* Device time of the last gm_gemm/gm_gemm_async per local worker (ms),
  * measured with CUDA events on the worker's compute stream. */
 int gm_last_op_device_ms(gm_session* s, float* ms, uint32_t cap, uint32_t* n);

@@ -362,6 +362,10 @@ int gm_session_transport(gm_session* s, int32_t* kind) {
   return guard([&] { *kind = s->s->transportKind(); });
 }
 
+int gm_session_set_panel_pipelining(gm_session* s, int32_t on) {
+  return guard([&] { s->s->setPanelPipelining(on != 0); });
+}
+
 int gm_last_op_device_ms(gm_session* s, float* ms, uint32_t cap, uint32_t* n) {
   return guard([&] {
     const auto v = s->s->lastOpDeviceMs();

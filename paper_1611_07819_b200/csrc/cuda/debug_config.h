@@ -17,6 +17,10 @@ struct DebugConfig {
   int l2_promo = 128;      // TMA L2 promotion bytes (0, 64, 128, 256)
   int hint_a = 0, hint_b = 0;  // TMA L2 cache hints (0 normal, 1 evict_last, 2 evict_first)
   int panel_flags = 1;     // 0 = GEMM waits for whole bands (no in-kernel panel pipelining)
+  int panel_min_gflop = -1;  // pipeline GEMMs of at least this many GFLOP per worker (-1 = 1000)
+  int panel_k = 0;         // k elements per pipelined panel (0 = auto)
+  int a_chunk_rows = 0;    // pipelined A block rows (0 = auto)
+  int b_chunk_cols = 0;    // pipelined B block columns (0 = auto)
   int ready_slots = 0;     // ready-flag ring slots per worker (0 = 65536; small values test reuse)
   int pull_streams = 0;    // copy-engine pull streams per exchange (0 = all)
   int fuse_epilogue = 1;   // 0 = replay does not fuse gemm -> biasAdd -> relu

@@ -13,7 +13,9 @@
 
 #include "convert.h"
 #include "fc_ops.h"
+#include "gemm_tc.h"
 #include "prec.cuh"
+#include "ptx.cuh"
 
 namespace gmk {
 
@@ -338,6 +340,132 @@ __global__ void __launch_bounds__(kAsThreads) line_sums_async_kernel(const void*
   }
 }
 
+// Line sums for 16-bit storage, TMA-fed: the same ascending chains (one
+// lane = one output), but the stages arrive by cp.async.bulk.tensor issued
+// by one thread, so the folding warp owns its SM sub-partition (no copy
+// warps competing for issue slots) and synchronises through mbarriers, not
+// a CTA barrier per stage. 64 threads: warp 0 folds, warp 1 lane 0 loads.
+//   by rows: a stage is 4 boxes of 32 rows x 64 elements (128-byte rows,
+//            128-byte swizzle: lane o's 16-byte chunk j of its row sits at
+//            j ^ (o & 7), so the 8 lanes of an LDS.128 phase hit 8 banks);
+//   by cols: a stage is one box of 256 rows x 32 elements (lane o reads
+//            column o: a warp reads one contiguous 64-byte row).
+// Out-of-range box elements are zero-filled by TMA: exact, a chain starting
+// at +0 never holds -0.
+constexpr int kTsThreads = 64;
+constexpr int kTsStep = 256;     // elements per chain per stage
+constexpr int kTsStages = 6;
+constexpr int kTsStage = 16384;  // bytes per stage (32 x 256 x 2)
+
+template <typename T, int P>
+__global__ void __launch_bounds__(kTsThreads) line_sums_tma_kernel(const __grid_constant__ CUtensorMap map,
+                                                                   uint64_t rows, uint64_t cols, int by_rows,
+                                                                   void* __restrict__ acc, uint64_t acc_stride,
+                                                                   int acc_prec, T alpha) {
+  using S = typename Stor<P>::type;
+  static_assert(sizeof(S) == 2, "16-bit storage only");
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  // Offset from the shared array itself (not through an integer cast), so
+  // the folds compile to LDS rather than generic loads.
+  unsigned char* ring = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  uint64_t* full = reinterpret_cast<uint64_t*>(ring + kTsStages * kTsStage);
+  uint64_t* empty = full + kTsStages;
+  const uint64_t outs = by_rows ? rows : cols;
+  const uint64_t len = by_rows ? cols : rows;
+  const uint64_t o0 = static_cast<uint64_t>(blockIdx.x) * 32;
+  const uint32_t nchunks = static_cast<uint32_t>((len + kTsStep - 1) / kTsStep);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 32) {
+    tma_prefetch_desc(&map);
+    for (int s = 0; s < kTsStages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    fence_barrier_init();
+  }
+  __syncthreads();
+  if (warp == 1) {
+    if (lane == 0) {
+      for (uint32_t i = 0; i < nchunks; ++i) {
+        const uint32_t s = i % kTsStages;
+        if (i >= kTsStages) mbar_wait(&empty[s], ((i / kTsStages) - 1) & 1);
+        unsigned char* st = ring + s * kTsStage;
+        mbar_arrive_expect_tx(&full[s], kTsStage);
+        const int32_t k0 = static_cast<int32_t>(i * kTsStep);
+        if (by_rows) {
+#pragma unroll
+          for (int b = 0; b < 4; ++b) tma_load_2d(st + b * 4096, &map, &full[s], k0 + b * 64, static_cast<int32_t>(o0));
+        } else {
+          tma_load_2d(st, &map, &full[s], static_cast<int32_t>(o0), k0);
+        }
+      }
+    }
+    return;
+  }
+  T sum = T(0);
+  for (uint32_t i = 0; i < nchunks; ++i) {
+    const uint32_t s = i % kTsStages;
+    mbar_wait(&full[s], (i / kTsStages) & 1);
+    const unsigned char* st = ring + s * kTsStage;
+    if (by_rows) {
+      // A box row (64 elements) is loaded ahead of its 64 ordered adds.
+      const unsigned char* row = st + lane * 128;
+#pragma unroll
+      for (int b = 0; b < 4; ++b) {
+        uint4 w[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) w[j] = *reinterpret_cast<const uint4*>(row + b * 4096 + ((j ^ (lane & 7)) << 4));
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const uint32_t q[4] = {w[j].x, w[j].y, w[j].z, w[j].w};
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            sum = add_rn(sum, widen<P, T>(static_cast<S>(q[k] & 0xFFFFu)));
+            sum = add_rn(sum, widen<P, T>(static_cast<S>(q[k] >> 16)));
+          }
+        }
+      }
+    } else {
+      // 32 rows of the lane's column are loaded ahead of their adds.
+      const S* col = reinterpret_cast<const S*>(st) + lane;
+#pragma unroll 1
+      for (int r0 = 0; r0 < kTsStep; r0 += 32) {
+        S v[32];
+#pragma unroll
+        for (int r = 0; r < 32; ++r) v[r] = col[(r0 + r) * 32];
+#pragma unroll
+        for (int r = 0; r < 32; ++r) sum = add_rn(sum, widen<P, T>(v[r]));
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[s]);
+  }
+  if (o0 + lane < outs) {
+    const uint64_t idx = (o0 + lane) * acc_stride;
+    const T cur = load_as<T>(acc, acc_prec, idx);
+    store_as(acc, acc_prec, idx, add_rn(cur, mul_rn(alpha, sum)));
+  }
+}
+
+template <typename T, int P>
+cudaError_t launch_sums_tma(EwView band, uint64_t rows, uint64_t cols, int by_rows, void* acc, uint64_t acc_stride,
+                            int acc_prec, T alpha, cudaStream_t s, bool* done) {
+  *done = false;
+  CUtensorMap map;
+  const int enc = by_rows ? encode_map_2d(&map, band.ptr, 2, cols, rows, band.ld, 64, 32, 128)
+                          : encode_map_2d(&map, band.ptr, 2, cols, rows, band.ld, 32, kTsStep, 0);
+  if (enc) return cudaSuccess;  // not encodable: the cp.async path runs instead
+  constexpr size_t smem = kTsStages * kTsStage + 2 * kTsStages * 8 + 1024;
+  const cudaError_t attr = cudaFuncSetAttribute(line_sums_tma_kernel<T, P>,
+                                                cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (attr != cudaSuccess) return attr;
+  const uint64_t outs = by_rows ? rows : cols;
+  line_sums_tma_kernel<T, P><<<static_cast<unsigned>((outs + 31) / 32), kTsThreads, smem, s>>>(
+      map, rows, cols, by_rows, acc, acc_stride, acc_prec, alpha);
+  *done = true;
+  return cudaSuccess;
+}
+
 template <typename T, int P>
 cudaError_t launch_sums_async(EwView band, uint64_t rows, uint64_t cols, int by_rows, void* acc,
                               uint64_t acc_stride, int acc_prec, T alpha, cudaStream_t s) {
@@ -426,6 +554,16 @@ cudaError_t line_sums(EwView band, uint64_t rows, uint64_t cols, int by_rows, vo
   if (vec_ok(band.ptr, band.ld, eb) && (double_compute ? band.prec == 2 : band.prec != 2)) {
     cudaError_t e;
     const float af = static_cast<float>(alpha);
+    if (band.prec == 0 || band.prec == 3) {
+      bool done = false;
+      e = band.prec == 0 ? launch_sums_tma<float, 0>(band, rows, cols, by_rows, acc, acc_stride, acc_prec, af, s, &done)
+                         : launch_sums_tma<float, 3>(band, rows, cols, by_rows, acc, acc_stride, acc_prec, af, s, &done);
+      if (e != cudaSuccess) return e;
+      if (done) {
+        count_launch();
+        return cudaGetLastError();
+      }
+    }
     switch (band.prec) {
       case 0: e = launch_sums_async<float, 0>(band, rows, cols, by_rows, acc, acc_stride, acc_prec, af, s); break;
       case 1: e = launch_sums_async<float, 1>(band, rows, cols, by_rows, acc, acc_stride, acc_prec, af, s); break;

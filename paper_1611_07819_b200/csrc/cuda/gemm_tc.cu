@@ -146,22 +146,35 @@ __device__ __forceinline__ void tile_coords(uint32_t t, const TcParams& p, uint3
   nb = r / gsize;
 }
 
-// Waits until every pull stream published blocks [c0, c1] x {panel} of one
-// operand's flag array, then orders the generic-proxy acquire before the
-// async-proxy (TMA) reads of the landed bytes.
-__device__ __forceinline__ void wait_ready(const uint64_t* flags, uint32_t c0, uint32_t c1, uint32_t panel,
-                                           const PanelReady& r) {
-  for (uint32_t c = c0; c <= c1; ++c)
-    for (uint32_t s = 0; s < r.streams; ++s) {
-      const uint64_t* f = flags + (static_cast<uint64_t>(c) * r.num_panels + panel) * r.streams + s;
-      for (;;) {
-        uint64_t v;
-        asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(f) : "memory");
-        if (v >= r.target) break;
-        __nanosleep(256);
-      }
+// Waits until blocks [c0, c1] x {panel} of one operand have landed, then
+// orders the generic-proxy acquire before the async-proxy (TMA) reads of
+// the landed bytes.
+__device__ __forceinline__ void wait_ready(const PanelFlags& r, uint32_t c0, uint32_t c1, uint32_t panel) {
+  for (uint32_t c = c0; c <= c1; ++c) {
+    const uint64_t* f = r.flags + static_cast<uint64_t>(c) * r.num_panels + panel;
+    for (;;) {
+      uint64_t v;
+      asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(f) : "memory");
+      if (v >= r.target) break;
+      __nanosleep(1024);
     }
+  }
   asm volatile("fence.proxy.async.global;" ::: "memory");
+}
+
+// True once every block of both operands has landed (non-blocking check).
+__device__ __forceinline__ bool all_ready(const PanelReady& r) {
+  for (int op = 0; op < 2; ++op) {
+    const PanelFlags& p = op ? r.b : r.a;
+    if (!p.flags) continue;
+    const uint32_t n = p.chunks * p.num_panels;
+    for (uint32_t i = 0; i < n; ++i) {
+      uint64_t v;
+      asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p.flags + i) : "memory");
+      if (v < p.target) return false;
+    }
+  }
+  return true;
 }
 
 __device__ __forceinline__ float load_c(const TcParams& p, uint64_t off) {
@@ -351,37 +364,41 @@ __global__ void __launch_bounds__(kNumThreads, 1)
       uint32_t timeouts = 0;
       const uint32_t cps_per_tile = synced ? (num_kb + p.sync_every - 1) / p.sync_every : 0;
       const PanelReady& rd = p.ready;
-      const uint32_t kb_per_panel = rd.num_panels ? rd.panel_k / kBlockK : 0;
+      const uint32_t a_kbp = rd.a.flags ? rd.a.panel_k / kBlockK : 0;  // k-blocks per panel
+      const uint32_t b_kbp = rd.b.flags ? rd.b.panel_k / kBlockK : 0;
+      // While panels are still landing, pairs stall on data at different
+      // times; lockstep timeouts then say nothing about residency, so they
+      // only end the wait for the current tile. They count towards the
+      // launch-wide cut-off once every block has landed.
+      bool data_done = !rd.on();
       uint32_t local_tile = 0;
       for (uint32_t t = unit; t < num_tiles; t += num_units, ++local_tile) {
         uint32_t mb, nb;
         tile_coords(t, p, p.num_n_blocks, mb, nb);
         const int32_t m0 = static_cast<int32_t>(mb * kBlockMcta * kCG + rank * kBlockMcta);
         bool wait_sync = synced && timeouts < kMaxLockstepTimeouts;
+        if (!data_done) data_done = all_ready(rd);
         // Flag blocks this CTA's loads touch: its own 128 rows of A, the
         // tile's columns of B.
         uint32_t ac0 = 0, ac1 = 0, bc0 = 0, bc1 = 0;
-        if (rd.a) {
+        if (rd.a.flags) {
           const uint32_t r1 = min(static_cast<uint32_t>(m0) + kBlockMcta, p.m) - 1;
-          ac0 = (rd.a_row0 + static_cast<uint32_t>(m0)) / rd.a_chunk_rows;
-          ac1 = (rd.a_row0 + r1) / rd.a_chunk_rows;
+          ac0 = (rd.a.origin + static_cast<uint32_t>(m0)) / rd.a.chunk;
+          ac1 = (rd.a.origin + r1) / rd.a.chunk;
         }
-        if (rd.b) {
+        if (rd.b.flags) {
           const uint32_t c0 = nb * Cfg::kBlockN, c1 = min(c0 + Cfg::kBlockN, p.n) - 1;
-          bc0 = (rd.b_col0 + c0) / rd.b_chunk_cols;
-          bc1 = (rd.b_col0 + c1) / rd.b_chunk_cols;
+          bc0 = (rd.b.origin + c0) / rd.b.chunk;
+          bc1 = (rd.b.origin + c1) / rd.b.chunk;
         }
         for (uint32_t kb = 0; kb < num_kb; ++kb) {
           if (synced && kb % p.sync_every == 0 &&
               !lockstep(p.sync_ctr, local_tile * cps_per_tile + kb / p.sync_every, num_units, wait_sync)) {
             wait_sync = false;  // rest of this tile
-            ++timeouts;
+            if (data_done) ++timeouts;
           }
-          if (kb_per_panel && kb % kb_per_panel == 0) {
-            const uint32_t panel = kb / kb_per_panel;
-            if (rd.a) wait_ready(rd.a, ac0, ac1, panel, rd);
-            if (rd.b) wait_ready(rd.b, bc0, bc1, panel, rd);
-          }
+          if (a_kbp && kb % a_kbp == 0) wait_ready(rd.a, ac0, ac1, kb / a_kbp);
+          if (b_kbp && kb % b_kbp == 0) wait_ready(rd.b, bc0, bc1, kb / b_kbp);
           mbar_wait(&empty_bar[stage], phase ^ 1);
           uint8_t* sa = smem + stage * Cfg::kStageBytes;
           uint8_t* sb = sa + Cfg::kParts * Cfg::kBytesA;
@@ -731,6 +748,24 @@ int make_map_2d(CUtensorMap* map, const void* ptr, CUtensorMapDataType dt, uint3
   return 0;
 }
 
+}  // namespace
+
+int encode_map_2d(CUtensorMap* map, const void* ptr, int elem_bytes, uint64_t inner, uint64_t outer,
+                  uint64_t pitch_elems, uint32_t box_inner, uint32_t box_outer, int swizzle_bytes) {
+  const char* err = nullptr;
+  const CUtensorMapDataType dt = elem_bytes == 2 ? CU_TENSOR_MAP_DATA_TYPE_UINT16
+                                 : elem_bytes == 4 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32
+                                                   : CU_TENSOR_MAP_DATA_TYPE_FLOAT64;
+  const CUtensorMapSwizzle sw = swizzle_bytes == 128 ? CU_TENSOR_MAP_SWIZZLE_128B
+                                : swizzle_bytes == 64 ? CU_TENSOR_MAP_SWIZZLE_64B
+                                : swizzle_bytes == 32 ? CU_TENSOR_MAP_SWIZZLE_32B
+                                                      : CU_TENSOR_MAP_SWIZZLE_NONE;
+  return make_map_2d(map, ptr, dt, static_cast<uint32_t>(elem_bytes), inner, outer, pitch_elems, box_inner,
+                     box_outer, &err, sw);
+}
+
+namespace {
+
 int sm_count(int dev) {
   static int counts[64] = {0};
   if (dev < 0 || dev >= 64) return 148;
@@ -820,11 +855,11 @@ int launch(const TcOperand& a, const TcOperand& b, const TcOperand* a_lo, const 
     mal = ma;
     mbl = mb;
   }
-  if (p.ready.num_panels && (p.ready.panel_k % Cfg::kBlockK || !p.ready.streams ||
-                             (p.ready.a && !p.ready.a_chunk_rows) || (p.ready.b && !p.ready.b_chunk_cols))) {
-    *err = "tc_gemm: panel flags need panel_k a multiple of the k-block and non-zero chunk sizes";
-    return 1;
-  }
+  for (const PanelFlags* f : {&p.ready.a, &p.ready.b})
+    if (f->flags && (!f->panel_k || f->panel_k % Cfg::kBlockK || !f->chunk || !f->num_panels)) {
+      *err = "tc_gemm: panel flags need panel_k a multiple of the k-block and non-zero chunk sizes";
+      return 1;
+    }
   p.num_m_blocks = (p.m + kBlockMcta * kCG - 1) / (kBlockMcta * kCG);
   // Raster group 16: an interleaved sweep at 32768^3 measured 12-16 2% faster
   // than 32 (DRAM 84 -> 67 GB).
@@ -862,7 +897,7 @@ int launch(const TcOperand& a, const TcOperand& b, const TcOperand* a_lo, const 
   if (dbg.verbose)
     std::fprintf(stderr, "[gm] tc_gemm cg=%d elem=%d split=%d chunks=%d m=%u n=%u k=%u grid=%d resident=%d stages=%u smem=%u panels=%u\n",
                  kCG, kElemBytes, kSplit, kChunks, p.m, p.n, p.k, ctas, res,
-                 Cfg::kStages, Cfg::kSmemBytes, p.ready.num_panels);
+                 Cfg::kStages, Cfg::kSmemBytes, p.ready.a.num_panels + p.ready.b.num_panels);
   CUtensorMap mc = ma;
   {
     const uint32_t cb = p.c_dtype == 2 ? 4 : 2;
@@ -975,7 +1010,7 @@ int tc_gemm(const TcGemmArgs& g, cudaStream_t stream, const char** err) {
     return wide ? launch<2, 2, 0, 2>(g.a, g.b, nullptr, nullptr, p, g.max_ctas, stream, err)
                 : launch<2, 2, 0, 1>(g.a, g.b, nullptr, nullptr, p, g.max_ctas, stream, err);
   }
-  if (g.ready.num_panels) {
+  if (g.ready.on()) {
     *err = "tc_gemm: panel flags are consumed by the 16-bit kinds only";
     return 1;
   }

@@ -1,6 +1,7 @@
 // SPDX-License-Identifier: Apache-2.0
 // Host-side entry for the tcgen05 tile GEMM (gemm_tc.cu).
 #pragma once
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <cstdint>
 
@@ -13,19 +14,27 @@ struct TcOperand {
   uint64_t ld = 0;            // row pitch in elements (pitch bytes % 16 == 0)
 };
 
-// In-GEMM panel pipelining: the consumer's pull streams copy the gathered
-// bands block by block -- (m-chunk x k-panel) of A, (n-chunk x k-panel) of B
-// -- and after its pieces of a block stream s writes
-// flags[(chunk * num_panels + panel) * streams + s] = target. The GEMM's
-// producer waits for the blocks a k-block reads before loading it, so
-// panel k+1 lands while panel k multiplies. Null flag array: resident.
-struct PanelReady {
-  const uint64_t* a = nullptr;
-  const uint64_t* b = nullptr;
+// In-GEMM panel pipelining: an operand arrives block by block -- A in
+// (m-chunk x k-panel) blocks, B in (n-chunk x k-panel) blocks -- and whoever
+// lands a block writes flags[chunk * num_panels + panel] = target (a
+// gathered band's pull streams, or a replication job per source piece). The
+// GEMM's producer waits for the blocks a k-block reads before loading it, so
+// panel k+1 lands while panel k multiplies. Null flags: operand resident.
+struct PanelFlags {
+  const uint64_t* flags = nullptr;
   uint64_t target = 0;
-  uint32_t a_row0 = 0, a_chunk_rows = 0;  // kernel row r lies in A chunk (a_row0 + r) / a_chunk_rows
-  uint32_t b_col0 = 0, b_chunk_cols = 0;  // kernel column j lies in B chunk (b_col0 + j) / b_chunk_cols
-  uint32_t panel_k = 0, num_panels = 0, streams = 0;  // num_panels 0 = off
+  uint32_t origin = 0;    // kernel row (A) / column (B) j lies in chunk (origin + j) / chunk
+  uint32_t chunk = 0;     // rows (A) / columns (B) per chunk
+  uint32_t chunks = 0;    // flag rows (all blocks landed: lockstep rule)
+  uint32_t panel_k = 0;   // k elements per panel (multiple of the k-block)
+  uint32_t num_panels = 0;
+};
+struct PanelReady {
+  PanelFlags a, b;
+#ifdef __CUDACC__
+  __host__ __device__
+#endif
+  bool on() const { return a.flags || b.flags; }
 };
 
 struct TcGemmArgs {
@@ -58,6 +67,12 @@ struct TcTilePlan {
   uint32_t block_m = 256, block_n = 512, group = 16, units = 74;
 };
 TcTilePlan tc_tile_plan(uint64_t m, uint64_t n, uint64_t k, int cta_group, int max_ctas);
+
+// 2D tensor map (cuTensorMapEncodeTiled through the runtime's driver entry
+// point) of a row-major matrix: inner = columns, outer = rows, pitch in
+// elements, box in elements, swizzle 0/32/64/128 bytes. 0 on success.
+int encode_map_2d(CUtensorMap* map, const void* ptr, int elem_bytes, uint64_t inner, uint64_t outer,
+                  uint64_t pitch_elems, uint32_t box_inner, uint32_t box_outer, int swizzle_bytes);
 
 // Launches on `stream`; returns 0 or 1 with *err set (static string).
 int tc_gemm(const TcGemmArgs& args, cudaStream_t stream, const char** err);

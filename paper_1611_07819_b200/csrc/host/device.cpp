@@ -223,7 +223,7 @@ void gemmLocal(const gm_gemm_desc& d, const void* a, const void* b, void* c, voi
                std::uint64_t workspaceBytes, cudaStream_t stream, const BiasReluEpilogue* ep,
                const gmk::PanelReady* ready) {
   if (d.m == 0 || d.n == 0) return;
-  if (ready && ready->num_panels && !gemmConsumesPanelFlags(d, a, b))
+  if (ready && ready->on() && !gemmConsumesPanelFlags(d, a, b))
     throw Error("gemm: panel flags need the 16-bit tcgen05 path reading both operands in place");
   if (ep && (d.alpha == 0.0 || d.k == 0 || d.prec_c != GM_BF16 || d.prec_a == GM_DOUBLE || d.prec_b == GM_DOUBLE))
     throw Error("gemm: fused bias/relu epilogue needs the tcgen05 path with bf16 C");

@@ -1042,6 +1042,7 @@ void Session::execDestroy(std::uint64_t id) {
     if (rit != w.replicas.end()) {
       cudaStreamWaitEvent(w.compute, rit->second.ready, 0);
       if (!rit->second.alias) w.arena.free(rit->second.full, w.compute);
+      if (rit->second.pieceReady) w.arena.free(rit->second.pieceReady, w.compute);
       cudaEventDestroy(rit->second.ready);
       w.replicas.erase(rit);
     }
@@ -1748,11 +1749,15 @@ void Session::execGemm(const OpDescriptor& op) {
   const bool f16Pair = (A.precision == Precision::BF16 || A.precision == Precision::Half) &&
                        A.precision == B.precision && C.precision != Precision::Double;
   bool pipelined = anyGather && f16Pair && op.s0 != 0.0 && (!nccl_ || ipc_) &&
-                         gmk::debug_config().panel_flags && opts_.pipelineChunks <= 0 && !streamedA &&
+                         gmk::debug_config().panel_flags && panelPipelining_ && opts_.pipelineChunks <= 0 && !streamedA &&
                          !chunkedSource(A.matrixId) && !chunkedSource(B.matrixId);
-  const std::uint64_t panelK = std::max<std::uint64_t>(64, (plan.k + 16 * 64 - 1) / (16 * 64) * 64);
+  const gmk::DebugConfig& dbg = gmk::debug_config();
+  const std::uint64_t panelK = dbg.panel_k > 0 ? (static_cast<std::uint64_t>(dbg.panel_k) + 63) / 64 * 64
+                                               : std::max<std::uint64_t>(64, (plan.k + 16 * 64 - 1) / (16 * 64) * 64);
   const std::uint64_t numPanels = (plan.k + panelK - 1) / panelK;
-  constexpr std::uint64_t kAChunkRows = 4096, kBChunkCols = 2048;  // raster group x 256; 4 wide tiles
+  // Raster group x 256 rows; 4 wide tiles of columns.
+  const std::uint64_t kAChunkRows = dbg.a_chunk_rows > 0 ? static_cast<std::uint64_t>(dbg.a_chunk_rows) : 4096;
+  const std::uint64_t kBChunkCols = dbg.b_chunk_cols > 0 ? static_cast<std::uint64_t>(dbg.b_chunk_cols) : 2048;
   bool fits = true;  // every local band's flag region fits its worker's ring
   for (const PlannedNeed& nd : plan.needs) {
     Worker* w = local(nd.worker);
@@ -1762,7 +1767,20 @@ void Session::execGemm(const OpDescriptor& op) {
     const std::uint64_t cs = nd.operand == 0 ? kAChunkRows : kBChunkCols;
     fits = fits && (ext + cs - 1) / cs * numPanels <= w->readyCap;
   }
-  pipelined = pipelined && fits;
+  // Only GEMMs long enough for the overlap to pay for the per-block copy
+  // and flag overhead (~5 us per block on its stream; measured: the FC dW
+  // GEMM, 0.16 TFLOP per worker, ran 225 -> 400 us pipelined). Per worker:
+  // 2 m n k over its C tiles >= 1 TFLOP (~0.7 ms of tcgen05 time).
+  double maxFlops = 0.0;
+  for (std::uint32_t w = 0; w < P; ++w) {
+    if (!isLocal(w)) continue;
+    double f = 0.0;
+    for (const auto& tl : C.layout.tiles)
+      if (tl.second.rank == w) f += 2.0 * static_cast<double>(tl.first.rowCount) * tl.first.colCount * plan.k;
+    maxFlops = std::max(maxFlops, f);
+  }
+  const double minFlops = dbg.panel_min_gflop >= 0 ? dbg.panel_min_gflop * 1e9 : 1e12;
+  pipelined = pipelined && fits && maxFlops >= minFlops;
   if (pipelined) S = 1;
   // One gathered band of a local consumer in pipelined mode.
   struct FlagBand {
@@ -1780,6 +1798,27 @@ void Session::execGemm(const OpDescriptor& op) {
     std::uint64_t chunk = 0, panel = 0;
   };
   std::vector<BlockXfer> blockXfers;
+  // B read from a replica still landing piece by piece: the GEMM polls the
+  // replica's per-piece flags instead of waiting for the whole matrix.
+  // Column-block layouts only (piece t = columns [t w, (t+1) w)).
+  struct ReplicaPoll {
+    const ReplicaEntry* entry = nullptr;
+    std::uint64_t width = 0;
+    std::uint64_t version = 0;
+  };
+  std::map<std::pair<Worker*, std::size_t>, ReplicaPoll> replicaPoll;  // (worker, B interval)
+  auto columnBlockWidth = [](const MatrixDescriptor& M) -> std::uint64_t {
+    const std::size_t T = M.layout.tiles.size();
+    if (T < 2) return 0;
+    const std::uint64_t w = M.layout.tiles[0].first.colCount;
+    for (std::size_t t = 0; t < T; ++t) {
+      const TileExtent& e = M.layout.tiles[t].first;
+      if (e.rowStart != 0 || e.rowCount != M.rows || e.colStart != t * w ||
+          e.colCount != std::min<std::uint64_t>(w, M.cols - t * w))
+        return 0;
+    }
+    return w;
+  };
 
   std::vector<std::vector<BandView>> aViews(P), bViews(P);
   for (std::uint32_t w = 0; w < P; ++w) {
@@ -1813,7 +1852,24 @@ void Session::execGemm(const OpDescriptor& op) {
           throw Error("replica of matrix " + std::to_string(M.matrixId) + " not readable on worker " +
                       std::to_string(nd.worker));
         w->activate();
-        cudaCheck(cudaStreamWaitEvent(w->compute, it->second.ready, 0), "gemm: wait replica");
+        const std::uint64_t width = columnBlockWidth(M);
+        const bool poll = nd.operand == 1 && !plan.transB && f16Pair && op.s0 != 0.0 && (!nccl_ || ipc_) &&
+                          gmk::debug_config().panel_flags && panelPipelining_ && !it->second.alias &&
+                          it->second.pieceReady && it->second.state == ReplicaState::Pending && width > 0;
+        if (poll) {
+          replicaPoll[{w, nd.interval}] = ReplicaPoll{&it->second, width, M.version};
+          // The pulls filling the replica wait on the sources' last writes;
+          // local sources (workers of this process, possibly on this GPU)
+          // finish those before the polling GEMM holds the SMs.
+          for (const auto& tl : M.layout.tiles)
+            if (Worker* sw = local(tl.second.rank)) {
+              auto lw = sw->lastWrite.find(M.matrixId);
+              if (lw != sw->lastWrite.end() && sw != w)
+                cudaCheck(cudaStreamWaitEvent(w->compute, lw->second, 0), "gemm: wait replica source");
+            }
+        } else {
+          cudaCheck(cudaStreamWaitEvent(w->compute, it->second.ready, 0), "gemm: wait replica");
+        }
         view = offsetView(it->second.full, it->second.ld, nd.rect.r0, nd.rect.c0, eb);
         break;
       }
@@ -2046,18 +2102,31 @@ void Session::execGemm(const OpDescriptor& op) {
       const auto ky = std::make_tuple(firstWave[y.band][y.chunk], y.panel, fy.operand, y.chunk, y.band);
       return kx < ky;
     });
-    std::map<Worker*, int> ordinal;
+    // Blocks copied from the consumer's own tiles (HBM -> HBM) alternate
+    // over pull streams 0-1, peers' blocks over 2-3, so the local copies and
+    // the NVLink pulls run on different copy engines at once instead of
+    // queueing behind each other (the first wave needs both).
+    std::map<Worker*, std::array<int, 2>> ordinal;
+    int stream = 0;
     for (std::size_t i = 0; i < blockXfers.size(); ++i) {
       BlockXfer& bx = blockXfers[i];
       Worker* w = flagBands[bx.band].w;
       const bool firstOfBlock = i == 0 || blockXfers[i - 1].x.flagAddr != bx.x.flagAddr;
-      if (firstOfBlock) ++ordinal[w];
-      bx.x.pullStream = (ordinal[w] - 1) % Worker::kPullStreams;
+      if (firstOfBlock) {
+        const int remote = bx.x.src == w->rank ? 0 : 1;
+        int& ord = ordinal[w][remote];
+        stream = 2 * remote + (ord++ % 2);
+      }
+      bx.x.pullStream = stream;
       bx.x.lastOfBlock = i + 1 == blockXfers.size() || blockXfers[i + 1].x.flagAddr != bx.x.flagAddr;
       bx.x.flagValue = w->readySeq + 1;
     }
     forEachLocal([&](Worker& w) {
-      if (ordinal.count(&w)) ++w.readySeq;
+      for (const FlagBand& fb : flagBands)
+        if (fb.w == &w) {
+          ++w.readySeq;
+          break;
+        }
     });
   }
   {
@@ -2222,30 +2291,44 @@ void Session::execGemm(const OpDescriptor& op) {
           ep.ldAct = at->ld;
         }
         gmk::PanelReady ready;
+        auto rp = replicaPoll.find({&w, ci});
+        if (rp != replicaPoll.end()) {
+          if (gemmConsumesPanelFlags(d, ap, bp)) {
+            gmk::PanelFlags& f = ready.b;
+            f.flags = rp->second.entry->pieceReady;
+            f.target = rp->second.version;
+            f.origin = static_cast<std::uint32_t>(e.colStart);  // B column j = matrix column colStart + j
+            f.chunk = static_cast<std::uint32_t>(rp->second.width);
+            f.chunks = rp->second.entry->pieces;
+            f.panel_k = static_cast<std::uint32_t>((plan.k + 63) / 64 * 64);
+            f.num_panels = 1;
+          } else {
+            cudaCheck(cudaStreamWaitEvent(w.compute, rp->second.entry->ready, 0), "gemm: wait replica");
+          }
+        }
         if (wPipe && !alphaZero) {
           auto ai = bandOf.find({&w, {0, ri}});
           auto bi = bandOf.find({&w, {1, ci}});
           if ((ai != bandOf.end() || bi != bandOf.end()) && gemmConsumesPanelFlags(d, ap, bp)) {
-            ready.target = w.readySeq;
-            ready.panel_k = static_cast<std::uint32_t>(panelK);
-            ready.num_panels = static_cast<std::uint32_t>(numPanels);
-            ready.streams = 1;
-            if (ai != bandOf.end()) {
-              ready.a = flagBands[ai->second].flags;
-              ready.a_row0 = static_cast<std::uint32_t>(r0 - plan.rowsOf[w.rank][ri].first);
-              ready.a_chunk_rows = static_cast<std::uint32_t>(kAChunkRows);
-            }
-            if (bi != bandOf.end()) {
-              ready.b = flagBands[bi->second].flags;
-              ready.b_col0 = static_cast<std::uint32_t>(e.colStart - plan.colsOf[w.rank][ci].first);
-              ready.b_chunk_cols = static_cast<std::uint32_t>(kBChunkCols);
-            }
+            auto fill = [&](gmk::PanelFlags& f, const FlagBand& fb, std::uint64_t origin, std::uint64_t chunk) {
+              f.flags = fb.flags;
+              f.target = w.readySeq;
+              f.origin = static_cast<std::uint32_t>(origin);
+              f.chunk = static_cast<std::uint32_t>(chunk);
+              f.chunks = static_cast<std::uint32_t>(fb.chunks);
+              f.panel_k = static_cast<std::uint32_t>(panelK);
+              f.num_panels = static_cast<std::uint32_t>(numPanels);
+            };
+            if (ai != bandOf.end())
+              fill(ready.a, flagBands[ai->second], r0 - plan.rowsOf[w.rank][ri].first, kAChunkRows);
+            if (bi != bandOf.end())
+              fill(ready.b, flagBands[bi->second], e.colStart - plan.colsOf[w.rank][ci].first, kBChunkCols);
           } else if (ai != bandOf.end() || bi != bandOf.end()) {
             // This launch cannot poll (staged operand): whole bands first.
             waitGroup(w, 0);
           }
         }
-        gemmLocal(d, ap, bp, cp, ws, wsb, w.compute, fused_ ? &ep : nullptr, ready.num_panels ? &ready : nullptr);
+        gemmLocal(d, ap, bp, cp, ws, wsb, w.compute, fused_ ? &ep : nullptr, ready.on() ? &ready : nullptr);
       }
       // Row-chunk completion of C (chunked downloads drain behind these).
       for (const auto& rr : chunkRows) {
@@ -2633,6 +2716,12 @@ void Session::execReplicate(std::uint64_t id) {
         e.ld = ld;
         e.alias = false;
       }
+      if (e.pieces != M.layout.tiles.size()) {
+        if (e.pieceReady) w->arena.free(e.pieceReady, w->comm);
+        e.pieces = static_cast<std::uint32_t>(M.layout.tiles.size());
+        e.pieceReady = static_cast<std::uint64_t*>(w->arena.alloc(e.pieces * sizeof(std::uint64_t), w->comm));
+        cudaCheck(cudaMemsetAsync(e.pieceReady, 0, e.pieces * sizeof(std::uint64_t), w->comm), "replica flags");
+      }
       entry = &e;
       targets.push_back(w);
     }
@@ -2663,6 +2752,9 @@ void Session::execReplicate(std::uint64_t id) {
       if (entry) {
         x.dstPtr = static_cast<std::uint8_t*>(entry->full) + (t.first.rowStart * entry->ld + t.first.colStart) * eb;
         x.dstLd = entry->ld;
+        x.flagAddr = entry->pieceReady + ti;  // published by the stream that copied the piece
+        x.flagValue = M.version;
+        x.lastOfBlock = true;
       }
       xs.push_back(x);
     }

@@ -221,6 +221,12 @@ struct ReplicaEntry {
   std::uint64_t version = 0;
   ReplicaState state = ReplicaState::Pending;
   cudaEvent_t ready = nullptr;
+  // One u64 per layout tile (source piece) of the matrix: the replication
+  // job's pull stream writes pieceReady[t] = version once tile t's copy has
+  // landed, so a GEMM reading the replica can start on the pieces already
+  // there (e.g. the next step's forward behind W's re-replication).
+  std::uint64_t* pieceReady = nullptr;
+  std::uint32_t pieces = 0;
 };
 
 struct BandView {
@@ -465,6 +471,8 @@ class Session {
   std::vector<std::uint32_t> localRanks() const;
   // 0 = copy engine (one process), 1 = NCCL, 2 = CUDA IPC copy engine (SPMD).
   int transportKind() const { return ipc_ ? 2 : (nccl_ ? 1 : 0); }
+  // In-GEMM panel pipelining on/off for later GEMMs (consumer-local).
+  void setPanelPipelining(bool on) { panelPipelining_ = on; }
 
   // Issues a Gemm op (gemm() below wraps it). sync: wait for completion
   // like the reference's acked gemm(); otherwise stream-ordered only.
@@ -553,6 +561,7 @@ class Session {
   SessionOptions opts_;
   DescriptorTable table_;
   std::uint64_t rootSeed_ = 0;
+  bool panelPipelining_ = true;
   EventTrace trace_;
   mutable std::mutex statsMu_;
   std::map<std::pair<std::uint32_t, std::uint32_t>, std::array<LinkStats, 3>> links_;

@@ -397,6 +397,10 @@ class Session:
     def getLocalPackedAsync(self, m: DistMatrix, ptr: int, nbytes: int):
         check(_lib.load().gm_matrix_get_local_packed_async(self._h, m.id, ptr, nbytes))
 
+    def setPanelPipelining(self, on: bool):
+        """In-GEMM panel pipelining for later GEMMs (default on)."""
+        check(_lib.load().gm_session_set_panel_pipelining(self._h, 1 if on else 0))
+
     def timerStart(self):
         check(_lib.load().gm_timer_start(self._h))
 

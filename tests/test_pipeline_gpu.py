@@ -31,12 +31,16 @@ def _run(tmp_path, tag, cfg, steps=40):
 
 @pytest.mark.timeout(900)
 def test_panel_pipelining_bitwise_equals_whole_band_path(tmp_path):
-    on, log = _run(tmp_path, "on", "verbose=1")
+    # panel_min_gflop=0: pipeline these test-sized GEMMs too (the product
+    # default pipelines GEMMs of >= 1 TFLOP per worker)
+    on, log = _run(tmp_path, "on", "verbose=1,panel_min_gflop=0")
     off, _ = _run(tmp_path, "off", "panel_flags=0")
-    small, _ = _run(tmp_path, "ring", "ready_slots=48", steps=120)
+    small, _ = _run(tmp_path, "ring", "ready_slots=48,panel_min_gflop=0", steps=120)
     # the pipelined launches really polled flags
     assert "panels=" in log and any(f"panels={p}" in log for p in range(1, 64)), log[-2000:]
     assert any(ln.split("panels=")[1].strip() != "0" for ln in log.splitlines() if "panels=" in ln)
+    # the replica-polling forward ran (a 1-panel B flag set per launch)
+    assert "replica_fwd" in on
     for k in off:
         if k.startswith("chain"):
             continue
@@ -51,7 +55,7 @@ def test_panel_pipelining_bitwise_equals_whole_band_path(tmp_path):
 
 @pytest.mark.timeout(600)
 def test_panel_pipelining_matches_oracle(tmp_path):
-    on, _ = _run(tmp_path, "o", "", steps=2)
+    on, _ = _run(tmp_path, "o", "panel_min_gflop=0", steps=2)
     from paper_1611_07819_b200 import gridmath as G
     m, n, k = 1536, 1280, 4608
     a = O.fill_uniform(m, k, 3, 7)

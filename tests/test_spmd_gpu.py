@@ -7,7 +7,8 @@ requires bitwise equality with the single-GPU result.
 * one rank per GPU (>= 2 GPUs): NCCL control channel, IPC and NCCL planes;
 * two ranks per GPU (any box, including a 1-GPU one): the gloo control
   channel and the IPC copy-engine plane (NCCL cannot put two ranks on one
-  GPU). On a 4-GPU box this runs the 2x4 grid's 8 ranks."""
+  GPU), with in-GEMM panel pipelining forced on for every 16-bit GEMM.
+  On a 4-GPU box this runs the 2x4 grid's 8 ranks."""
 import os
 import socket
 import subprocess
@@ -25,14 +26,17 @@ def _gpus():
     return torch.cuda.device_count() if torch.cuda.is_available() else 0
 
 
-def _run(nproc):
+def _run(nproc, debug_config=None):
     s = socket.socket()
     s.bind(("127.0.0.1", 0))
     port = s.getsockname()[1]
     s.close()
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={nproc}",
            "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.join(ROOT, "tools", "spmd_check.py")]
-    out = subprocess.run(cmd, capture_output=True, text=True, timeout=840)
+    env = dict(os.environ)
+    if debug_config:
+        env["GM_DEBUG_CONFIG"] = debug_config
+    out = subprocess.run(cmd, capture_output=True, text=True, timeout=840, env=env)
     assert out.returncode == 0 and "SPMD_CHECK PASS" in out.stdout, out.stdout[-3000:] + out.stderr[-3000:]
     return out.stdout
 
@@ -49,5 +53,7 @@ def test_spmd_one_rank_per_gpu_matches_single_gpu():
 def test_spmd_two_ranks_per_gpu_gloo_control_matches_single_gpu():
     n = _gpus()
     world = 8 if n >= 4 else (4 if n >= 2 else 2)
-    out = _run(world)
+    # panel_min_gflop=0: the (small) check GEMMs take the in-GEMM panel
+    # pipelining path across ranks too
+    out = _run(world, "panel_min_gflop=0")
     assert f"SPMD_CHECK world={world}" in out and "control=gloo" in out, out[-2000:]

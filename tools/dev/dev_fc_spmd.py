@@ -38,7 +38,17 @@ s.fillUniform(DL, 4)
 s.replicateSync(W)
 s.replicateSync(Bv)
 SC, EU, EB, RCS = 5, 8, 9, 7
+seed = [100]
+
+
+def refill():
+    seed[0] += 2
+    s.fillUniform(X, seed[0])
+    s.fillUniform(DL, seed[0] + 1)
+
+
 ops = [
+    ("fillUniform X + dAct (new batch)", refill),
     ("fwd gemm (W replica)", lambda: s.gemmAsync(X, W, Z)),
     ("biasAdd", lambda: s.opIssue(EB, [Z.id, Bv.id, Z.id], flags=(5,))),
     ("relu", lambda: s.opIssue(EU, [Z.id, ACT.id], flags=(0,))),
@@ -83,7 +93,15 @@ def step():
     for _, fn in ops:
         fn()
 ms = timed(lambda: [step() for _ in range(10)]) / 10
+import time
+s.synchronize()
+t0 = time.perf_counter()
+for _ in range(10):
+    step()
+host = (time.perf_counter() - t0) / 10
+s.synchronize()
 if rank == 0:
+    print(f"{'host issue per step':38s} {host * 1e6:8.1f} us")
     print(f"{'step (async, back to back)':38s} {ms * 1e3:8.1f} us   cache hits/misses {st['cache_hits']}/{st['cache_misses']}")
 s.close()
 dist.destroy_process_group()

@@ -66,6 +66,28 @@ def chain(s, steps, out):
     out["chain"] = s.getDataRaw(X[steps % 2])
 
 
+def replica_forward(s, out):
+    """The FC forward behind W's re-replication: W column-block, every step
+    mutates W, replicates it asynchronously and immediately multiplies by
+    it, so the GEMM reads a replica whose pieces are still landing (it polls
+    the per-piece flags when pipelining is on)."""
+    P = s.workers
+    g = G.makeWorkerGroup(P)
+    batch, fi, fo = 512, 768, 1024
+    X = s.createMatrix(batch, fi, G.Precision.BF16, G.makeRowBlockLayout(batch, fi, g))
+    W = s.createMatrix(fi, fo, G.Precision.BF16, G.makeColBlockLayout(fi, fo, g))
+    Z = s.createMatrix(batch, fo, G.Precision.Single, G.makeRowBlockLayout(batch, fo, g))
+    s.fillUniform(X, 5)
+    s.fillUniform(W, 6, -0.05, 0.05)
+    zs = []
+    for i in range(4):
+        G.mulScalar(s, W, 1.25)
+        s.replicateAsync(W)
+        s.gemmAsync(X, W, Z)
+        zs.append(s.getDataRaw(Z))
+    out["replica_fwd"] = np.stack(zs)
+
+
 def main():
     path = sys.argv[1]
     steps = int(sys.argv[2]) if len(sys.argv) > 2 else 40
@@ -73,6 +95,7 @@ def main():
     with G.Session(workers=4, devices=[0], panel_cache_bytes=1) as s:
         cases(s, out)
         chain(s, steps, out)
+        replica_forward(s, out)
     ref = {}
     with G.Session(workers=1, devices=[0]) as s1:  # single worker: no exchange at all
         chain(s1, steps, ref)
