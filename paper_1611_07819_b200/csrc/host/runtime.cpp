@@ -2599,6 +2599,9 @@ bool Session::fusableBiasRelu(const std::vector<OpDescriptor>& ops, std::size_t 
   // served from a copied replica is not fused: the GEMM would then wait for
   // that replication (issued after W's at the end of the previous step),
   // which measured 17 us slower per FC step at N = 2 than the separate ops.
+  // (Replicating small matrices on the compute stream instead, so the bias
+  // lands first, measured worse: the compute stream then waits on the peers'
+  // bias writes every step -- FC step N = 4 0.655 -> 0.74 ms.)
   for (const auto& tl : C.layout.tiles) {
     const Rect need{0, 1, tl.first.colStart, tl.first.colEnd()};
     bool own = false;
@@ -2703,6 +2706,7 @@ void Session::execReplicate(std::uint64_t id) {
         continue;
       }
       const std::uint64_t ld = paddedLd(M.cols, eb);
+      cudaStream_t base = w->comm;
       if (e.full && !e.alias) {
         // GEMMs on the compute stream may still read the previous version.
         cudaEvent_t ev = w->event();
@@ -2711,16 +2715,16 @@ void Session::execReplicate(std::uint64_t id) {
         w->recycle(ev);
       }
       if (!e.full || e.alias || e.ld != ld) {
-        if (e.full && !e.alias) w->arena.free(e.full, w->comm);
-        e.full = w->arena.alloc(M.rows * ld * eb, w->comm);
+        if (e.full && !e.alias) w->arena.free(e.full, base);
+        e.full = w->arena.alloc(M.rows * ld * eb, base);
         e.ld = ld;
         e.alias = false;
       }
       if (e.pieces != M.layout.tiles.size()) {
-        if (e.pieceReady) w->arena.free(e.pieceReady, w->comm);
+        if (e.pieceReady) w->arena.free(e.pieceReady, base);
         e.pieces = static_cast<std::uint32_t>(M.layout.tiles.size());
-        e.pieceReady = static_cast<std::uint64_t*>(w->arena.alloc(e.pieces * sizeof(std::uint64_t), w->comm));
-        cudaCheck(cudaMemsetAsync(e.pieceReady, 0, e.pieces * sizeof(std::uint64_t), w->comm), "replica flags");
+        e.pieceReady = static_cast<std::uint64_t*>(w->arena.alloc(e.pieces * sizeof(std::uint64_t), base));
+        cudaCheck(cudaMemsetAsync(e.pieceReady, 0, e.pieces * sizeof(std::uint64_t), base), "replica flags");
       }
       entry = &e;
       targets.push_back(w);
