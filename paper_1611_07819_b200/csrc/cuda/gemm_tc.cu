@@ -46,7 +46,6 @@ namespace gmk {
 constexpr uint32_t kBlockMcta = 128;  // accumulator rows per CTA (TMEM lanes)
 constexpr uint32_t kMmaN = 256;       // N of one tcgen05.mma (TMEM columns per chunk)
 constexpr uint32_t kSwizzleBytes = 128;
-constexpr uint32_t kNumThreads = 192;  // 6 warps
 
 // Operand element = 2 bytes (kind::f16) or 4 bytes (kind::tf32). A k-block
 // is one 128-byte swizzle row: 64 x 16-bit or 32 x 32-bit elements.
@@ -67,8 +66,14 @@ struct TcCfg {
   static constexpr uint32_t kParts = kSplit ? 2 : 1;               // hi (+ lo)
   static constexpr uint32_t kStageBytes = kParts * (kBytesA + kBytesB);
   static constexpr uint32_t kStages = (192u * 1024u) / kStageBytes;
-  // Epilogue staging for TMA stores: 4 warps x 2 buffers x (32 rows x 128 B).
+  // Epilogue warps: 4 (one per TMEM lane quarter), 8 for the wide tile (two
+  // per quarter, each draining half of the 512 accumulator columns), so the
+  // single-buffered wide accumulator is released twice as fast.
+  static constexpr uint32_t kEpiWarps = kChunks == 2 ? 8 : 4;
+  static constexpr uint32_t kThreads = (2 + kEpiWarps) * 32;
+  // Epilogue staging for TMA stores: 32 KB over the epilogue warps.
   static constexpr uint32_t kStagingBytes = 4u * 2u * 4096u;
+  static constexpr uint32_t kWarpStaging = kStagingBytes / kEpiWarps;
   static constexpr uint32_t kSmemBytes = kStages * kStageBytes + kStagingBytes + 1024 + 256;
   static constexpr uint32_t kClusterCtas = kCG;
   static_assert(kAccStages * kChunks * kMmaN <= 512, "TMEM columns");
@@ -290,7 +295,7 @@ __device__ __forceinline__ void store_row32(const TcParams& p, uint32_t row, uin
 
 // kSplit: 3xTF32 (maps a_hi/a_lo, b_hi/b_lo). Otherwise a single pair.
 template <int kCG, int kElemBytes, int kSplit, int kChunks>
-__global__ void __launch_bounds__(kNumThreads, 1)
+__global__ void __launch_bounds__(TcCfg<kCG, kElemBytes, kSplit, kChunks>::kThreads, 1)
     tc_gemm_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid_constant__ CUtensorMap tm_b,
                    const __grid_constant__ CUtensorMap tm_a_lo,
                    const __grid_constant__ CUtensorMap tm_b_lo,
@@ -334,7 +339,7 @@ __global__ void __launch_bounds__(kNumThreads, 1)
     }
     for (uint32_t a = 0; a < kAcc; ++a) {
       mbar_init(&tfull_bar[a], 1);
-      mbar_init(&tempty_bar[a], 4 * kCG);
+      mbar_init(&tempty_bar[a], Cfg::kEpiWarps * kCG);
     }
     fence_barrier_init();
   }
@@ -528,8 +533,12 @@ __global__ void __launch_bounds__(kNumThreads, 1)
   } else {
     // ------------------------------------------------------------ epilogue
     const uint32_t lane_grp = warp & 3;  // TMEM lanes [32*lane_grp, +32)
-    const uint32_t ew = warp - 2;        // epilogue warp 0..3
-    uint8_t* stg = staging + ew * 2 * 4096;
+    const uint32_t ew = warp - 2;        // epilogue warp 0 .. kEpiWarps-1
+    uint8_t* stg = staging + ew * Cfg::kWarpStaging;
+    // Columns of the tile this warp drains: all of them, or one half when
+    // two warps share a lane quarter.
+    constexpr uint32_t kCols = Cfg::kBlockN * 4 / Cfg::kEpiWarps;
+    const uint32_t col_begin = (ew / 4) * kCols;
     const uint32_t cbytes = p.c_dtype == 2 ? 4 : 2;
     uint32_t acc = 0, acc_phase = 0, iter = 0;
     uint32_t fq = 0;  // fold mode: k-chunks consumed so far
@@ -543,19 +552,16 @@ __global__ void __launch_bounds__(kNumThreads, 1)
         store_row32(p, row, nb * Cfg::kBlockN + c, v, alpha_eff);
         return;
       }
-      // 16-bit C: a slice is 2 KB, so the warp's 8 KB holds four of them
-      // (three stores in flight while the next slice is staged); fp32 C: two.
-      uint8_t* buf;
-      if (p.act_tma) {
-        // Fused bias/relu: C and act slices side by side (2 x 2 KB), two pairs in flight.
-        buf = stg + (iter & 1) * 4096;
-        if (lane == 0 && iter >= 2) bulk_wait_read<1>();
-      } else if (cbytes == 2) {
-        buf = stg + (iter & 3) * 2048;
-        if (lane == 0 && iter >= 4) bulk_wait_read<3>();
-      } else {
-        buf = stg + (iter & 1) * 4096;
-        if (lane == 0 && iter >= 2) bulk_wait_read<1>();
+      // A slot holds one slice: 2 KB for 16-bit C, 4 KB for fp32 C or a
+      // fused C + act pair; the warp's staging holds `slots` of them (that
+      // many stores in flight while the next slice is staged).
+      const uint32_t slot_bytes = (p.act_tma || cbytes == 4) ? 4096u : 2048u;
+      const uint32_t slots = Cfg::kWarpStaging / slot_bytes;
+      uint8_t* buf = stg + (iter % slots) * slot_bytes;
+      if (lane == 0 && iter >= slots) {
+        if (slots >= 4) bulk_wait_read<3>();
+        else if (slots == 2) bulk_wait_read<1>();
+        else bulk_wait_read<0>();
       }
       ++iter;
       __syncwarp();
@@ -668,11 +674,11 @@ __global__ void __launch_bounds__(kNumThreads, 1)
       // after all stores.
       uint32_t va[32], vb[32];
       __syncwarp();
-      tmem_ld_32x32b_x32(taddr, va);
+      tmem_ld_32x32b_x32(taddr + col_begin, va);
       tmem_wait_ld();
 #pragma unroll 1
-      for (uint32_t c = 0; c < Cfg::kBlockN; c += 64) {
-        const bool more = c + 64 < Cfg::kBlockN;
+      for (uint32_t c = col_begin; c < col_begin + kCols; c += 64) {
+        const bool more = c + 64 < col_begin + kCols;
         tmem_ld_32x32b_x32(taddr + c + 32, vb);
         emit(nb, row0, row, c, va, p.alpha);
         tmem_wait_ld();
@@ -808,7 +814,7 @@ int resident_ctas(int dev) {
     auto kern = tc_gemm_kernel<kCG, kElemBytes, kSplit, kChunks>;
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::kSmemBytes);
     cudaLaunchConfig_t cfg{};
-    cfg.blockDim = dim3(kNumThreads, 1, 1);
+    cfg.blockDim = dim3(Cfg::kThreads, 1, 1);
     cfg.dynamicSmemBytes = Cfg::kSmemBytes;
     cfg.gridDim = dim3(sm_count(dev), 1, 1);
     cudaLaunchAttribute attrs[1];
@@ -876,7 +882,7 @@ int launch(const TcOperand& a, const TcOperand& b, const TcOperand* a_lo, const 
   cudaGetDevice(&dev);
   auto kern = tc_gemm_kernel<kCG, kElemBytes, kSplit, kChunks>;
   cudaLaunchConfig_t cfg{};
-  cfg.blockDim = dim3(kNumThreads, 1, 1);
+  cfg.blockDim = dim3(Cfg::kThreads, 1, 1);
   cfg.dynamicSmemBytes = Cfg::kSmemBytes;
   cfg.stream = stream;
   cudaLaunchAttribute attrs[1];
