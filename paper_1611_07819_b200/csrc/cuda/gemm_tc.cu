@@ -936,7 +936,10 @@ int launch(const TcOperand& a, const TcOperand& b, const TcOperand* a_lo, const 
 bool wide_tiles(uint64_t m, uint64_t n, uint64_t k, int cg) {
   const int env_chunks = debug_config().tc_chunks;
   if (env_chunks) return env_chunks == 2;
-  if (!(k >= 4096 && n > kMmaN)) return false;
+  // k >= 2048: with 8 epilogue warps draining the single accumulator the
+  // wide tile beats 256-wide tiles from k = 2048 on (8192^2: 252 vs 266 us),
+  // not at 1024 (166 vs 154).
+  if (!(k >= 2048 && n > kMmaN)) return false;
   int dev = 0;
   cudaGetDevice(&dev);
   const uint64_t units = static_cast<uint64_t>(sm_count(dev)) / cg;

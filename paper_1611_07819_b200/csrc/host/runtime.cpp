@@ -2139,7 +2139,18 @@ void Session::execGemm(const OpDescriptor& op) {
       for (const BlockXfer& bx : blockXfers) all.push_back(bx.x);
       batches.push_back(std::move(all));
     }
-    for (std::uint32_t gi = 0; gi <= S; ++gi) {
+    // Group order on the comm stream: B first (every row chunk of C needs
+    // it), unless B was written after A -- then A's pulls go first, so they
+    // do not queue behind pulls that wait for B's later write (the FC dW
+    // GEMM: X is a new batch written at the step's start, delta only by the
+    // reluGrad just before). lastMut_ is replicated, so every rank issues the
+    // groups in the same order (the NCCL plane needs that).
+    const auto lmA = lastMut_.find(A.matrixId), lmB = lastMut_.find(B.matrixId);
+    const bool aFirst = !pipelined && S >= 1 && lmA != lastMut_.end() && lmB != lastMut_.end() &&
+                        lmB->second > lmA->second;
+    std::vector<std::uint32_t> order;
+    for (std::uint32_t gi = 0; gi <= S; ++gi) order.push_back(aFirst ? (gi + 1) % (S + 1) : gi);
+    for (std::uint32_t gi : order) {
       if (!pipelined && !groups[gi].empty()) exchange(groups[gi], true, false);
       if (pipelined && gi == 0 && !batches[0].empty()) exchange(batches[0], true, false);
       if (pipelined ? gi != 0 : groups[gi].empty()) continue;
