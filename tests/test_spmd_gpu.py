@@ -57,3 +57,20 @@ def test_spmd_two_ranks_per_gpu_gloo_control_matches_single_gpu():
     # pipelining path across ranks too
     out = _run(world, "panel_min_gflop=0")
     assert f"SPMD_CHECK world={world}" in out and "control=gloo" in out, out[-2000:]
+
+
+@pytest.mark.timeout(1200)
+def test_spmd_headline_size_on_the_bench_grid_matches_single_gpu():
+    """bf16 32768^3 on the bench's grid (2 ranks on a 1-GPU box, 1x2; 8 ranks
+    = the 2x4 grid on a 4-GPU box) plus a dependent GEMM on its output, every
+    rank's tiles bitwise equal to one GPU."""
+    n = _gpus()
+    world = 8 if n >= 4 else 2
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.join(ROOT, "tools", "spmd_fullsize.py")]
+    out = subprocess.run(cmd, capture_output=True, text=True, timeout=1100)
+    assert out.returncode == 0 and "SPMD_FULLSIZE PASS" in out.stdout, out.stdout[-3000:] + out.stderr[-3000:]
