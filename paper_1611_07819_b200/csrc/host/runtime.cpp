@@ -1942,7 +1942,6 @@ void Session::execGemm(const OpDescriptor& op) {
           const std::size_t bi = flagBands.size();
           flagBands.push_back(fb);
           for (const PieceRoute& pr : nd.pieces) {
-            Worker* sw = local(pr.src);
             const std::uint64_t m0 = chunkRows ? pr.rect.r0 - nd.rect.r0 : pr.rect.c0 - nd.rect.c0;
             const std::uint64_t m1 = chunkRows ? pr.rect.r1 - nd.rect.r0 : pr.rect.c1 - nd.rect.c0;
             const std::uint64_t k0 = chunkRows ? pr.rect.c0 - nd.rect.c0 : pr.rect.r0 - nd.rect.r0;
@@ -1974,7 +1973,6 @@ void Session::execGemm(const OpDescriptor& op) {
                 bx.chunk = c;
                 bx.panel = pk;
                 blockXfers.push_back(bx);
-                (void)sw;
               }
           }
           break;
