@@ -95,6 +95,7 @@ struct TcParams {
   uint32_t sync_every;                  // k-blocks per lockstep checkpoint
   uint32_t tma_store;                   // C written by TMA stores (beta == 0, aligned C)
   uint32_t fold_kb;                     // k-blocks per folded k-chunk (Single compute), 0 = off
+  uint32_t lockstep_data;               // wait at lockstep checkpoints before all panels landed
   // Fused FC forward epilogue (bf16 C only; null = off): bias[col] of the
   // local C columns, act = relu output with pitch ld_act.
   const uint16_t* bias;
@@ -372,17 +373,19 @@ __global__ void __launch_bounds__(TcCfg<kCG, kElemBytes, kSplit, kChunks>::kThre
       const uint32_t a_kbp = rd.a.flags ? rd.a.panel_k / kBlockK : 0;  // k-blocks per panel
       const uint32_t b_kbp = rd.b.flags ? rd.b.panel_k / kBlockK : 0;
       // While panels are still landing, pairs stall on data at different
-      // times; lockstep timeouts then say nothing about residency, so they
-      // only end the wait for the current tile. They count towards the
-      // launch-wide cut-off once every block has landed.
+      // times, so a lockstep timeout then says nothing about residency: it
+      // ends the wait for the current tile only, and counts towards the
+      // launch-wide cut-off once every block has landed. (Not waiting at all
+      // during that phase measured worse: the pairs drift apart and lose
+      // their L2 reuse -- dependent chain N = 2 26.41 vs 25.77 ms.)
       bool data_done = !rd.on();
       uint32_t local_tile = 0;
       for (uint32_t t = unit; t < num_tiles; t += num_units, ++local_tile) {
         uint32_t mb, nb;
         tile_coords(t, p, p.num_n_blocks, mb, nb);
         const int32_t m0 = static_cast<int32_t>(mb * kBlockMcta * kCG + rank * kBlockMcta);
-        bool wait_sync = synced && timeouts < kMaxLockstepTimeouts;
         if (!data_done) data_done = all_ready(rd);
+        bool wait_sync = synced && (data_done || p.lockstep_data) && timeouts < kMaxLockstepTimeouts;
         // Flag blocks this CTA's loads touch: its own 128 rows of A, the
         // tile's columns of B.
         uint32_t ac0 = 0, ac1 = 0, bc0 = 0, bc1 = 0;
@@ -878,6 +881,7 @@ int launch(const TcOperand& a, const TcOperand& b, const TcOperand* a_lo, const 
   const uint32_t kblocks = (p.k + Cfg::kBlockK - 1) / Cfg::kBlockK;
   p.sync_every = dbg.tc_sync >= 0 ? static_cast<uint32_t>(dbg.tc_sync) : (kblocks >= 64 && kChunks == 2 ? 8u : 0u);
   p.sync_ctr = nullptr;
+  p.lockstep_data = static_cast<uint32_t>(dbg.lockstep_data);
   if (p.group > p.num_m_blocks) p.group = p.num_m_blocks;
   p.num_n_blocks = (p.n + Cfg::kBlockN - 1) / Cfg::kBlockN;
   int dev = 0;

@@ -2092,12 +2092,25 @@ void Session::execGemm(const OpDescriptor& op) {
         waveOff += (tiles + tp.units - 1) / tp.units;
       }
     });
+    // An operand whose last write is older goes first as a whole: its pulls
+    // can run during the previous GEMM (prefetch) instead of queueing on the
+    // pull streams behind blocks that wait for a newer write (a dependent
+    // chain's A is the previous GEMM's output; its B is not).
+    auto lastWriteOf = [&](int operand) {
+      auto it = lastMut_.find(operand == 0 ? A.matrixId : B.matrixId);
+      return it == lastMut_.end() ? std::uint64_t{0} : it->second;
+    };
+    const std::uint64_t lwA = lastWriteOf(0), lwB = lastWriteOf(1);
+    const bool byClass = dbg.class_sort != 0;
+    auto cls = [&](int operand) {
+      return (!byClass || lwA == lwB) ? 0 : ((operand == 0) == (lwA > lwB) ? 1 : 0);
+    };
     std::stable_sort(blockXfers.begin(), blockXfers.end(), [&](const BlockXfer& x, const BlockXfer& y) {
       const FlagBand& fx = flagBands[x.band];
       const FlagBand& fy = flagBands[y.band];
       if (fx.w->rank != fy.w->rank) return fx.w->rank < fy.w->rank;
-      const auto kx = std::make_tuple(firstWave[x.band][x.chunk], x.panel, fx.operand, x.chunk, x.band);
-      const auto ky = std::make_tuple(firstWave[y.band][y.chunk], y.panel, fy.operand, y.chunk, y.band);
+      const auto kx = std::make_tuple(cls(fx.operand), firstWave[x.band][x.chunk], x.panel, fx.operand, x.chunk, x.band);
+      const auto ky = std::make_tuple(cls(fy.operand), firstWave[y.band][y.chunk], y.panel, fy.operand, y.chunk, y.band);
       return kx < ky;
     });
     // Blocks copied from the consumer's own tiles (HBM -> HBM) alternate
