@@ -48,7 +48,7 @@ loops = {
     "dep": lambda i: s.gemmAsync(pair[i % 2], B, pair[(i + 1) % 2], alpha, 0.0),
 }
 res = {(m, k): [] for m in (1, 0) for k in loops}
-for rnd in range(3):
+for rnd in range(int(os.environ.get("AB_ROUNDS", "5"))):
     for mode in (1, 0):
         s.setPanelPipelining(bool(mode))
         for k, fn in loops.items():
@@ -62,7 +62,7 @@ DL = s.createMatrix(batch, fo, G.Precision.BF16, G.makeRowBlockLayout(batch, fo,
 dW = s.createMatrix(fi, fo, G.Precision.BF16, G.makeColBlockLayout(fi, fo, g))
 s.fillUniform(DL, 4)
 fc = {1: [], 0: []}
-for rnd in range(3):
+for rnd in range(int(os.environ.get("AB_ROUNDS", "5"))):
     for mode in (1, 0):
         s.setPanelPipelining(bool(mode))
         fc[mode].append(timed(lambda i: (s.fillUniform(X, 100 + i), s.gemmAsync(X, DL, dW, 1.0, 0.0, True, False)), 10))
