@@ -38,7 +38,12 @@ enum { GM_HALF = 0, GM_SINGLE = 1, GM_DOUBLE = 2, GM_BF16 = 3 };
 /* Math mode for Single-compute GEMMs, carried in OpDescriptor.flags[3]
  * (unused by the reference's Gemm, kernels.cpp:209-211). */
 enum { GM_MATH_DEFAULT = 0, /* 3xTF32: fp32-accurate */
-       GM_MATH_TF32 = 1     /* 1xTF32: opt-in, ~1e-4 rel */ };
+       GM_MATH_TF32 = 1,    /* 1xTF32: opt-in, ~1e-4 rel */
+       /* 16-bit operands (fp32 accumulate): fold the tensor cores' fp32
+        * accumulation into a round-to-nearest fp32 running sum every 256 of
+        * k, as the Single path does -- the error of the reference's serial
+        * fp32 sum instead of one that grows with k (opt-in; 256-wide tiles). */
+       GM_MATH_FOLD = 2 };
 
 /* Replication states (reference gridmath::ReplState, session.hpp:36). */
 enum { GM_REPL_IN_FLIGHT = 0, GM_REPL_DONE = 1, GM_REPL_FAILED = 2 };

@@ -16,7 +16,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libgridmath_b200.so")
 
 GM_HALF, GM_SINGLE, GM_DOUBLE, GM_BF16 = 0, 1, 2, 3
-GM_MATH_DEFAULT, GM_MATH_TF32 = 0, 1
+GM_MATH_DEFAULT, GM_MATH_TF32, GM_MATH_FOLD = 0, 1, 2
 GM_REPL_IN_FLIGHT, GM_REPL_DONE, GM_REPL_FAILED = 0, 1, 2
 GM_OP_SET_CONST, GM_OP_GEMM, GM_OP_ADD_ROW_COL_SUM, GM_OP_EW_UNARY, GM_OP_EW_BINARY = 5, 6, 7, 8, 9
 

@@ -357,7 +357,7 @@ __global__ void __launch_bounds__(TcCfg<kCG, kElemBytes, kSplit, kChunks>::kThre
   const uint32_t num_kb = (p.k + kBlockK - 1) / kBlockK;
   // Fold mode (tf32 kinds, 256-wide tiles): one chunk accumulator plus a
   // running-sum region in TMEM instead of two tile accumulators.
-  const bool fold = kChunks == 1 && kElemBytes == 4 && p.fold_kb > 0;
+  const bool fold = kChunks == 1 && p.fold_kb > 0;
   const uint32_t unit = blockIdx.x / Cfg::kClusterCtas, num_units = gridDim.x / Cfg::kClusterCtas;
 
   if (warp == 0) {
@@ -1011,6 +1011,17 @@ int tc_gemm(const TcGemmArgs& g, cudaStream_t stream, const char** err) {
   if (g.kind == TcKind::F16 || g.kind == TcKind::BF16) {
     const uint32_t fmt = g.kind == TcKind::BF16 ? 1 : 0;
     p.idesc = make_idesc(fmt, fmt, p.a_mn_major, p.b_mn_major, mrows, kMmaN);
+    if (g.fold_k) {
+      // k-chunk folding (GM_MATH_FOLD): 256-wide tiles, TMEM split into the
+      // chunk accumulator and the running sum.
+      if (g.fold_k % 64 || g.bias) {
+        *err = "tc_gemm: 16-bit fold_k must be a multiple of 64 (and no fused epilogue)";
+        return 1;
+      }
+      p.fold_kb = static_cast<uint32_t>(g.fold_k / 64);  // 64 16-bit elements per k-block
+      return cg == 1 ? launch<1, 2, 0, 1>(g.a, g.b, nullptr, nullptr, p, g.max_ctas, stream, err)
+                     : launch<2, 2, 0, 1>(g.a, g.b, nullptr, nullptr, p, g.max_ctas, stream, err);
+    }
     // Wide tiles (256 x 512 per CTA pair, two UMMAs per k-step) halve the
     // distinct A panels in flight and cut L2->SMEM traffic by a quarter;
     // their single accumulator leaves the epilogue unoverlapped, which only

@@ -357,6 +357,11 @@ void gemmLocal(const gm_gemm_desc& d, const void* a, const void* b, void* c, voi
     const std::uint64_t L = tf32Chunk();
     if (d.k > L) g.fold_k = L;
   }
+  if (pl.path == Plan::F16 && d.math == GM_MATH_FOLD && !ep) {
+    // Same fixed global k-chunks as the Single path: layout/P independent.
+    const std::uint64_t L = tf32Chunk();
+    if (d.k > L) g.fold_k = L;
+  }
   if (ep) {
     g.bias = ep->bias;
     g.act = ep->act;

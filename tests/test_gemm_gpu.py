@@ -291,3 +291,27 @@ def test_ragged_shapes_vs_oracle(m, n, k):
                                        0.75, 0.5, ta, tb)
                 err = O.rel_fro(O.to_f64(got, pc), O.to_f64(want, pc))
                 assert err <= tol, (m, n, k, pa, pb, pc, ta, tb, p, err)
+
+
+@pytest.mark.parametrize("tb", [0, 1])
+def test_bf16_fold_mode_matches_reference_serial_sum(tb):
+    """GM_MATH_FOLD: bf16 operands, Single C, long k -- the accumulation is
+    folded into a round-to-nearest fp32 sum every 256 of k, so the result
+    tracks the reference's serial fp32 chain (runGemm<float>) far closer than
+    the default whole-k tensor-core accumulation; layout-invariant bitwise."""
+    m, n, k = 512, 384, 16384
+    a = O.fill_uniform(m, k, 3, 41)
+    b = O.fill_uniform(n, k, 3, 42) if tb else O.fill_uniform(k, n, 3, 42)
+    c = np.zeros((m, n), dtype=np.float32)
+    rows = (100, 132)
+    want = O.gemm_c(m, n, k, a, 3, b, 3, c, 1, 1.0, 0.0, 0, tb, rows)[rows[0]:rows[1]]
+    grid = lambda r, cc: O.grid_tiles(r, cc, 2, 2)
+    bt = grid(n, k) if tb else grid(k, n)
+    fold = run_session_gemm(4, a, 3, grid(m, k), b, 3, bt, c, 1, grid(m, n), 1.0, 0.0, 0, tb, math=2)
+    plain = run_session_gemm(4, a, 3, grid(m, k), b, 3, bt, c, 1, grid(m, n), 1.0, 0.0, 0, tb, math=0)
+    e_fold = O.rel_fro(fold[rows[0]:rows[1]], want)
+    e_plain = O.rel_fro(plain[rows[0]:rows[1]], want)
+    assert e_fold <= 1e-5 and e_fold < e_plain / 2, (e_fold, e_plain)
+    one = run_session_gemm(1, a, 3, O.grid_tiles(m, k, 1, 1), b, 3, O.grid_tiles(*b.shape, 1, 1), c, 1,
+                           O.grid_tiles(m, n, 1, 1), 1.0, 0.0, 0, tb, math=2)
+    assert np.array_equal(fold.view(np.uint8), one.view(np.uint8))
