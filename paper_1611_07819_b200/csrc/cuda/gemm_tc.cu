@@ -66,10 +66,11 @@ struct TcCfg {
   static constexpr uint32_t kParts = kSplit ? 2 : 1;               // hi (+ lo)
   static constexpr uint32_t kStageBytes = kParts * (kBytesA + kBytesB);
   static constexpr uint32_t kStages = (192u * 1024u) / kStageBytes;
-  // Epilogue warps: 4 (one per TMEM lane quarter), 8 for the wide tile (two
-  // per quarter, each draining half of the 512 accumulator columns), so the
-  // single-buffered wide accumulator is released twice as fast.
-  static constexpr uint32_t kEpiWarps = kChunks == 2 ? 8 : 4;
+  // Epilogue warps: 8 for the 16-bit kinds (two per TMEM lane quarter, each
+  // draining half of the accumulator columns), so the single-buffered wide
+  // accumulator -- and a folded k-chunk -- is released twice as fast; 4 (one
+  // per quarter) for the tf32 kinds, whose register count leaves no room.
+  static constexpr uint32_t kEpiWarps = kElemBytes == 2 ? 8 : 4;
   static constexpr uint32_t kThreads = (2 + kEpiWarps) * 32;
   // Epilogue staging for TMA stores: 32 KB over the epilogue warps.
   static constexpr uint32_t kStagingBytes = 4u * 2u * 4096u;
@@ -649,13 +650,13 @@ __global__ void __launch_bounds__(TcCfg<kCG, kElemBytes, kSplit, kChunks>::kThre
           tc_fence_after();
           const bool last = q + 1 == nq;
 #pragma unroll 1
-          for (uint32_t c = 0; c < Cfg::kBlockN; c += 32) {
+          for (uint32_t c = col_begin; c < col_begin + kCols; c += 32) {
             uint32_t v[32], sum[32];
             __syncwarp();
             tmem_ld_32x32b_x32(tchunk + c, v);
             if (q > 0) tmem_ld_32x32b_x32(tsum + c, sum);
             tmem_wait_ld();
-            if (c + 32 == Cfg::kBlockN) release(0);  // chunk buffer fully read
+            if (c + 32 == col_begin + kCols) release(0);  // this warp's part of the chunk buffer read
 #pragma unroll
             for (int i = 0; i < 32; ++i) {
               const float x = __uint_as_float(v[i]);
