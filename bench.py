@@ -13,7 +13,15 @@ device) and resident in HBM when the timed region starts; A, B, C are
 2 GiB each, far larger than L2 (no flush needed). `value` is device time
 (CUDA events on every worker stream, max over ranks); `e2e` repeats the step
 through the public API from pinned host buffers (H2D of the local A/B tiles,
-gemm, D2H of the local C tile inside the timed region).
+gemm, D2H of the local C tile inside the timed region). `dependent` times the
+same GEMM in a chain A_i = a C_{i-1} B, whose A panels cannot move before the
+previous GEMM ends (the in-GEMM panel pipelining carries it). `nvlink` carries
+the planner's bytes per step, the event-timed exchange of one isolated op, and
+NVML NVLink byte counters around the timed loop where the driver supports them
+(`counters.unavailable` says why not).
+
+--config fc / fp64: BASELINE configs[3] / [4] (secondary lines; the FC step
+gets a new X and dAct every step and reports bytes received per step).
 
 --impl reference times the reference's own CPU implementation (the
 unmodified library compiled into oracle/_ref from /root/reference) on this

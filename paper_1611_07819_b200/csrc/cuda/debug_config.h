@@ -17,6 +17,7 @@ struct DebugConfig {
   int l2_promo = 128;      // TMA L2 promotion bytes (0, 64, 128, 256)
   int hint_a = 0, hint_b = 0;  // TMA L2 cache hints (0 normal, 1 evict_last, 2 evict_first)
   int panel_flags = 1;     // 0 = GEMM waits for whole bands (no in-kernel panel pipelining)
+  int pdl = 1;             // 0 = no programmatic dependent launch between GEMM kernels
   int lockstep_data = 1;   // 0 = pairs do not wait at lockstep checkpoints while panels are landing
   int class_sort = 1;      // 0 = pipelined blocks purely in need order (no older-operand-first)
   int panel_min_gflop = -1;  // pipeline GEMMs of at least this many GFLOP per worker (-1 = 1000)

@@ -353,6 +353,12 @@ __global__ void __launch_bounds__(TcCfg<kCG, kElemBytes, kSplit, kChunks>::kThre
   }
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  // Programmatic dependent launch: this CTA lets the next kernel on the
+  // stream be scheduled onto SMs as they free up, and the prologue above
+  // (barriers, TMEM, descriptor prefetch) overlapped the previous kernel's
+  // tail; global memory is touched only once the previous grid completed.
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  asm volatile("griddepcontrol.wait;" ::: "memory");
 
   const uint32_t num_tiles = p.num_m_blocks * p.num_n_blocks;
   const uint32_t num_kb = (p.k + kBlockK - 1) / kBlockK;
@@ -892,13 +898,15 @@ int launch(const TcOperand& a, const TcOperand& b, const TcOperand* a_lo, const 
   cfg.blockDim = dim3(Cfg::kThreads, 1, 1);
   cfg.dynamicSmemBytes = Cfg::kSmemBytes;
   cfg.stream = stream;
-  cudaLaunchAttribute attrs[1];
+  cudaLaunchAttribute attrs[2];
   attrs[0].id = cudaLaunchAttributeClusterDimension;
   attrs[0].val.clusterDim.x = Cfg::kClusterCtas;
   attrs[0].val.clusterDim.y = 1;
   attrs[0].val.clusterDim.z = 1;
+  attrs[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attrs[1].val.programmaticStreamSerializationAllowed = dbg.pdl ? 1 : 0;
   cfg.attrs = attrs;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = 2;
   const int res = resident_ctas<kCG, kElemBytes, kSplit, kChunks>(dev);
   int ctas = res;
   if (max_ctas > 0 && max_ctas < ctas) ctas = max_ctas;

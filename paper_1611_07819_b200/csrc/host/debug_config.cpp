@@ -24,7 +24,7 @@ const DebugConfig& debug_config() {
                         {"hint_b", &c.hint_b},             {"panel_flags", &c.panel_flags},
                         {"ready_slots", &c.ready_slots},
                         {"panel_k", &c.panel_k},           {"lockstep_data", &c.lockstep_data},
-                        {"class_sort", &c.class_sort},           {"panel_min_gflop", &c.panel_min_gflop},           {"a_chunk_rows", &c.a_chunk_rows},
+                        {"class_sort", &c.class_sort},           {"pdl", &c.pdl},           {"panel_min_gflop", &c.panel_min_gflop},           {"a_chunk_rows", &c.a_chunk_rows},
                         {"b_chunk_cols", &c.b_chunk_cols},
                         {"pull_streams", &c.pull_streams}, {"fuse_epilogue", &c.fuse_epilogue},
                         {"tf32_chunk", &c.tf32_chunk},     {"verbose", &c.verbose}};
