@@ -339,7 +339,7 @@ __global__ void __launch_bounds__(TcCfg<kCG, kElemBytes, kSplit, kChunks>::kThre
       mbar_init(&full_bar[s], 1);
       mbar_init(&empty_bar[s], 1);
     }
-    for (uint32_t a = 0; a < kAcc; ++a) {
+    for (uint32_t a = 0; a < 2; ++a) {  // wide tiles: [0] / [1] = the two accumulator halves
       mbar_init(&tfull_bar[a], 1);
       mbar_init(&tempty_bar[a], Cfg::kEpiWarps * kCG);
     }
@@ -484,13 +484,81 @@ __global__ void __launch_bounds__(TcCfg<kCG, kElemBytes, kSplit, kChunks>::kThre
       const uint32_t a_step = p.a_mn_major ? kMmaK * kSwizzleBytes : 32;
       const uint32_t b_step = p.b_mn_major ? kMmaK * kSwizzleBytes : 32;
       uint32_t fq = 0;  // fold mode: k-chunks issued so far
+      // Issues k-block kq's UMMAs of chunks [c0, c1) from `stage`.
+      auto issue = [&](uint32_t stage_i, uint32_t kq, uint32_t tmem_acc, uint32_t c0, uint32_t c1) {
+        const uint32_t sa = smem_u32(smem + stage_i * Cfg::kStageBytes);
+        const uint32_t sb = sa + Cfg::kParts * Cfg::kBytesA;
+#pragma unroll
+        for (uint32_t kk = 0; kk < kBlockK / kMmaK; ++kk) {
+          const uint32_t first = (kq | kk) == 0 ? 0u : 1u;
+          const uint64_t ah = sdesc_sw128(sa + kk * a_step, a_lbo, 1024);
+#pragma unroll
+          for (uint32_t c = 0; c < kChunks; ++c) {
+            if (c < c0 || c >= c1) continue;
+            const uint32_t tmem_d = tmem_acc + c * kMmaN;
+            const uint32_t bc = sb + c * Cfg::kBytesBChunk;
+            const uint64_t bh = sdesc_sw128(bc + kk * b_step, b_lbo, 1024);
+            if constexpr (kSplit) {
+              const uint64_t al = sdesc_sw128(sa + Cfg::kBytesA + kk * a_step, a_lbo, 1024);
+              const uint64_t bl = sdesc_sw128(bc + Cfg::kBytesB + kk * b_step, b_lbo, 1024);
+              mma_tf32<kCG>(tmem_d, al, bh, p.idesc, first);
+              mma_tf32<kCG>(tmem_d, ah, bl, p.idesc, 1u);
+              mma_tf32<kCG>(tmem_d, ah, bh, p.idesc, 1u);
+            } else if constexpr (kElemBytes == 4) {
+              mma_tf32<kCG>(tmem_d, ah, bh, p.idesc, first);
+            } else {
+              mma_f16<kCG>(tmem_d, ah, bh, p.idesc, first);
+            }
+          }
+        }
+      };
+      auto commit_stage = [&](uint32_t stage_i) {
+        if constexpr (kCG == 2) mma_commit_2sm(&empty_bar[stage_i], pair_mask);
+        else mma_commit(&empty_bar[stage_i]);
+      };
       for (uint32_t t = unit; t < num_tiles; t += num_units) {
-        if (!fold) {
+        uint32_t kb0 = 0;  // k-blocks already issued for this tile
+        if (kChunks == 2 && !fold) {
+          // Wide tile: the epilogue frees the accumulator's low half (chunk
+          // 0's columns) before the high half, so chunk 0 of the first
+          // staged k-blocks starts while chunk 1 is still being drained;
+          // each chunk's k order is unchanged (bitwise identical results).
+          mbar_wait(&tempty_bar[0], acc_phase ^ 1);
+          tc_fence_after();
+          const uint32_t ahead = min(kStages, num_kb);
+          const uint32_t s0 = stage, ph0 = phase;
+          for (uint32_t j = 0; j < ahead; ++j) {
+            mbar_wait(&full_bar[stage], phase);
+            tc_fence_after();
+            issue(stage, j, tmem_base, 0, 1);
+            if (++stage == kStages) {
+              stage = 0;
+              phase ^= 1;
+            }
+          }
+          mbar_wait(&tempty_bar[1], acc_phase ^ 1);
+          tc_fence_after();
+          stage = s0;
+          phase = ph0;
+          for (uint32_t j = 0; j < ahead; ++j) {
+            issue(stage, j, tmem_base, 1, 2);
+            commit_stage(stage);
+            if (j + 1 == num_kb) {
+              if constexpr (kCG == 2) mma_commit_2sm(&tfull_bar[0], pair_mask);
+              else mma_commit(&tfull_bar[0]);
+            }
+            if (++stage == kStages) {
+              stage = 0;
+              phase ^= 1;
+            }
+          }
+          kb0 = ahead;
+        } else if (!fold) {
           mbar_wait(&tempty_bar[acc], acc_phase ^ 1);
           tc_fence_after();
         }
         const uint32_t tmem_acc = fold ? tmem_base : tmem_base + acc * kChunks * kMmaN;
-        for (uint32_t kb = 0; kb < num_kb; ++kb) {
+        for (uint32_t kb = kb0; kb < num_kb; ++kb) {
           const uint32_t kq = fold ? kb % p.fold_kb : kb;  // k-block within the accumulation
           if (fold && kq == 0) {
             mbar_wait(&tempty_bar[0], (fq & 1) ^ 1);  // chunk buffer folded by the epilogue
@@ -498,32 +566,8 @@ __global__ void __launch_bounds__(TcCfg<kCG, kElemBytes, kSplit, kChunks>::kThre
           }
           mbar_wait(&full_bar[stage], phase);
           tc_fence_after();
-          const uint32_t sa = smem_u32(smem + stage * Cfg::kStageBytes);
-          const uint32_t sb = sa + Cfg::kParts * Cfg::kBytesA;
-#pragma unroll
-          for (uint32_t kk = 0; kk < kBlockK / kMmaK; ++kk) {
-            const uint32_t first = (kq | kk) == 0 ? 0u : 1u;
-            const uint64_t ah = sdesc_sw128(sa + kk * a_step, a_lbo, 1024);
-#pragma unroll
-            for (uint32_t c = 0; c < kChunks; ++c) {
-              const uint32_t tmem_d = tmem_acc + c * kMmaN;
-              const uint32_t bc = sb + c * Cfg::kBytesBChunk;
-              const uint64_t bh = sdesc_sw128(bc + kk * b_step, b_lbo, 1024);
-              if constexpr (kSplit) {
-                const uint64_t al = sdesc_sw128(sa + Cfg::kBytesA + kk * a_step, a_lbo, 1024);
-                const uint64_t bl = sdesc_sw128(bc + Cfg::kBytesB + kk * b_step, b_lbo, 1024);
-                mma_tf32<kCG>(tmem_d, al, bh, p.idesc, first);
-                mma_tf32<kCG>(tmem_d, ah, bl, p.idesc, 1u);
-                mma_tf32<kCG>(tmem_d, ah, bh, p.idesc, 1u);
-              } else if constexpr (kElemBytes == 4) {
-                mma_tf32<kCG>(tmem_d, ah, bh, p.idesc, first);
-              } else {
-                mma_f16<kCG>(tmem_d, ah, bh, p.idesc, first);
-              }
-            }
-          }
-          if constexpr (kCG == 2) mma_commit_2sm(&empty_bar[stage], pair_mask);
-          else mma_commit(&empty_bar[stage]);
+          issue(stage, kq, tmem_acc, 0, kChunks);
+          commit_stage(stage);
           if (fold ? (kq + 1 == p.fold_kb || kb + 1 == num_kb) : kb + 1 == num_kb) {
             if constexpr (kCG == 2) mma_commit_2sm(&tfull_bar[fold ? 0 : acc], pair_mask);
             else mma_commit(&tfull_bar[fold ? 0 : acc]);
@@ -682,22 +726,33 @@ __global__ void __launch_bounds__(TcCfg<kCG, kElemBytes, kSplit, kChunks>::kThre
       // slice s is converted and stored. TMA-store path: the accumulator is
       // released as soon as the last slice is in registers; the direct path
       // after all stores.
+      // Wide tiles drain chunk 0's columns first (released on tempty[0]),
+      // then chunk 1's (tempty[1]): the MMA warp restarts chunk 0 early.
+      // Each warp takes a quarter-row slice of each chunk.
+      constexpr bool kSplitRelease = kChunks == 2;
+      constexpr uint32_t kSegs = kSplitRelease ? 2 : 1;
+      constexpr uint32_t kSegCols = kSplitRelease ? kMmaN * 4 / Cfg::kEpiWarps : kCols;
       uint32_t va[32], vb[32];
-      __syncwarp();
-      tmem_ld_32x32b_x32(taddr + col_begin, va);
-      tmem_wait_ld();
 #pragma unroll 1
-      for (uint32_t c = col_begin; c < col_begin + kCols; c += 64) {
-        const bool more = c + 64 < col_begin + kCols;
-        tmem_ld_32x32b_x32(taddr + c + 32, vb);
-        emit(nb, row0, row, c, va, p.alpha);
+      for (uint32_t seg = 0; seg < kSegs; ++seg) {
+        const uint32_t c_begin = kSplitRelease ? seg * kMmaN + (ew / 4) * kSegCols : col_begin;
+        const uint32_t rel = kSplitRelease ? seg : acc;
+        __syncwarp();
+        tmem_ld_32x32b_x32(taddr + c_begin, va);
         tmem_wait_ld();
-        if (p.tma_store && !more) release(acc);
-        if (more) tmem_ld_32x32b_x32(taddr + c + 64, va);
-        emit(nb, row0, row, c + 32, vb, p.alpha);
-        if (more) tmem_wait_ld();
+#pragma unroll 1
+        for (uint32_t c = c_begin; c < c_begin + kSegCols; c += 64) {
+          const bool more = c + 64 < c_begin + kSegCols;
+          tmem_ld_32x32b_x32(taddr + c + 32, vb);
+          emit(nb, row0, row, c, va, p.alpha);
+          tmem_wait_ld();
+          if (p.tma_store && !more) release(rel);
+          if (more) tmem_ld_32x32b_x32(taddr + c + 64, va);
+          emit(nb, row0, row, c + 32, vb, p.alpha);
+          if (more) tmem_wait_ld();
+        }
+        if (!p.tma_store) release(rel);
       }
-      if (!p.tma_store) release(acc);
       if (++acc == kAcc) {
         acc = 0;
         acc_phase ^= 1;
