@@ -350,6 +350,17 @@ int gm_session_transport(gm_session* s, int32_t* kind);
  * it off for later GEMMs of this session (they wait for whole bands). Local
  * to this process (SPMD ranks may differ). */
 int gm_session_set_panel_pipelining(gm_session* s, int32_t on);
+/* Pipeline replay as one CUDA graph per process (default off, or
+ * GM_DEBUG_CONFIG graph_replay=1): the first replay of a pipeline runs op by
+ * op, later ones are stream-captured and launched as one graph whose
+ * executable is updated in place. The reference's replay is one control
+ * message per step (session.cpp:385-409); bitwise the same results either
+ * way. Off by default because the graph boundary serialises consecutive
+ * steps (measured slower). */
+int gm_session_set_graph_replay(gm_session* s, int32_t on);
+/* Launches, instantiations (over all pipelines) and node count of the last
+ * captured replay graph. */
+int gm_session_graph_stats(gm_session* s, uint64_t* launches, uint64_t* instantiations, uint64_t* nodes);
 /* Device time of the last gm_gemm/gm_gemm_async per local worker (ms),
  * measured with CUDA events on the worker's compute stream. */
 int gm_last_op_device_ms(gm_session* s, float* ms, uint32_t cap, uint32_t* n);

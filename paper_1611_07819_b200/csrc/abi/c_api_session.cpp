@@ -366,6 +366,19 @@ int gm_session_set_panel_pipelining(gm_session* s, int32_t on) {
   return guard([&] { s->s->setPanelPipelining(on != 0); });
 }
 
+int gm_session_set_graph_replay(gm_session* s, int32_t on) {
+  return guard([&] { s->s->setGraphReplay(on != 0); });
+}
+
+int gm_session_graph_stats(gm_session* s, uint64_t* launches, uint64_t* instantiations, uint64_t* nodes) {
+  return guard([&] {
+    const gridmath::Session::GraphStats g = s->s->graphStats();
+    *launches = g.launches;
+    *instantiations = g.instantiations;
+    *nodes = g.nodes;
+  });
+}
+
 int gm_last_op_device_ms(gm_session* s, float* ms, uint32_t cap, uint32_t* n) {
   return guard([&] {
     const auto v = s->s->lastOpDeviceMs();

@@ -848,9 +848,24 @@ int sm_count(int dev) {
 // the last pair of each launch zeroes the counter, so one zeroed counter per
 // (device, stream) serves every launch without aliasing (stream ids are
 // unique for the process lifetime, cudaStreamGetId).
+// cudaStreamGetId invalidates a stream capture in progress (CUDA-graph
+// replay, host/capture.hpp): while capturing, the counter is found by the
+// stream handle, as the last uncaptured launch on that handle resolved it
+// (none yet: no lockstep for this launch).
 uint32_t* lockstep_counter(int dev, cudaStream_t stream) {
   static std::mutex mu;
   static std::map<std::pair<int, unsigned long long>, uint32_t*> ctrs;
+  static std::map<std::pair<int, cudaStream_t>, uint32_t*> byHandle;
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  if (cudaStreamIsCapturing(stream, &cs) != cudaSuccess) {
+    cudaGetLastError();
+    return nullptr;
+  }
+  if (cs != cudaStreamCaptureStatusNone) {
+    std::lock_guard<std::mutex> lock(mu);
+    auto h = byHandle.find({dev, stream});
+    return h == byHandle.end() ? nullptr : h->second;
+  }
   unsigned long long sid = 0;
   if (cudaStreamGetId(stream, &sid) != cudaSuccess) {
     cudaGetLastError();
@@ -858,7 +873,10 @@ uint32_t* lockstep_counter(int dev, cudaStream_t stream) {
   }
   std::lock_guard<std::mutex> lock(mu);
   auto it = ctrs.find({dev, sid});
-  if (it != ctrs.end()) return it->second;
+  if (it != ctrs.end()) {
+    byHandle[{dev, stream}] = it->second;
+    return it->second;
+  }
   uint32_t* c = nullptr;
   if (cudaMalloc(&c, sizeof(uint32_t)) != cudaSuccess || cudaMemsetAsync(c, 0, sizeof(uint32_t), stream) != cudaSuccess) {
     cudaGetLastError();
@@ -866,6 +884,7 @@ uint32_t* lockstep_counter(int dev, cudaStream_t stream) {
     return nullptr;
   }
   ctrs[{dev, sid}] = c;
+  byHandle[{dev, stream}] = c;
   return c;
 }
 

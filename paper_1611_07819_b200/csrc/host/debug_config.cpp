@@ -27,7 +27,8 @@ const DebugConfig& debug_config() {
                         {"class_sort", &c.class_sort},           {"pdl", &c.pdl},           {"panel_min_gflop", &c.panel_min_gflop},           {"a_chunk_rows", &c.a_chunk_rows},
                         {"b_chunk_cols", &c.b_chunk_cols},
                         {"pull_streams", &c.pull_streams}, {"fuse_epilogue", &c.fuse_epilogue},
-                        {"tf32_chunk", &c.tf32_chunk},     {"verbose", &c.verbose}};
+                        {"tf32_chunk", &c.tf32_chunk},     {"verbose", &c.verbose},
+                        {"graph_replay", &c.graph_replay}};
     std::string s(env);
     std::size_t pos = 0;
     while (pos < s.size()) {

@@ -1,4 +1,5 @@
 // SPDX-License-Identifier: Apache-2.0
+#include "capture.hpp"
 #include "device.hpp"
 
 #include <algorithm>
@@ -58,7 +59,7 @@ void* DeviceArena::alloc(std::uint64_t bytes, cudaStream_t stream, std::uint64_t
     Block b = *pick;
     list.erase(pick);
     if (b.released) {
-      cudaCheck(cudaStreamWaitEvent(stream, b.released, 0), "arena: wait on release");
+      cudaCheck(capture::wait(stream, b.released, 0), "arena: wait on release");
       eventPool_.push_back(b.released);
     }
     stats_.reuses += 1;
@@ -94,7 +95,7 @@ void DeviceArena::free(void* p, cudaStream_t stream, std::uint64_t epoch) {
   } else {
     cudaCheck(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming), "arena: event");
   }
-  cudaCheck(cudaEventRecord(ev, stream), "arena: record release");
+  cudaCheck(capture::record(ev, stream), "arena: record release");
   free_[cls].push_back(Block{p, ev, epoch});
   stats_.frees += 1;
   stats_.held_bytes += cls;

@@ -15,6 +15,7 @@
 
 #include <algorithm>
 
+#include "capture.hpp"
 #include "internal.hpp"
 #include "runtime.hpp"
 
@@ -79,7 +80,7 @@ void Session::setLocalPackedAsync(DistMatrix m, const void* host, std::uint64_t 
                                     src + r * rowBytes, rowBytes, rowBytes, n, cudaMemcpyDefault, w->h2d),
                   "upload: chunk");
         Worker::UploadChunk c{e.rowStart + r, e.rowStart + r + n, w->event()};
-        cudaCheck(cudaEventRecord(c.done, w->h2d), "upload: chunk event");
+        cudaCheck(capture::record(c.done, w->h2d), "upload: chunk event");
         if (ipc_)  // peers pulling these rows wait for this value (ChunkedWrite::base)
           ipcWrite(w->h2d, w->flags + kUpChunkOff + slotOf(m.id()),
                    chunked_.at(m.id()).base[w->rank] + static_cast<std::uint64_t>(up.chunks.size()) + 1);
@@ -91,7 +92,7 @@ void Session::setLocalPackedAsync(DistMatrix m, const void* host, std::uint64_t 
   for (Worker* w : started) {
     Worker::Upload& up = w->uploads[m.id()];
     up.done = w->event();
-    cudaCheck(cudaEventRecord(up.done, w->h2d), "upload: done");
+    cudaCheck(capture::record(up.done, w->h2d), "upload: done");
   }
 }
 
@@ -133,14 +134,14 @@ void Session::getLocalPackedAsync(DistMatrix m, void* host, std::uint64_t bytes)
       }
       if (parts.empty() || !contiguous || covered != e.rowEnd()) {
         cudaEvent_t ev = w->event();
-        cudaCheck(cudaEventRecord(ev, w->compute), "download: order");
+        cudaCheck(capture::record(ev, w->compute), "download: order");
         parts.assign(1, Worker::UploadChunk{e.rowStart, e.rowEnd(), ev});
-        cudaCheck(cudaStreamWaitEvent(w->d2h, ev, 0), "download: wait");
+        cudaCheck(capture::wait(w->d2h, ev, 0), "download: wait");
         w->recycle(ev);
         parts[0].done = nullptr;
       }
       for (const auto& p : parts) {
-        if (p.done) cudaCheck(cudaStreamWaitEvent(w->d2h, p.done, 0), "download: wait chunk");
+        if (p.done) cudaCheck(capture::wait(w->d2h, p.done, 0), "download: wait chunk");
         const std::uint64_t r = p.r0 - e.rowStart;
         cudaCheck(cudaMemcpy2DAsync(dst + r * rowBytes, rowBytes, static_cast<const std::uint8_t*>(dt.ptr) + r * dt.ld * eb,
                                     dt.ld * eb, rowBytes, p.r1 - p.r0, cudaMemcpyDefault, w->d2h),
@@ -152,7 +153,7 @@ void Session::getLocalPackedAsync(DistMatrix m, void* host, std::uint64_t bytes)
   // WAR: the next mutation of m waits for these reads.
   for (Worker* w : used) {
     cudaEvent_t e = w->event();
-    cudaCheck(cudaEventRecord(e, w->d2h), "download: done");
+    cudaCheck(capture::record(e, w->d2h), "download: done");
     w->addReader(m.id(), e, w);
   }
 }

@@ -20,6 +20,7 @@
 
 #include <algorithm>
 
+#include "capture.hpp"
 #include "../cuda/fc_ops.h"
 #include "internal.hpp"
 #include "runtime.hpp"
@@ -41,7 +42,7 @@ void Session::resolveReads(std::vector<ReadNeed>& needs, std::uint64_t mutated, 
         throw Error("replica of matrix " + std::to_string(M.matrixId) + " not readable on worker " +
                     std::to_string(nd.worker));
       w->activate();
-      cudaCheck(cudaStreamWaitEvent(w->compute, it->second.ready, 0), "pointwise: wait replica");
+      cudaCheck(capture::wait(w->compute, it->second.ready, 0), "pointwise: wait replica");
       nd.view = offsetView(it->second.full, it->second.ld, nd.rect.r0, nd.rect.c0, eb);
       continue;
     }
@@ -61,7 +62,7 @@ void Session::resolveReads(std::vector<ReadNeed>& needs, std::uint64_t mutated, 
       CacheEntry* hit = dir.lookup(M.matrixId, M.version, nd.rect, tick_);  // LRU on every rank
       if (!w) continue;
       w->activate();
-      cudaCheck(cudaStreamWaitEvent(w->compute, hit->ready, 0), "pointwise: wait panel");
+      cudaCheck(capture::wait(w->compute, hit->ready, 0), "pointwise: wait panel");
       nd.view = {hit->ptr, hit->ld};
       continue;
     }
@@ -215,8 +216,8 @@ void Session::runPointwise(const OpDescriptor& op0, bool sync) {
       if (!w || j.byRows || forked.count(w)) continue;
       w->activate();
       cudaEvent_t e = w->event();
-      cudaCheck(cudaEventRecord(e, w->compute), "addRowColSum: fork");
-      cudaCheck(cudaStreamWaitEvent(w->aux, e, 0), "addRowColSum: fork");
+      cudaCheck(capture::record(e, w->compute), "addRowColSum: fork");
+      cudaCheck(capture::wait(w->aux, e, 0), "addRowColSum: fork");
       w->recycle(e);
       forked.insert(w);
     }
@@ -247,8 +248,8 @@ void Session::runPointwise(const OpDescriptor& op0, bool sync) {
   for (Worker* w : forked) {
     w->activate();
     cudaEvent_t e = w->event();
-    cudaCheck(cudaEventRecord(e, w->aux), "addRowColSum: join");
-    cudaCheck(cudaStreamWaitEvent(w->compute, e, 0), "addRowColSum: join");
+    cudaCheck(capture::record(e, w->aux), "addRowColSum: join");
+    cudaCheck(capture::wait(w->compute, e, 0), "addRowColSum: join");
     w->recycle(e);
   }
   for (auto& tp : temps) {

@@ -14,6 +14,7 @@
 // tensor-core kernel) instead of 256-wide host panels; the per-element
 // order is therefore independent of the layout and of P (deterministic
 // mode, reference kernels.hpp:19-22).
+#include "capture.hpp"
 #include "runtime.hpp"
 
 #include <cuda.h>  // types of the driver entry points (resolved at run time, no -lcuda)
@@ -293,7 +294,7 @@ std::uint64_t Worker::reserveReady(std::uint64_t n) {
   if (start % readyCap + n > readyCap) start += readyCap - start % readyCap;  // contiguous in memory
   const std::uint64_t end = start + n;
   while (!readyInUse.empty() && readyInUse.front().first + readyCap < end) {
-    cudaCheck(cudaStreamWaitEvent(comm, readyInUse.front().done, 0), "gemm: ready region reuse");
+    cudaCheck(capture::wait(comm, readyInUse.front().done, 0), "gemm: ready region reuse");
     recycle(readyInUse.front().done);
     readyInUse.pop_front();
   }
@@ -350,7 +351,7 @@ void Worker::joinUpload(std::uint64_t matrix) {
   auto it = uploads.find(matrix);
   if (it == uploads.end()) return;
   activate();
-  cudaCheck(cudaStreamWaitEvent(compute, it->second.done, 0), "upload: join");
+  cudaCheck(capture::wait(compute, it->second.done, 0), "upload: join");
   for (auto& c : it->second.chunks) recycle(c.done);
   recycle(it->second.done);
   uploads.erase(it);
@@ -400,7 +401,7 @@ void Worker::beforeMutation(std::uint64_t matrix, cudaStream_t on) {
   if (it == readers_.end()) return;
   activate();
   for (auto& rd : it->second) {
-    cudaCheck(cudaStreamWaitEvent(on ? on : compute, rd.first, 0), "worker: wait reader");
+    cudaCheck(capture::wait(on ? on : compute, rd.first, 0), "worker: wait reader");
     rd.second->recycle(rd.first);
   }
   readers_.erase(it);
@@ -632,7 +633,7 @@ void Session::flushWritten(std::uint64_t before) {
       // A pending chunked upload is the write being published: from the h2d
       // stream, after its last chunk (the compute stream has not joined it).
       cudaStream_t ws = w.uploads.count(pw.first) ? w.h2d : w.compute;
-      cudaCheck(cudaEventRecord(e, ws), "worker: record write");
+      cudaCheck(capture::record(e, ws), "worker: record write");
       if (ipc_) ipcWrite(ws, w.flags + slotOf(pw.first), pw.second);
     }
   }
@@ -746,6 +747,7 @@ Session::~Session() {
   // worker goes away.
   for (auto& w : workers_)
     if (w) w->releaseReaders();
+  graphs_.clear();
   workers_.clear();
 }
 
@@ -842,7 +844,7 @@ std::uint64_t Session::issue(OpDescriptor& op) {
       wp->activate();
       cudaEvent_t& e = wp->lastTouch[id];
       if (!e) cudaCheck(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "worker: touch event");
-      cudaCheck(cudaEventRecord(e, wp->compute), "worker: record touch");
+      cudaCheck(capture::record(e, wp->compute), "worker: record touch");
     }
   pendingTouched_.clear();
   for (std::uint64_t id : op.ids)
@@ -925,7 +927,7 @@ void Session::mutationHook(std::uint64_t id, std::uint64_t oldVersion, bool toH2
     w.dropChunkDone(id);
     if (toH2d) {
       auto lt = w.lastTouch.find(id);
-      if (lt != w.lastTouch.end()) cudaCheck(cudaStreamWaitEvent(w.h2d, lt->second, 0), "upload: wait last use");
+      if (lt != w.lastTouch.end()) cudaCheck(capture::wait(w.h2d, lt->second, 0), "upload: wait last use");
     }
     // Peers that pulled from this worker's tiles of the matrix (SPMD
     // copy-engine plane) must be done before it changes.
@@ -1040,7 +1042,7 @@ void Session::execDestroy(std::uint64_t id) {
     }
     auto rit = w.replicas.find(id);
     if (rit != w.replicas.end()) {
-      cudaStreamWaitEvent(w.compute, rit->second.ready, 0);
+      capture::wait(w.compute, rit->second.ready, 0);
       if (!rit->second.alias) w.arena.free(rit->second.full, w.compute);
       if (rit->second.pieceReady) w.arena.free(rit->second.pieceReady, w.compute);
       cudaEventDestroy(rit->second.ready);
@@ -1280,7 +1282,7 @@ void Session::reshape(DistMatrix m, const Layout& newLayout, std::optional<Preci
           auto it = w->replicas.find(old.matrixId);
           if (it == w->replicas.end() || it->second.version != old.version)
             throw Error("reshape: replica of matrix " + std::to_string(old.matrixId) + " missing");
-          cudaCheck(cudaStreamWaitEvent(w->compute, it->second.ready, 0), "reshape: wait replica");
+          cudaCheck(capture::wait(w->compute, it->second.ready, 0), "reshape: wait replica");
           cudaCheck(cudaMemcpy2DAsync(dst, dstLd * oldEb,
                                       static_cast<const std::uint8_t*>(it->second.full) +
                                           (e.rowStart * it->second.ld + e.colStart) * oldEb,
@@ -1383,8 +1385,8 @@ void Session::exchange(std::vector<Xfer>& xs, bool onComm, bool commit, int maxP
       cudaStream_t ps = fixed >= 0 ? d.pulls[fixed % Worker::kPullStreams] : d.pulls[src % np];
       if (forked.insert({&d, ps}).second) {
         cudaEvent_t e = d.event();
-        cudaCheck(cudaEventRecord(e, streamOf(d)), "exchange: fork");
-        cudaCheck(cudaStreamWaitEvent(ps, e, 0), "exchange: fork");
+        cudaCheck(capture::record(e, streamOf(d)), "exchange: fork");
+        cudaCheck(capture::wait(ps, e, 0), "exchange: fork");
         d.recycle(e);
       }
       return ps;
@@ -1398,7 +1400,7 @@ void Session::exchange(std::vector<Xfer>& xs, bool onComm, bool commit, int maxP
       if (s) {
         auto it = s->lastWrite.find(x.matrix);
         if (it != s->lastWrite.end() && (s != &d || onComm))
-          cudaCheck(cudaStreamWaitEvent(ps, it->second, 0), "exchange: wait writer");
+          cudaCheck(capture::wait(ps, it->second, 0), "exchange: wait writer");
       } else {
         ipcWait(ps, peerFlags_[x.src] + slotOf(x.matrix), lastMut_.at(x.matrix));
       }
@@ -1454,7 +1456,7 @@ void Session::exchange(std::vector<Xfer>& xs, bool onComm, bool commit, int maxP
             if (ord >= chunks.size()) throw Error("exchange: upload chunk geometry mismatch");
             // (the upload runs on the h2d stream: waited even for own tiles)
             if (chunkWaited.insert({x.dst, chunks[ord].done, ps}).second)
-              cudaCheck(cudaStreamWaitEvent(ps, chunks[ord].done, 0), "exchange: wait chunk");
+              cudaCheck(capture::wait(ps, chunks[ord].done, 0), "exchange: wait chunk");
           } else {
             const std::uint64_t v = cw->base[x.src] + ord + 1;
             if (flagWaited.insert({x.dst, x.src, v, ps}).second)
@@ -1479,8 +1481,8 @@ void Session::exchange(std::vector<Xfer>& xs, bool onComm, bool commit, int maxP
       Worker& d = *fk.first;
       d.activate();
       cudaEvent_t e = d.event();
-      cudaCheck(cudaEventRecord(e, fk.second), "exchange: join");
-      cudaCheck(cudaStreamWaitEvent(streamOf(d), e, 0), "exchange: join");
+      cudaCheck(capture::record(e, fk.second), "exchange: join");
+      cudaCheck(capture::wait(streamOf(d), e, 0), "exchange: join");
       d.recycle(e);
     }
     for (const auto& rt : routes) {
@@ -1490,7 +1492,7 @@ void Session::exchange(std::vector<Xfer>& xs, bool onComm, bool commit, int maxP
         if (s == &d && !onComm) continue;
         d.activate();
         cudaEvent_t e = d.event();
-        cudaCheck(cudaEventRecord(e, streamOf(d)), "exchange: record done");
+        cudaCheck(capture::record(e, streamOf(d)), "exchange: record done");
         s->addReader(std::get<2>(rt), e, &d);
       } else {
         pendingReads_.insert({std::get<1>(rt), std::get<2>(rt), sIdx});
@@ -1509,7 +1511,7 @@ void Session::exchange(std::vector<Xfer>& xs, bool onComm, bool commit, int maxP
     auto it = s.lastWrite.find(rs.second);
     if (onComm && it != s.lastWrite.end()) {
       s.activate();
-      cudaCheck(cudaStreamWaitEvent(s.comm, it->second, 0), "exchange: wait writer");
+      cudaCheck(capture::wait(s.comm, it->second, 0), "exchange: wait writer");
     }
   }
   struct Staged {
@@ -1590,7 +1592,7 @@ void Session::exchange(std::vector<Xfer>& xs, bool onComm, bool commit, int maxP
       Worker& s = *local(rs.first);
       s.activate();
       cudaEvent_t e = s.event();
-      cudaCheck(cudaEventRecord(e, s.comm), "exchange: record");
+      cudaCheck(capture::record(e, s.comm), "exchange: record");
       s.addReader(rs.second, e, &s);
     }
   }
@@ -1693,7 +1695,7 @@ void Session::execGemm(const OpDescriptor& op) {
 
   forEachLocal([&](Worker& w) {
     w.timed = true;
-    cudaCheck(cudaEventRecord(w.tStart, w.compute), "gemm: timing");
+    cudaCheck(capture::recordTiming(w.tStart, w.compute), "gemm: timing");
   });
 
   auto dirOf = [&](std::uint32_t r) -> PanelCache& {
@@ -1865,10 +1867,10 @@ void Session::execGemm(const OpDescriptor& op) {
             if (Worker* sw = local(tl.second.rank)) {
               auto lw = sw->lastWrite.find(M.matrixId);
               if (lw != sw->lastWrite.end() && sw != w)
-                cudaCheck(cudaStreamWaitEvent(w->compute, lw->second, 0), "gemm: wait replica source");
+                cudaCheck(capture::wait(w->compute, lw->second, 0), "gemm: wait replica source");
             }
         } else {
-          cudaCheck(cudaStreamWaitEvent(w->compute, it->second.ready, 0), "gemm: wait replica");
+          cudaCheck(capture::wait(w->compute, it->second.ready, 0), "gemm: wait replica");
         }
         view = offsetView(it->second.full, it->second.ld, nd.rect.r0, nd.rect.c0, eb);
         break;
@@ -1885,7 +1887,7 @@ void Session::execGemm(const OpDescriptor& op) {
         CacheEntry* hit = cachedHits[ni];
         if (!w) break;
         w->activate();
-        cudaCheck(cudaStreamWaitEvent(w->compute, hit->ready, 0), "gemm: wait panel");
+        cudaCheck(capture::wait(w->compute, hit->ready, 0), "gemm: wait panel");
         view = {hit->ptr, hit->ld};
         break;
       }
@@ -2040,7 +2042,7 @@ void Session::execGemm(const OpDescriptor& op) {
   flushWritten(curExec_);
   forEachLocal([&](Worker& w) {
     w.commTimed = anyXfer;
-    if (anyXfer) cudaCheck(cudaEventRecord(w.cStart, w.comm), "gemm: comm timing");
+    if (anyXfer) cudaCheck(capture::recordTiming(w.cStart, w.comm), "gemm: comm timing");
   });
   // Pipelined mode: order each local consumer's blocks by when its GEMM
   // first needs them -- the wave of the persistent grid whose tiles first
@@ -2169,21 +2171,21 @@ void Session::execGemm(const OpDescriptor& op) {
         if (!wp) continue;
         wp->activate();
         cudaEvent_t ev = wp->event();
-        cudaCheck(cudaEventRecord(ev, wp->comm), "gemm: group done");
+        cudaCheck(capture::record(ev, wp->comm), "gemm: group done");
         groupDone[gi].push_back(ev);
       }
     }
   }
   commitReads();
   forEachLocal([&](Worker& w) {
-    if (w.commTimed) cudaCheck(cudaEventRecord(w.cEnd, w.comm), "gemm: comm timing");
+    if (w.commTimed) cudaCheck(capture::recordTiming(w.cEnd, w.comm), "gemm: comm timing");
   });
   // Gathered bands become cache entries ready when the last group lands.
   for (std::size_t i = 0; i < freshEntries.size(); ++i) {
     Worker* w = freshOwners[i];
     w->activate();
     freshEntries[i]->ready = w->event();
-    cudaCheck(cudaEventRecord(freshEntries[i]->ready, w->comm), "gemm: panel ready");
+    cudaCheck(capture::record(freshEntries[i]->ready, w->comm), "gemm: panel ready");
   }
   auto waitGroup = [&](Worker& w, std::uint32_t gi) {
     if (groupDone[gi].empty()) return;
@@ -2191,7 +2193,7 @@ void Session::execGemm(const OpDescriptor& op) {
     for (auto& wp : workers_) {
       if (!wp) continue;
       if (wp.get() == &w) {
-        cudaCheck(cudaStreamWaitEvent(w.compute, groupDone[gi][idx], 0), "gemm: wait group");
+        cudaCheck(capture::wait(w.compute, groupDone[gi][idx], 0), "gemm: wait group");
         return;
       }
       ++idx;
@@ -2215,7 +2217,7 @@ void Session::execGemm(const OpDescriptor& op) {
     if (up == w.uploads.end()) return;
     for (const auto& c : up->second.chunks)
       if (c.r0 < hi && lo < c.r1 && waited.insert(c.done).second)
-        cudaCheck(cudaStreamWaitEvent(w.compute, c.done, 0), "gemm: wait upload chunk");
+        cudaCheck(capture::wait(w.compute, c.done, 0), "gemm: wait upload chunk");
   };
   forEachLocal([&](Worker& w) {
     w.dropChunkDone(C.matrixId);
@@ -2236,18 +2238,18 @@ void Session::execGemm(const OpDescriptor& op) {
         if (!sw) continue;
         auto it = sw->lastWrite.find(bx.x.matrix);
         if (it != sw->lastWrite.end() && raw.insert(it->second).second)
-          cudaCheck(cudaStreamWaitEvent(w.compute, it->second, 0), "gemm: wait source write");
+          cudaCheck(capture::wait(w.compute, it->second, 0), "gemm: wait source write");
       }
     }
     if (!alphaZero)
       for (std::size_t ci = 0; ci < plan.colsOf[w.rank].size(); ++ci)
         if (bLocal[w.rank][ci]) waitUploadRows(w, B.matrixId, 0, ~0ull, waited);
-    cudaCheck(cudaEventRecord(w.kStart, w.compute), "gemm: timing");
+    cudaCheck(capture::recordTiming(w.kStart, w.compute), "gemm: timing");
     if (w.windowOpen) {
       std::pair<cudaEvent_t, cudaEvent_t> ev{};
       cudaCheck(cudaEventCreate(&ev.first), "gemm: window event");
       cudaCheck(cudaEventCreate(&ev.second), "gemm: window event");
-      cudaCheck(cudaEventRecord(ev.first, w.compute), "gemm: timing");
+      cudaCheck(capture::recordTiming(ev.first, w.compute), "gemm: timing");
       w.kernelWindow.push_back(ev);
     }
     for (std::uint32_t j = 0; j < S; ++j) {
@@ -2325,7 +2327,7 @@ void Session::execGemm(const OpDescriptor& op) {
             f.panel_k = static_cast<std::uint32_t>((plan.k + 63) / 64 * 64);
             f.num_panels = 1;
           } else {
-            cudaCheck(cudaStreamWaitEvent(w.compute, rp->second.entry->ready, 0), "gemm: wait replica");
+            cudaCheck(capture::wait(w.compute, rp->second.entry->ready, 0), "gemm: wait replica");
           }
         }
         if (wPipe && !alphaZero) {
@@ -2355,12 +2357,12 @@ void Session::execGemm(const OpDescriptor& op) {
       // Row-chunk completion of C (chunked downloads drain behind these).
       for (const auto& rr : chunkRows) {
         Worker::UploadChunk c{rr.first, rr.second, w.event()};
-        cudaCheck(cudaEventRecord(c.done, w.compute), "gemm: chunk done");
+        cudaCheck(capture::record(c.done, w.compute), "gemm: chunk done");
         w.chunkDone[C.matrixId].push_back(c);
       }
     }
-    cudaCheck(cudaEventRecord(w.tEnd, w.compute), "gemm: timing");
-    if (w.windowOpen) cudaCheck(cudaEventRecord(w.kernelWindow.back().second, w.compute), "gemm: timing");
+    cudaCheck(capture::recordTiming(w.tEnd, w.compute), "gemm: timing");
+    if (w.windowOpen) cudaCheck(capture::recordTiming(w.kernelWindow.back().second, w.compute), "gemm: timing");
     // Flag regions polled by this op's GEMMs become reusable after them.
     for (const FlagBand& fb : flagBands) {
       if (fb.w != &w) continue;
@@ -2368,7 +2370,7 @@ void Session::execGemm(const OpDescriptor& op) {
       rr.first = fb.first;
       rr.end = fb.first + fb.chunks * numPanels;
       rr.done = w.event();
-      cudaCheck(cudaEventRecord(rr.done, w.compute), "gemm: ready region done");
+      cudaCheck(capture::record(rr.done, w.compute), "gemm: ready region done");
       w.readyInUse.push_back(rr);
     }
   });
@@ -2494,11 +2496,11 @@ void Session::timerStart() {
     // The side streams' prior work is part of "before": fold it in.
     for (cudaStream_t side : {w.comm, w.h2d, w.d2h}) {
       cudaEvent_t e = w.event();
-      cudaCheck(cudaEventRecord(e, side), "timer");
-      cudaCheck(cudaStreamWaitEvent(w.compute, e, 0), "timer");
+      cudaCheck(capture::record(e, side), "timer");
+      cudaCheck(capture::wait(w.compute, e, 0), "timer");
       w.recycle(e);
     }
-    cudaCheck(cudaEventRecord(w.uStart, w.compute), "timer start");
+    cudaCheck(capture::record(w.uStart, w.compute), "timer start");
     for (auto& ev : w.kernelWindow) {
       cudaEventDestroy(ev.first);
       cudaEventDestroy(ev.second);
@@ -2528,11 +2530,11 @@ float Session::timerStop() {
   forEachLocal([&](Worker& w) {
     for (cudaStream_t side : {w.comm, w.h2d, w.d2h}) {
       cudaEvent_t e = w.event();
-      cudaCheck(cudaEventRecord(e, side), "timer");
-      cudaCheck(cudaStreamWaitEvent(w.compute, e, 0), "timer");
+      cudaCheck(capture::record(e, side), "timer");
+      cudaCheck(capture::wait(w.compute, e, 0), "timer");
       w.recycle(e);
     }
-    cudaCheck(cudaEventRecord(w.uEnd, w.compute), "timer stop");
+    cudaCheck(capture::record(w.uEnd, w.compute), "timer stop");
     w.windowOpen = false;
     cudaCheck(cudaEventSynchronize(w.uEnd), "timer sync");
     float ms = 0.0f;
@@ -2562,6 +2564,48 @@ void Session::replay(std::uint64_t pipelineId, bool sync) {
   if (!closedPipelines_.count(pipelineId))
     throw Error("replay: unknown or unfinished pipeline " + std::to_string(pipelineId));
   const std::vector<OpDescriptor>& ops = pipelines_.at(pipelineId);
+  // Graph replay (opt-in): the first replay runs op by op (the planner's
+  // steady state: arena blocks, replicas, cached panels); later ones are
+  // captured into one CUDA graph per process (capture.hpp), its executable
+  // updated in place.
+  capture::Graph* graph = nullptr;
+  if (graphReplay_.value_or(gmk::debug_config().graph_replay != 0)) {
+    std::unique_ptr<capture::Graph>& g = graphs_[pipelineId];
+    if (!g) {
+      g = std::make_unique<capture::Graph>();
+    } else {
+      std::vector<capture::WorkerStreams> ws;
+      for (std::uint32_t r : localRanks()) {
+        Worker& w = *local(r);
+        capture::WorkerStreams x;
+        x.device = w.device;
+        x.compute = w.compute;
+        x.side = {w.comm, w.aux, w.h2d, w.d2h};
+        for (cudaStream_t ps : w.pulls) x.side.push_back(ps);
+        ws.push_back(x);
+      }
+      local(localRanks().front())->activate();
+      g->begin(ws);
+      graph = g.get();
+    }
+  }
+  try {
+    replayOps(ops);
+  } catch (...) {
+    if (graph) graph->abort();
+    throw;
+  }
+  if (graph) {
+    graph->endAndLaunch();
+    graphStats_.launches += 1;
+    graphStats_.nodes = graph->nodes;
+    graphStats_.instantiations = 0;
+    for (const auto& kv : graphs_) graphStats_.instantiations += kv.second->instantiations;
+  }
+  if (sync) synchronize();
+}
+
+void Session::replayOps(const std::vector<OpDescriptor>& ops) {
   for (std::size_t i = 0; i < ops.size(); ++i) {
     OpDescriptor step = ops[i];
     step.execId = 0;
@@ -2570,10 +2614,13 @@ void Session::replay(std::uint64_t pipelineId, bool sync) {
       OpDescriptor bo = ops[i + 1], ro = ops[i + 2];
       bo.execId = ro.execId = 0;
       bo.recordPipeline = ro.recordPipeline = 0;
+      capture::checkpoint("replay: before gemm+biasAdd+relu");
       runGemmBiasRelu(step, bo, ro);
+      capture::checkpoint("replay: gemm+biasAdd+relu");
       i += 2;
       continue;
     }
+    capture::checkpoint("replay: before op");
     switch (step.opcode) {
       case OpCode::Gemm:
         runGemm(step, false);
@@ -2590,8 +2637,11 @@ void Session::replay(std::uint64_t pipelineId, bool sync) {
       default:
         throw Error("replay: op not supported on the B200 GEMM path");
     }
+    capture::checkpoint(step.opcode == OpCode::Gemm             ? "replay: gemm"
+                        : step.opcode == OpCode::ReplicateStart ? "replay: replicate"
+                        : step.opcode == OpCode::AddRowColSum   ? "replay: addRowColSum"
+                                                                : "replay: pointwise");
   }
-  if (sync) synchronize();
 }
 
 bool Session::fusableBiasRelu(const std::vector<OpDescriptor>& ops, std::size_t i) const {
@@ -2716,15 +2766,15 @@ void Session::execReplicate(std::uint64_t id) {
         const DeviceTile& dt = w->tiles.at(id).front();
         if (e.full && !e.alias) {
           cudaEvent_t ev = w->event();
-          cudaCheck(cudaEventRecord(ev, w->compute), "replica: record readers");
-          cudaCheck(cudaStreamWaitEvent(w->comm, ev, 0), "replica: wait readers");
+          cudaCheck(capture::record(ev, w->compute), "replica: record readers");
+          cudaCheck(capture::wait(w->comm, ev, 0), "replica: wait readers");
           w->recycle(ev);
           w->arena.free(e.full, w->comm);
         }
         e.full = dt.ptr;
         e.ld = dt.ld;
         e.alias = true;
-        cudaCheck(cudaEventRecord(e.ready, w->compute), "replica ready");
+        cudaCheck(capture::record(e.ready, w->compute), "replica ready");
         continue;
       }
       const std::uint64_t ld = paddedLd(M.cols, eb);
@@ -2732,8 +2782,8 @@ void Session::execReplicate(std::uint64_t id) {
       if (e.full && !e.alias) {
         // GEMMs on the compute stream may still read the previous version.
         cudaEvent_t ev = w->event();
-        cudaCheck(cudaEventRecord(ev, w->compute), "replica: record readers");
-        cudaCheck(cudaStreamWaitEvent(w->comm, ev, 0), "replica: wait readers");
+        cudaCheck(capture::record(ev, w->compute), "replica: record readers");
+        cudaCheck(capture::wait(w->comm, ev, 0), "replica: wait readers");
         w->recycle(ev);
       }
       if (!e.full || e.alias || e.ld != ld) {
@@ -2792,7 +2842,7 @@ void Session::execReplicate(std::uint64_t id) {
   exchange(xs, true, true, 2);
   for (Worker* w : targets) {
     w->activate();
-    cudaCheck(cudaEventRecord(w->replicas[id].ready, w->comm), "replica ready");
+    cudaCheck(capture::record(w->replicas[id].ready, w->comm), "replica ready");
   }
 }
 

@@ -35,6 +35,7 @@
 #include <vector>
 
 #include "../../../include/gridmath_b200.h"
+#include "capture.hpp"
 #include "core.hpp"
 #include "device.hpp"
 #include "ops.hpp"
@@ -436,6 +437,14 @@ class Session {
   std::uint64_t beginRecord();
   void endRecord();
   void replay(std::uint64_t pipelineId, bool sync = true);
+  // Replays after a pipeline's first run as one CUDA graph per process
+  // (capture.hpp). Off by default (measured slower);
+  // GM_DEBUG_CONFIG graph_replay=1 or setGraphReplay(true) turns it on.
+  void setGraphReplay(bool on) { graphReplay_ = on; }
+  struct GraphStats {
+    std::uint64_t launches = 0, instantiations = 0, nodes = 0;  // nodes: last captured graph
+  };
+  GraphStats graphStats() const { return graphStats_; }
 
   ReplicationHandle replicateAsync(DistMatrix m);
   void replicateSync(DistMatrix m);
@@ -486,6 +495,7 @@ class Session {
   };
   const FusedBiasRelu* fused_ = nullptr;
   bool fusableBiasRelu(const std::vector<OpDescriptor>& ops, std::size_t i) const;
+  void replayOps(const std::vector<OpDescriptor>& ops);
   void runGemmBiasRelu(const OpDescriptor& g, const OpDescriptor& bo, const OpDescriptor& ro);
   // FC-layer neighbours on device (reference session.cpp:547-609,
   // kernels.cpp:435-815): SetConst, EwUnary, EwBinary, AddRowColSum.
@@ -568,6 +578,11 @@ class Session {
   void countLink(std::uint32_t src, std::uint32_t dst, MsgKind k, std::uint64_t bytes);
   std::vector<std::unique_ptr<Worker>> workers_;  // indexed by rank; null if remote
   std::vector<PanelCache> remoteCaches_;          // directory for non-local workers (SPMD)
+  // Per pipeline: the captured replay's executable (declared after workers_,
+  // so it is destroyed before them).
+  std::map<std::uint64_t, std::unique_ptr<capture::Graph>> graphs_;
+  std::optional<bool> graphReplay_;
+  GraphStats graphStats_;
   std::map<std::pair<std::uint64_t, std::uint64_t>, bool> replFailed_;
   std::uint64_t nextMatrixId_ = 1;
   // Chunked uploads that are the last write of a matrix. The op carries the

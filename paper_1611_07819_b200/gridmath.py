@@ -401,6 +401,16 @@ class Session:
         """In-GEMM panel pipelining for later GEMMs (default on)."""
         check(_lib.load().gm_session_set_panel_pipelining(self._h, 1 if on else 0))
 
+    def setGraphReplay(self, on: bool):
+        """Replays after a pipeline's first as one CUDA graph (default off)."""
+        check(_lib.load().gm_session_set_graph_replay(self._h, 1 if on else 0))
+
+    def graphStats(self) -> dict:
+        """{launches, instantiations, nodes} of the captured replays."""
+        a, b, c = ctypes.c_uint64(), ctypes.c_uint64(), ctypes.c_uint64()
+        check(_lib.load().gm_session_graph_stats(self._h, ctypes.byref(a), ctypes.byref(b), ctypes.byref(c)))
+        return {"launches": a.value, "instantiations": b.value, "nodes": c.value}
+
     def timerStart(self):
         check(_lib.load().gm_timer_start(self._h))
 

@@ -227,3 +227,55 @@ def test_fused_epilogue_on_column_blocks(p, batch, fin, fout):
     assert n_rep == n_eager - 2 * p, (n_rep, n_eager)
     a = got[1].view(np.uint16)
     assert (a != 0).any() and not (a & 0x8000).any()  # relu output: non-trivial, no negatives
+
+
+@pytest.mark.parametrize("p,prec", [(1, G.Precision.BF16), (1, G.Precision.Single), (4, G.Precision.BF16),
+                                    (2, G.Precision.Single)])
+def test_graph_replay_matches_op_by_op(p, prec):
+    # Replays after the first are captured into one CUDA graph (executable
+    # updated in place); a new batch is written eagerly between replays, as
+    # the bench and the reference Trainer do. Same bits and versions as
+    # replays issued op by op.
+    k = 5
+
+    def run(graph):
+        with G.Session(workers=p) as s:
+            s.setGraphReplay(graph)
+            m = build(s, p, prec)
+            pid = s.beginRecord()
+            step(s, m)
+            s.endRecord()
+            for i in range(k):
+                s.fillUniform(m["X"], 100 + i)
+                s.replay(pid, sync=(i % 2 == 1))
+            s.synchronize()
+            s.verifyMetadataConsistency()
+            return snapshot(s, m), s.graphStats()
+
+    got, gs = run(True)
+    want, off = run(False)
+    assert off["launches"] == 0
+    assert gs["launches"] == k - 1, gs
+    assert 1 <= gs["instantiations"] <= 2, gs
+    assert gs["nodes"] > 0
+    for name in got:
+        assert got[name][1] == want[name][1], name
+        assert np.array_equal(got[name][0], want[name][0]), name
+
+
+def test_graph_replay_keeps_kernel_timing():
+    # The per-GEMM timing window rides inside the graph as event-record nodes.
+    with G.Session(workers=1) as s:
+        s.setGraphReplay(True)
+        m = build(s, 1, G.Precision.BF16, 1024, 2048, 1024)
+        pid = s.beginRecord()
+        step(s, m)
+        s.endRecord()
+        s.replay(pid)
+        s.timerStart()
+        for _ in range(3):
+            s.replay(pid, sync=False)
+        ms = s.timerStop()
+        (tot, cnt), = s.timerKernelMs()
+        assert s.graphStats()["launches"] == 3
+        assert ms > 0 and cnt == 9 and 0 < tot < ms * 1.01, (ms, tot, cnt)

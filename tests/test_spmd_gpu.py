@@ -54,9 +54,12 @@ def test_spmd_two_ranks_per_gpu_gloo_control_matches_single_gpu():
     n = _gpus()
     world = 8 if n >= 4 else (4 if n >= 2 else 2)
     # panel_min_gflop=0: the (small) check GEMMs take the in-GEMM panel
-    # pipelining path across ranks too
-    out = _run(world, "panel_min_gflop=0")
+    # pipelining path across ranks too; graph_replay=1: the FC step's replays
+    # run as one CUDA graph per rank (IPC flag waits / writes captured),
+    # checked against op-by-op replay in one process
+    out = _run(world, "panel_min_gflop=0,graph_replay=1")
     assert f"SPMD_CHECK world={world}" in out and "control=gloo" in out, out[-2000:]
+    assert "graph_launches=2 bitwise_vs_1process=True" in out, out[-2000:]
 
 
 @pytest.mark.timeout(1200)

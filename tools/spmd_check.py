@@ -166,13 +166,16 @@ def run(transport, nccl_id):
         # vs the same pipeline on one process with `world` workers on one GPU
         # (bf16: the replay runs gemm -> biasAdd -> relu as one fused GEMM on every rank)
         for fprec in (G.Precision.Single, G.Precision.BF16):
-            fc = fc_steps(s, 3, fprec)
+            g0 = s.graphStats()["launches"]
+            fc = fc_steps(s, 4, fprec)
+            graphs = s.graphStats()["launches"] - g0  # replays run as CUDA graphs (GM_DEBUG_CONFIG graph_replay=1)
             if rank == 0:
                 with G.Session(workers=world, devices=[local]) as s1:
-                    ref = fc_steps(s1, 3, fprec)
+                    s1.setGraphReplay(False)
+                    ref = fc_steps(s1, 4, fprec)
                 good = all(np.array_equal(fc[k].view(np.uint8), ref[k].view(np.uint8)) for k in fc)
                 say(f"[rank0 {plane}] FC step {fprec.name} record/replay (gemm, biasAdd, relu, reluGrad, rowcolsum, "
-                    f"axpy, replication) bitwise_vs_1process={good}")
+                    f"axpy, replication) graph_launches={graphs} bitwise_vs_1process={good}")
                 ok = ok and good
         # chunked async host streaming: upload A/B, gemm, download C
         n = 1024
