@@ -10,6 +10,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <type_traits>
 
 #include "convert.h"
 #include "fc_ops.h"
@@ -239,6 +240,36 @@ __device__ __forceinline__ void cp_async_wait() {
   asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
 }
 
+// s + widen(v) in one instruction: sm_100's mixed-precision add (PTX
+// add.rn.f32.bf16 / .f16, SASS FHADD[.BF16], which also reads the upper half
+// of a register directly). The 16-bit value converts to fp32 exactly, so the
+// result is the same round-to-nearest fp32 add as add_rn(s, widen(v)), with
+// no widen instruction on the ordered chain.
+template <int P>
+__device__ __forceinline__ float add_mixed(float s, uint16_t v) {
+  static_assert(P == 0 || P == 3, "16-bit storage only");
+  if constexpr (P == 3)
+    asm("add.rn.f32.bf16 %0, %1, %0;" : "+f"(s) : "h"(v));
+  else
+    asm("add.rn.f32.f16 %0, %1, %0;" : "+f"(s) : "h"(v));
+  return s;
+}
+template <int P>
+__device__ __forceinline__ float add_mixed2(float s, uint32_t word) {
+  uint16_t lo, hi;
+  asm("mov.b32 {%0, %1}, %2;" : "=h"(lo), "=h"(hi) : "r"(word));
+  return add_mixed<P>(add_mixed<P>(s, lo), hi);
+}
+// One step of an ordered line-sum chain: the mixed-precision add when the
+// chain is fp32 over 16-bit storage, else widen + add_rn.
+template <int P, typename T>
+__device__ __forceinline__ T fold_step(T s, typename Stor<P>::type v) {
+  if constexpr (std::is_same<T, float>::value && (P == 0 || P == 3))
+    return add_mixed<P>(s, static_cast<uint16_t>(v));
+  else
+    return add_rn(s, widen<P, T>(v));
+}
+
 template <typename T, int P>
 __global__ void __launch_bounds__(kAsThreads) line_sums_async_kernel(const void* __restrict__ a, uint64_t lda,
                                                                       uint64_t rows, uint64_t cols, int by_rows,
@@ -323,12 +354,12 @@ __global__ void __launch_bounds__(kAsThreads) line_sums_async_kernel(const void*
           } w;
           w.u = *reinterpret_cast<const uint4*>(row + v * 16);
 #pragma unroll
-          for (int k = 0; k < VE; ++k) sum = add_rn(sum, widen<P, T>(w.e[k]));
+          for (int k = 0; k < VE; ++k) sum = fold_step<P, T>(sum, w.e[k]);
         }
       } else {
         const S* col = reinterpret_cast<const S*>(st) + lane;
 #pragma unroll 64
-        for (int sr = 0; sr < kAsStep; ++sr) sum = add_rn(sum, widen<P, T>(col[sr * 32]));
+        for (int sr = 0; sr < kAsStep; ++sr) sum = fold_step<P, T>(sum, col[sr * 32]);
       }
     }
   }
@@ -350,6 +381,8 @@ __global__ void __launch_bounds__(kAsThreads) line_sums_async_kernel(const void*
 //            j ^ (o & 7), so the 8 lanes of an LDS.128 phase hit 8 banks);
 //   by cols: a stage is one box of 256 rows x 32 elements (lane o reads
 //            column o: a warp reads one contiguous 64-byte row).
+// The chain step is sm_100's mixed-precision add (add_mixed), one FHADD per
+// element with no separate widen.
 // Out-of-range box elements are zero-filled by TMA: exact, a chain starting
 // at +0 never holds -0.
 constexpr int kTsThreads = 64;
@@ -419,10 +452,7 @@ __global__ void __launch_bounds__(kTsThreads) line_sums_tma_kernel(const __grid_
         for (int j = 0; j < 8; ++j) {
           const uint32_t q[4] = {w[j].x, w[j].y, w[j].z, w[j].w};
 #pragma unroll
-          for (int k = 0; k < 4; ++k) {
-            sum = add_rn(sum, widen<P, T>(static_cast<S>(q[k] & 0xFFFFu)));
-            sum = add_rn(sum, widen<P, T>(static_cast<S>(q[k] >> 16)));
-          }
+          for (int k = 0; k < 4; ++k) sum = add_mixed2<P>(sum, q[k]);
         }
       }
     } else {
@@ -434,7 +464,7 @@ __global__ void __launch_bounds__(kTsThreads) line_sums_tma_kernel(const __grid_
 #pragma unroll
         for (int r = 0; r < 32; ++r) v[r] = col[(r0 + r) * 32];
 #pragma unroll
-        for (int r = 0; r < 32; ++r) sum = add_rn(sum, widen<P, T>(v[r]));
+        for (int r = 0; r < 32; ++r) sum = add_mixed<P>(sum, static_cast<uint16_t>(v[r]));
       }
     }
     __syncwarp();

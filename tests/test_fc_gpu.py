@@ -237,16 +237,19 @@ def test_row_col_sums_vs_c_restatement(prec, lay):
         assert same_bits(got_r, want_r, prec) and same_bits(got_c, want_c, prec), (prec, lay, det)
 
 
-@pytest.mark.parametrize("prec", [3, 1])
-@pytest.mark.parametrize("shape", [(600, 1000), (4096, 264), (33, 4104)])
+@pytest.mark.parametrize("prec", [3, 1, 0])
+@pytest.mark.parametrize("shape", [(600, 1000), (4096, 264), (33, 4104), (4096, 4096), (129, 4160)])
 def test_row_col_sums_aligned_rows_vs_c_restatement(prec, shape):
-    """16-byte aligned rows take the cp.async ring (256-element stages for
-    16-bit storage, 128 for Single): chains that end mid-stage and output
-    counts that are not multiples of 32, bit-for-bit."""
+    """16-byte aligned rows take the TMA-fed kernel for 16-bit storage
+    (256-element stages, mixed-precision FHADD chain steps) and the cp.async
+    ring for Single: chains that end mid-stage and output counts that are not
+    multiples of 32, bit-for-bit. Half inputs stay clear of subnormals
+    (the reference decodes those to half their IEEE value)."""
     rows, cols = shape
-    a = O.fill_uniform(rows, cols, prec, 41).reshape(rows, cols)
-    r = O.fill_uniform(rows, 1, prec, 42).reshape(rows, 1)
-    c = O.fill_uniform(1, cols, prec, 43).reshape(1, cols)
+    lo = 0.125 if prec == 0 else -1.0
+    a = O.fill_uniform(rows, cols, prec, 41, lo, 1.0).reshape(rows, cols)
+    r = O.fill_uniform(rows, 1, prec, 42, lo, 1.0).reshape(rows, 1)
+    c = O.fill_uniform(1, cols, prec, 43, lo, 1.0).reshape(1, cols)
     want_r, want_c = O.rowcolsum_c(1.0, a, prec, r, prec, c, prec)
     with G.Session(workers=1) as s:
         one = lambda rr, cc: G.makeSingleTileLayout(rr, cc, 0)

@@ -10,6 +10,7 @@ from paper_1611_07819_b200 import gridmath as G  # noqa: E402
 
 
 def timed(s, fn, reps=20):
+    """Issued from Python op by op: host-bound for ops under ~20 us."""
     fn()
     s.synchronize()
     s.timerStart()
@@ -18,10 +19,26 @@ def timed(s, fn, reps=20):
     return s.timerStop() / reps * 1e3  # us
 
 
+def timed_graph(s, fn, reps=20):
+    """reps ops recorded as a pipeline and replayed as one CUDA graph: the
+    device runs them back to back, so small ops show their device time."""
+    pid = s.beginRecord()
+    for _ in range(reps):
+        fn()
+    s.endRecord()
+    s.replay(pid)
+    s.replay(pid)
+    s.synchronize()
+    s.timerStart()
+    s.replay(pid, sync=False)
+    return s.timerStop() / reps * 1e3  # us
+
+
 def main():
     P = G.Precision.BF16
     b, fo, fi = 4096, 4096, 9216
     with G.Session(workers=1) as s:
+        s.setGraphReplay(True)
         one = lambda r, c: G.makeSingleTileLayout(r, c, 0)
         Z = s.createMatrix(b, fo, P, one(b, fo))
         D = s.createMatrix(b, fo, P, one(b, fo))
@@ -43,7 +60,16 @@ def main():
             "fillUniform (SplitMix64)": (timed(s, lambda: s.fillUniform(D, 77)), e),
         }
         for k, (us, byts) in res.items():
-            print(f"{k:30s} {us:8.1f} us  {byts / (us * 1e-6) / 1e9:8.1f} GB/s")
+            print(f"{k:30s} {us:8.1f} us  {byts / (us * 1e-6) / 1e9:8.1f} GB/s  (python issue)")
+        res = {
+            "addRowColSum (row+col sums)": (timed_graph(s, lambda: s.opIssue(7, [Z.id, R.id, C.id], 1.0, flags=(1,))), e),
+            "biasAdd": (timed_graph(s, lambda: s.opIssue(9, [Z.id, Bv.id, Z.id], flags=(5,))), 2 * e),
+            "relu": (timed_graph(s, lambda: s.opIssue(8, [Z.id, A.id], flags=(0,))), 2 * e),
+            "reluGrad": (timed_graph(s, lambda: s.opIssue(9, [Z.id, D.id, D.id], flags=(3,))), 3 * e),
+            "axpy W": (timed_graph(s, lambda: s.opIssue(9, [dW.id, W.id, W.id], -1e-3, flags=(2,))), 3 * fi * fo * 2),
+        }
+        for k, (us, byts) in res.items():
+            print(f"{k:30s} {us:8.1f} us  {byts / (us * 1e-6) / 1e9:8.1f} GB/s  (graph replay)")
 
 
 if __name__ == "__main__":
