@@ -361,6 +361,14 @@ int gm_session_set_graph_replay(gm_session* s, int32_t on);
 /* Launches, instantiations (over all pipelines) and node count of the last
  * captured replay graph. */
 int gm_session_graph_stats(gm_session* s, uint64_t* launches, uint64_t* instantiations, uint64_t* nodes);
+/* Developer timeline of later replays (not in the reference): with on != 0,
+ * every replay records device events on the first local worker's compute and
+ * comm streams at its start and after each replayed op. gm_session_op_timeline
+ * returns, for the last replay, the ms from its start at which each stream
+ * passed each op, and the op labels joined by '\n' into `labels`. */
+int gm_session_set_op_timeline(gm_session* s, int32_t on);
+int gm_session_op_timeline(gm_session* s, float* compute_ms, float* comm_ms, uint32_t cap, char* labels,
+                           uint32_t label_bytes, uint32_t* n);
 /* Device time of the last gm_gemm/gm_gemm_async per local worker (ms),
  * measured with CUDA events on the worker's compute stream. */
 int gm_last_op_device_ms(gm_session* s, float* ms, uint32_t cap, uint32_t* n);

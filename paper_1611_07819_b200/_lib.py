@@ -157,6 +157,9 @@ _SIGNATURES = {
     "gm_session_transport": ([c_void_p, _P(c_int32)], c_int32),
     "gm_session_set_panel_pipelining": ([c_void_p, c_int32], c_int32),
     "gm_session_set_graph_replay": ([c_void_p, c_int32], c_int32),
+    "gm_session_set_op_timeline": ([c_void_p, c_int32], c_int32),
+    "gm_session_op_timeline": ([c_void_p, _P(ctypes.c_float), _P(ctypes.c_float), c_uint32, ctypes.c_char_p, c_uint32,
+                                _P(c_uint32)], c_int32),
     "gm_session_graph_stats": ([c_void_p, _P(c_uint64), _P(c_uint64), _P(c_uint64)], c_int32),
     "gm_last_op_kernel_ms": ([c_void_p, _P(ctypes.c_float), c_uint32, _P(c_uint32)], c_int32),
     "gm_last_op_comm_ms": ([c_void_p, _P(ctypes.c_float), c_uint32, _P(c_uint32)], c_int32),

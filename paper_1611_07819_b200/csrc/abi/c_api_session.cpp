@@ -379,6 +379,32 @@ int gm_session_graph_stats(gm_session* s, uint64_t* launches, uint64_t* instanti
   });
 }
 
+int gm_session_set_op_timeline(gm_session* s, int32_t on) {
+  return guard([&] { s->s->setOpTimeline(on != 0); });
+}
+
+int gm_session_op_timeline(gm_session* s, float* compute_ms, float* comm_ms, uint32_t cap, char* labels,
+                           uint32_t label_bytes, uint32_t* n) {
+  return guard([&] {
+    const auto t = s->s->opTimeline();
+    *n = static_cast<uint32_t>(t.size());
+    std::string joined;
+    for (std::size_t i = 0; i < t.size(); ++i) {
+      if (i < cap) {
+        compute_ms[i] = t[i].computeMs;
+        comm_ms[i] = t[i].commMs;
+      }
+      joined += t[i].label;
+      joined += '\n';
+    }
+    if (label_bytes) {
+      const std::size_t k = std::min<std::size_t>(joined.size(), label_bytes - 1);
+      std::memcpy(labels, joined.data(), k);
+      labels[k] = '\0';
+    }
+  });
+}
+
 int gm_last_op_device_ms(gm_session* s, float* ms, uint32_t cap, uint32_t* n) {
   return guard([&] {
     const auto v = s->s->lastOpDeviceMs();

@@ -747,6 +747,10 @@ Session::~Session() {
   // worker goes away.
   for (auto& w : workers_)
     if (w) w->releaseReaders();
+  for (TimelineMark& m : timeline_) {
+    cudaEventDestroy(m.compute);
+    cudaEventDestroy(m.comm);
+  }
   graphs_.clear();
   workers_.clear();
 }
@@ -2606,6 +2610,28 @@ void Session::replay(std::uint64_t pipelineId, bool sync) {
 }
 
 void Session::replayOps(const std::vector<OpDescriptor>& ops) {
+  // Developer timeline (setOpTimeline): events on the first local worker's
+  // compute and comm streams at the start and after every replayed op.
+  Worker* tw = opTimeline_ && !localRanks().empty() ? local(localRanks().front()) : nullptr;
+  auto mark = [&](const char* label) {
+    if (!tw) return;
+    tw->activate();
+    TimelineMark m;
+    m.label = label;
+    cudaCheck(cudaEventCreate(&m.compute), "timeline");
+    cudaCheck(cudaEventCreate(&m.comm), "timeline");
+    cudaCheck(capture::recordTiming(m.compute, tw->compute), "timeline");
+    cudaCheck(capture::recordTiming(m.comm, tw->comm), "timeline");
+    timeline_.push_back(m);
+  };
+  if (tw) {
+    for (TimelineMark& m : timeline_) {
+      cudaEventDestroy(m.compute);
+      cudaEventDestroy(m.comm);
+    }
+    timeline_.clear();
+    mark("start");
+  }
   for (std::size_t i = 0; i < ops.size(); ++i) {
     OpDescriptor step = ops[i];
     step.execId = 0;
@@ -2617,6 +2643,7 @@ void Session::replayOps(const std::vector<OpDescriptor>& ops) {
       capture::checkpoint("replay: before gemm+biasAdd+relu");
       runGemmBiasRelu(step, bo, ro);
       capture::checkpoint("replay: gemm+biasAdd+relu");
+      mark("gemm+biasAdd+relu");
       i += 2;
       continue;
     }
@@ -2637,11 +2664,32 @@ void Session::replayOps(const std::vector<OpDescriptor>& ops) {
       default:
         throw Error("replay: op not supported on the B200 GEMM path");
     }
-    capture::checkpoint(step.opcode == OpCode::Gemm             ? "replay: gemm"
-                        : step.opcode == OpCode::ReplicateStart ? "replay: replicate"
-                        : step.opcode == OpCode::AddRowColSum   ? "replay: addRowColSum"
-                                                                : "replay: pointwise");
+    const char* what = step.opcode == OpCode::Gemm             ? "replay: gemm"
+                       : step.opcode == OpCode::ReplicateStart ? "replay: replicate"
+                       : step.opcode == OpCode::AddRowColSum   ? "replay: addRowColSum"
+                       : step.opcode == OpCode::SetConst       ? "replay: setConst"
+                       : step.opcode == OpCode::EwUnary        ? "replay: unary"
+                                                               : "replay: binary";
+    capture::checkpoint(what);
+    mark(what + 8);
   }
+}
+
+std::vector<Session::TimelineEntry> Session::opTimeline() {
+  std::vector<TimelineEntry> out;
+  if (timeline_.empty()) return out;
+  Worker* tw = local(localRanks().front());
+  tw->activate();
+  for (const TimelineMark& m : timeline_) {
+    TimelineEntry e;
+    e.label = m.label;
+    cudaCheck(cudaEventSynchronize(m.compute), "timeline");
+    cudaCheck(cudaEventSynchronize(m.comm), "timeline");
+    cudaCheck(cudaEventElapsedTime(&e.computeMs, timeline_.front().compute, m.compute), "timeline");
+    cudaCheck(cudaEventElapsedTime(&e.commMs, timeline_.front().compute, m.comm), "timeline");
+    out.push_back(e);
+  }
+  return out;
 }
 
 bool Session::fusableBiasRelu(const std::vector<OpDescriptor>& ops, std::size_t i) const {

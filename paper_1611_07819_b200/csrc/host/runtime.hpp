@@ -445,6 +445,15 @@ class Session {
     std::uint64_t launches = 0, instantiations = 0, nodes = 0;  // nodes: last captured graph
   };
   GraphStats graphStats() const { return graphStats_; }
+  // Developer timeline of the next replays: device time (ms, from the
+  // replay's start on the first local worker's compute stream) at which its
+  // compute and comm streams passed the end of each replayed op.
+  void setOpTimeline(bool on) { opTimeline_ = on; }
+  struct TimelineEntry {
+    std::string label;
+    float computeMs = 0.0f, commMs = 0.0f;
+  };
+  std::vector<TimelineEntry> opTimeline();
 
   ReplicationHandle replicateAsync(DistMatrix m);
   void replicateSync(DistMatrix m);
@@ -582,6 +591,12 @@ class Session {
   // so it is destroyed before them).
   std::map<std::uint64_t, std::unique_ptr<capture::Graph>> graphs_;
   std::optional<bool> graphReplay_;
+  struct TimelineMark {
+    std::string label;
+    cudaEvent_t compute = nullptr, comm = nullptr;
+  };
+  bool opTimeline_ = false;
+  std::vector<TimelineMark> timeline_;
   GraphStats graphStats_;
   std::map<std::pair<std::uint64_t, std::uint64_t>, bool> replFailed_;
   std::uint64_t nextMatrixId_ = 1;

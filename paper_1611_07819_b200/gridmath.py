@@ -411,6 +411,20 @@ class Session:
         check(_lib.load().gm_session_graph_stats(self._h, ctypes.byref(a), ctypes.byref(b), ctypes.byref(c)))
         return {"launches": a.value, "instantiations": b.value, "nodes": c.value}
 
+    def setOpTimeline(self, on: bool):
+        """Developer: record a per-op device timeline of later replays."""
+        check(_lib.load().gm_session_set_op_timeline(self._h, 1 if on else 0))
+
+    def opTimeline(self) -> List[tuple]:
+        """[(label, compute_ms, comm_ms)] of the last replay (first local worker)."""
+        cap = 256
+        cm, co = (ctypes.c_float * cap)(), (ctypes.c_float * cap)()
+        lab = ctypes.create_string_buffer(8192)
+        n = ctypes.c_uint32()
+        check(_lib.load().gm_session_op_timeline(self._h, cm, co, cap, lab, 8192, ctypes.byref(n)))
+        labels = lab.value.decode().split("\n")
+        return [(labels[i], cm[i], co[i]) for i in range(min(n.value, cap))]
+
     def timerStart(self):
         check(_lib.load().gm_timer_start(self._h))
 

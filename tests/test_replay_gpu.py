@@ -279,3 +279,18 @@ def test_graph_replay_keeps_kernel_timing():
         (tot, cnt), = s.timerKernelMs()
         assert s.graphStats()["launches"] == 3
         assert ms > 0 and cnt == 9 and 0 < tot < ms * 1.01, (ms, tot, cnt)
+
+
+def test_op_timeline_marks_every_replayed_op():
+    with G.Session(workers=2) as s:
+        m = build(s, 2)
+        pid = s.beginRecord()
+        step(s, m)
+        s.endRecord()
+        s.setOpTimeline(True)
+        s.replay(pid)
+        tl = s.opTimeline()
+        assert tl[0][0] == "start" and len(tl) == 1 + 13, tl  # 13 recorded ops (Single: nothing fused)
+        comp = [c for _, c, _ in tl]
+        assert comp == sorted(comp) and comp[-1] > 0, tl
+        assert [lab for lab, _, _ in tl[1:4]] == ["gemm", "binary", "unary"], tl
