@@ -272,6 +272,7 @@ Worker::Worker(std::uint32_t r, int dev, std::uint64_t budget)
   cudaCheck(cudaStreamCreateWithFlags(&h2d, cudaStreamNonBlocking), "worker: h2d stream");
   cudaCheck(cudaStreamCreateWithFlags(&d2h, cudaStreamNonBlocking), "worker: d2h stream");
   cudaCheck(cudaStreamCreateWithFlags(&aux, cudaStreamNonBlocking), "worker: aux stream");
+  cudaCheck(cudaStreamCreateWithPriority(&flagPub, cudaStreamNonBlocking, hi), "worker: flag stream");
   for (cudaStream_t& ps : pulls)
     cudaCheck(cudaStreamCreateWithPriority(&ps, cudaStreamNonBlocking, hi), "worker: pull stream");
   cudaCheck(cudaEventCreate(&tStart), "worker: event");
@@ -309,6 +310,7 @@ Worker::~Worker() {
   cudaStreamSynchronize(h2d);
   cudaStreamSynchronize(d2h);
   cudaStreamSynchronize(aux);
+  cudaStreamSynchronize(flagPub);
   for (cudaStream_t ps : pulls) cudaStreamSynchronize(ps);
   for (auto& kv : uploads) {
     for (auto& c : kv.second.chunks) cudaEventDestroy(c.done);
@@ -342,6 +344,7 @@ Worker::~Worker() {
   cudaStreamDestroy(compute);
   cudaStreamDestroy(comm);
   cudaStreamDestroy(h2d);
+  cudaStreamDestroy(flagPub);
   cudaStreamDestroy(d2h);
   cudaStreamDestroy(aux);
   for (cudaStream_t ps : pulls) cudaStreamDestroy(ps);
@@ -634,9 +637,28 @@ void Session::flushWritten(std::uint64_t before) {
       // stream, after its last chunk (the compute stream has not joined it).
       cudaStream_t ws = w.uploads.count(pw.first) ? w.h2d : w.compute;
       cudaCheck(capture::record(e, ws), "worker: record write");
-      if (ipc_) ipcWrite(ws, w.flags + slotOf(pw.first), pw.second);
+      if (ipc_) {
+        // A compute-stream write is published when a peer first pulls the
+        // matrix (publishWritten): a flag write between kernels costs ~3 us
+        // of compute-stream time (tools/dev/memop_probe.cu).
+        if (ws == w.compute && gmk::debug_config().lazy_written) {
+          unpublished_[pw.first] = pw.second;
+        } else {
+          unpublished_.erase(pw.first);
+          ipcWrite(ws, w.flags + slotOf(pw.first), pw.second);
+        }
+      }
     }
   }
+}
+
+void Session::publishWritten(Worker& w, std::uint64_t matrix) {
+  auto it = unpublished_.find(matrix);
+  if (it == unpublished_.end()) return;
+  w.activate();
+  cudaCheck(capture::wait(w.flagPub, w.lastWrite.at(matrix), 0), "publish write");
+  ipcWrite(w.flagPub, w.flags + slotOf(matrix), it->second);
+  unpublished_.erase(it);
 }
 
 // Consumers publish readDone[stream][slot] = exec id once this op's pulls
@@ -1023,6 +1045,7 @@ void Session::destroy(DistMatrix m) {
 }
 
 void Session::execDestroy(std::uint64_t id) {
+  unpublished_.erase(id);
   forEachLocal([&](Worker& w) {
     w.joinUpload(id);
     w.dropChunkDone(id);
@@ -1415,8 +1438,10 @@ void Session::exchange(std::vector<Xfer>& xs, bool onComm, bool commit, int maxP
       Worker* d = local(x.dst);
       Worker* s = local(x.src);
       if (!d) {
-        // Producer side of a peer's pull: remember the reader (WAR).
+        // Producer side of a peer's pull: publish the write it waits for,
+        // remember the reader (WAR).
         if (s) {
+          publishWritten(*s, x.matrix);
           s->bytesSent += bytes;
           std::uint64_t& last = remoteReaders_[x.matrix][{x.dst, sIdx}];
           last = std::max(last, curExec_);
@@ -2399,6 +2424,7 @@ void Session::synchronize() {
     cudaCheck(cudaStreamSynchronize(w.comm), "sync comm");
     cudaCheck(cudaStreamSynchronize(w.compute), "sync compute");
     cudaCheck(cudaStreamSynchronize(w.d2h), "sync d2h");
+    cudaCheck(cudaStreamSynchronize(w.flagPub), "sync flags");
   });
 }
 
@@ -2584,7 +2610,7 @@ void Session::replay(std::uint64_t pipelineId, bool sync) {
         capture::WorkerStreams x;
         x.device = w.device;
         x.compute = w.compute;
-        x.side = {w.comm, w.aux, w.h2d, w.d2h};
+        x.side = {w.comm, w.aux, w.h2d, w.d2h, w.flagPub};
         for (cudaStream_t ps : w.pulls) x.side.push_back(ps);
         ws.push_back(x);
       }

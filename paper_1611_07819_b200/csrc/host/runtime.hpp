@@ -314,6 +314,9 @@ class Worker {
   // Forked from and joined back into `compute` inside one op (e.g. the
   // column sums of addRowColSum run beside the row sums).
   cudaStream_t aux = nullptr;
+  // SPMD copy-engine plane: written[slot] flags are published here, behind
+  // the write's event, when a peer first pulls the matrix (not on compute).
+  cudaStream_t flagPub = nullptr;
   // Copy-engine pull streams: one exchange's pieces from different source
   // workers run on different streams (different copy engines), forked from
   // and joined back into the comm or compute stream.
@@ -628,6 +631,10 @@ class Session {
   std::uint64_t curExec_ = 0;                              // exec id of the op being executed
   std::map<std::uint64_t, std::uint64_t> lastMut_;         // matrix -> exec id of its last write
   std::vector<std::pair<std::uint64_t, std::uint64_t>> pendingWritten_;  // (matrix, exec id)
+  // Writes of local tiles whose written[slot] flag is not published yet
+  // (matrix -> exec id): published on flagPub when a peer pulls the matrix.
+  std::map<std::uint64_t, std::uint64_t> unpublished_;
+  void publishWritten(Worker& w, std::uint64_t matrix);
   std::map<std::uint64_t, std::uint32_t> slots_;           // matrix -> flag slot (same on all ranks)
   std::vector<std::uint32_t> freeSlots_;
   std::uint32_t nextSlot_ = 0;
