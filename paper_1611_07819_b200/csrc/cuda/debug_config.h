@@ -28,7 +28,8 @@ struct DebugConfig {
   int pull_streams = 0;    // copy-engine pull streams per exchange (0 = all)
   int fuse_epilogue = 1;   // 0 = replay does not fuse gemm -> biasAdd -> relu
   int tf32_chunk = 256;    // Single-compute k-chunk folded into the fp32 running sum
-  int lazy_written = 1;    // 0 = publish written[slot] flags on the compute stream after every write
+  int lazy_written = 1;
+  int war_side = 1;        // 0 = peers' readDone waits go straight onto the mutating stream    // 0 = publish written[slot] flags on the compute stream after every write
   int graph_replay = 0;    // 1 = replays after the first run as one captured CUDA graph
   int verbose = 0;         // 1 = log every GEMM launch configuration to stderr
 };

@@ -273,6 +273,7 @@ Worker::Worker(std::uint32_t r, int dev, std::uint64_t budget)
   cudaCheck(cudaStreamCreateWithFlags(&d2h, cudaStreamNonBlocking), "worker: d2h stream");
   cudaCheck(cudaStreamCreateWithFlags(&aux, cudaStreamNonBlocking), "worker: aux stream");
   cudaCheck(cudaStreamCreateWithPriority(&flagPub, cudaStreamNonBlocking, hi), "worker: flag stream");
+  cudaCheck(cudaStreamCreateWithPriority(&warWait, cudaStreamNonBlocking, hi), "worker: WAR stream");
   for (cudaStream_t& ps : pulls)
     cudaCheck(cudaStreamCreateWithPriority(&ps, cudaStreamNonBlocking, hi), "worker: pull stream");
   cudaCheck(cudaEventCreate(&tStart), "worker: event");
@@ -311,6 +312,7 @@ Worker::~Worker() {
   cudaStreamSynchronize(d2h);
   cudaStreamSynchronize(aux);
   cudaStreamSynchronize(flagPub);
+  cudaStreamSynchronize(warWait);
   for (cudaStream_t ps : pulls) cudaStreamSynchronize(ps);
   for (auto& kv : uploads) {
     for (auto& c : kv.second.chunks) cudaEventDestroy(c.done);
@@ -345,6 +347,7 @@ Worker::~Worker() {
   cudaStreamDestroy(comm);
   cudaStreamDestroy(h2d);
   cudaStreamDestroy(flagPub);
+  cudaStreamDestroy(warWait);
   cudaStreamDestroy(d2h);
   cudaStreamDestroy(aux);
   for (cudaStream_t ps : pulls) cudaStreamDestroy(ps);
@@ -649,6 +652,21 @@ void Session::flushWritten(std::uint64_t before) {
         }
       }
     }
+  }
+}
+
+void Session::waitRemoteReaders(Worker& w, std::uint64_t matrix, cudaStream_t ws) {
+  auto rr = remoteReaders_.find(matrix);
+  if (rr == remoteReaders_.end() || rr->second.empty()) return;
+  const bool side = gmk::debug_config().war_side != 0;
+  cudaStream_t q = side ? w.warWait : ws;
+  for (const auto& rd : rr->second)
+    ipcWait(q, peerFlags_[rd.first.first] + kSlots * (1 + rd.first.second) + slotOf(matrix), rd.second);
+  if (side) {
+    cudaEvent_t e = w.event();
+    cudaCheck(capture::record(e, q), "WAR: record");
+    cudaCheck(capture::wait(ws, e, 0), "WAR: wait");
+    w.recycle(e);
   }
 }
 
@@ -957,10 +975,7 @@ void Session::mutationHook(std::uint64_t id, std::uint64_t oldVersion, bool toH2
     }
     // Peers that pulled from this worker's tiles of the matrix (SPMD
     // copy-engine plane) must be done before it changes.
-    auto rr = remoteReaders_.find(id);
-    if (rr != remoteReaders_.end() && w.tiles.count(id))
-      for (const auto& rd : rr->second)
-        ipcWait(ws, peerFlags_[rd.first.first] + kSlots * (1 + rd.first.second) + slotOf(id), rd.second);
+    if (w.tiles.count(id)) waitRemoteReaders(w, id, ws);
   }
   remoteReaders_.erase(id);
   for (std::uint32_t r = 0; r < opts_.workers; ++r)
@@ -2425,6 +2440,7 @@ void Session::synchronize() {
     cudaCheck(cudaStreamSynchronize(w.compute), "sync compute");
     cudaCheck(cudaStreamSynchronize(w.d2h), "sync d2h");
     cudaCheck(cudaStreamSynchronize(w.flagPub), "sync flags");
+    cudaCheck(cudaStreamSynchronize(w.warWait), "sync WAR waits");
   });
 }
 
@@ -2610,7 +2626,7 @@ void Session::replay(std::uint64_t pipelineId, bool sync) {
         capture::WorkerStreams x;
         x.device = w.device;
         x.compute = w.compute;
-        x.side = {w.comm, w.aux, w.h2d, w.d2h, w.flagPub};
+        x.side = {w.comm, w.aux, w.h2d, w.d2h, w.flagPub, w.warWait};
         for (cudaStream_t ps : w.pulls) x.side.push_back(ps);
         ws.push_back(x);
       }
@@ -2784,10 +2800,7 @@ void Session::runGemmBiasRelu(const OpDescriptor& g0, const OpDescriptor& bo0, c
   forEachLocal([&](Worker& w) {
     if (!w.tiles.count(act)) return;
     w.beforeMutation(act, w.compute);
-    auto rr = remoteReaders_.find(act);
-    if (rr != remoteReaders_.end())
-      for (const auto& rd : rr->second)
-        ipcWait(w.compute, peerFlags_[rd.first.first] + kSlots * (1 + rd.first.second) + slotOf(act), rd.second);
+    waitRemoteReaders(w, act, w.compute);
   });
   issue(g);
   fused_ = &f;

@@ -317,6 +317,9 @@ class Worker {
   // SPMD copy-engine plane: written[slot] flags are published here, behind
   // the write's event, when a peer first pulls the matrix (not on compute).
   cudaStream_t flagPub = nullptr;
+  // ...and peers' readDone flags are awaited here before a mutation (the
+  // compute stream then waits on one event instead of one memop per reader).
+  cudaStream_t warWait = nullptr;
   // Copy-engine pull streams: one exchange's pieces from different source
   // workers run on different streams (different copy engines), forked from
   // and joined back into the comm or compute stream.
@@ -635,6 +638,9 @@ class Session {
   // (matrix -> exec id): published on flagPub when a peer pulls the matrix.
   std::map<std::uint64_t, std::uint64_t> unpublished_;
   void publishWritten(Worker& w, std::uint64_t matrix);
+  // WAR on the SPMD plane: `ws` waits until every peer that pulled worker w's
+  // tiles of `matrix` has published readDone for those pulls.
+  void waitRemoteReaders(Worker& w, std::uint64_t matrix, cudaStream_t ws);
   std::map<std::uint64_t, std::uint32_t> slots_;           // matrix -> flag slot (same on all ranks)
   std::vector<std::uint32_t> freeSlots_;
   std::uint32_t nextSlot_ = 0;
