@@ -26,6 +26,7 @@ struct DebugConfig {
   int b_chunk_cols = 0;    // pipelined B block columns (0 = auto)
   int ready_slots = 0;     // ready-flag ring slots per worker (0 = 65536; small values test reuse)
   int pull_streams = 0;    // copy-engine pull streams per exchange (0 = all)
+  int fuse_zero_sums = 1;  // 0 = replay runs setConst(0) x2 before addRowColSum as kernels
   int fuse_epilogue = 1;   // 0 = replay does not fuse gemm -> biasAdd -> relu
   int tf32_chunk = 256;    // Single-compute k-chunk folded into the fp32 running sum
   int lazy_written = 1;

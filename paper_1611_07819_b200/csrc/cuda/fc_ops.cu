@@ -39,6 +39,16 @@ __device__ __forceinline__ T ew_eval(int kind, T xv, const EwView& y, uint64_t y
 // Generic path (operands of different storage precisions): blockIdx.y
 // strides rows, threads stride columns, so every warp touches one contiguous
 // row segment of each operand; the kind and precision switches are uniform.
+// Line-sum output: acc[idx] = acc[idx] + alpha * sum, or 0 + alpha * sum
+// when the caller zeroed the outputs by definition (kLineSumsZeroAcc in
+// acc_prec: the replay peephole that folds setConst(0) into the sums).
+template <typename T>
+__device__ __forceinline__ void line_sum_out(void* acc, int acc_prec, uint64_t idx, T alpha, T sum) {
+  const int p = acc_prec & 0xFF;
+  const T cur = (acc_prec & kLineSumsZeroAcc) ? T(0) : load_as<T>(acc, p, idx);
+  store_as(acc, p, idx, add_rn(cur, mul_rn(alpha, sum)));
+}
+
 template <typename T>
 __global__ void ew_kernel(EwView x, EwView y, int ybc, void* __restrict__ d, uint64_t dld, int dprec,
                           uint64_t rows, uint64_t cols, int kind, T alpha) {
@@ -209,8 +219,7 @@ __global__ void __launch_bounds__(kLsThreads) line_sums_kernel(EwView a, uint64_
   }
   if (tid < kOut && o0 + tid < outs) {
     const uint64_t idx = (o0 + tid) * acc_stride;
-    const T cur = load_as<T>(acc, acc_prec, idx);
-    store_as(acc, acc_prec, idx, add_rn(cur, mul_rn(alpha, sum)));
+    line_sum_out<T>(acc, acc_prec, idx, alpha, sum);
   }
 }
 
@@ -366,8 +375,7 @@ __global__ void __launch_bounds__(kAsThreads) line_sums_async_kernel(const void*
   cp_async_wait<0>();
   if (folder && o0 + lane < outs) {
     const uint64_t idx = (o0 + lane) * acc_stride;
-    const T cur = load_as<T>(acc, acc_prec, idx);
-    store_as(acc, acc_prec, idx, add_rn(cur, mul_rn(alpha, sum)));
+    line_sum_out<T>(acc, acc_prec, idx, alpha, sum);
   }
 }
 
@@ -472,8 +480,7 @@ __global__ void __launch_bounds__(kTsThreads) line_sums_tma_kernel(const __grid_
   }
   if (o0 + lane < outs) {
     const uint64_t idx = (o0 + lane) * acc_stride;
-    const T cur = load_as<T>(acc, acc_prec, idx);
-    store_as(acc, acc_prec, idx, add_rn(cur, mul_rn(alpha, sum)));
+    line_sum_out<T>(acc, acc_prec, idx, alpha, sum);
   }
 }
 

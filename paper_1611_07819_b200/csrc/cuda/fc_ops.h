@@ -36,6 +36,9 @@ cudaError_t ew_apply(EwView x, EwView y, int y_row_bcast, void* dst, uint64_t dl
 // Every element of the rows x cols rectangle = value (storeScalar<double>).
 cudaError_t set_const(void* dst, uint64_t ld, int prec, uint64_t rows, uint64_t cols, double value,
                       cudaStream_t s);
+// acc_prec | kLineSumsZeroAcc: the outputs count as zero (acc[o] = 0 + alpha
+// * sum, bit-for-bit a setConst(0) followed by the sums).
+constexpr int kLineSumsZeroAcc = 0x100;
 // acc[o] = acc[o] + alpha * sum, one sum per row (by_rows) or per column of
 // the rows x cols band, accumulated in ascending index order in the compute
 // type (bit-for-bit the reference's runRowColSumDet chain). acc element o

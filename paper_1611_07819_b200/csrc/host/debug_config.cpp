@@ -28,7 +28,7 @@ const DebugConfig& debug_config() {
                         {"b_chunk_cols", &c.b_chunk_cols},
                         {"pull_streams", &c.pull_streams}, {"fuse_epilogue", &c.fuse_epilogue},
                         {"tf32_chunk", &c.tf32_chunk},     {"verbose", &c.verbose},
-                        {"graph_replay", &c.graph_replay}, {"lazy_written", &c.lazy_written}, {"war_side", &c.war_side}};
+                        {"graph_replay", &c.graph_replay}, {"lazy_written", &c.lazy_written}, {"war_side", &c.war_side}, {"fuse_zero_sums", &c.fuse_zero_sums}};
     std::string s(env);
     std::size_t pos = 0;
     while (pos < s.size()) {

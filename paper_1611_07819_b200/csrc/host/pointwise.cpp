@@ -234,7 +234,9 @@ void Session::runPointwise(const OpDescriptor& op0, bool sync) {
     const gmk::EwView xv{xn.view.ptr, xn.view.ld, static_cast<int>(X.precision)};
     if (sums) {
       cudaCheck(gmk::line_sums(xv, xn.rect.rows(), xn.rect.cols(), j.byRows ? 1 : 0, tile->ptr,
-                               j.byRows ? tile->ld : 1, static_cast<int>(T.precision), op.s0, dbl ? 1 : 0,
+                               j.byRows ? tile->ld : 1,
+                               static_cast<int>(T.precision) | (zeroSums_ ? gmk::kLineSumsZeroAcc : 0), op.s0,
+                               dbl ? 1 : 0,
                                j.byRows || !forked.count(w) ? w->compute : w->aux),
                 "addRowColSum");
       continue;

@@ -2689,6 +2689,29 @@ void Session::replayOps(const std::vector<OpDescriptor>& ops) {
       i += 2;
       continue;
     }
+    if (fusableZeroSums(ops, i)) {
+      for (std::size_t k = i; k < i + 2; ++k) {
+        OpDescriptor sc = ops[k];
+        sc.execId = 0;
+        sc.recordPipeline = 0;
+        issue(sc);  // versions, hazards, invalidation; no kernel
+      }
+      OpDescriptor rcs = ops[i + 2];
+      rcs.execId = 0;
+      rcs.recordPipeline = 0;
+      zeroSums_ = true;
+      try {
+        runPointwise(rcs, false);
+      } catch (...) {
+        zeroSums_ = false;
+        throw;
+      }
+      zeroSums_ = false;
+      capture::checkpoint("replay: setConst x2 + addRowColSum");
+      mark("setConst+setConst+addRowColSum");
+      i += 2;
+      continue;
+    }
     capture::checkpoint("replay: before op");
     switch (step.opcode) {
       case OpCode::Gemm:
@@ -2732,6 +2755,18 @@ std::vector<Session::TimelineEntry> Session::opTimeline() {
     out.push_back(e);
   }
   return out;
+}
+
+bool Session::fusableZeroSums(const std::vector<OpDescriptor>& ops, std::size_t i) const {
+  if (!gmk::debug_config().fuse_zero_sums || i + 2 >= ops.size()) return false;
+  const OpDescriptor& a = ops[i];
+  const OpDescriptor& b = ops[i + 1];
+  const OpDescriptor& r = ops[i + 2];
+  if (a.opcode != OpCode::SetConst || b.opcode != OpCode::SetConst || r.opcode != OpCode::AddRowColSum) return false;
+  if (a.s0 != 0.0 || b.s0 != 0.0 || a.ids[0] == b.ids[0]) return false;
+  const std::uint64_t R = r.ids[1], C = r.ids[2];
+  if (R == C || r.ids[0] == R || r.ids[0] == C) return false;
+  return (a.ids[0] == R && b.ids[0] == C) || (a.ids[0] == C && b.ids[0] == R);
 }
 
 bool Session::fusableBiasRelu(const std::vector<OpDescriptor>& ops, std::size_t i) const {

@@ -511,6 +511,11 @@ class Session {
   const FusedBiasRelu* fused_ = nullptr;
   bool fusableBiasRelu(const std::vector<OpDescriptor>& ops, std::size_t i) const;
   void replayOps(const std::vector<OpDescriptor>& ops);
+  // Replay peephole: setConst(R, 0) and setConst(C, 0) right before
+  // addRowColSum(X, R, C) issue only their metadata; the sums then write
+  // 0 + alpha * sum (same bits, two launches fewer).
+  bool fusableZeroSums(const std::vector<OpDescriptor>& ops, std::size_t i) const;
+  bool zeroSums_ = false;
   void runGemmBiasRelu(const OpDescriptor& g, const OpDescriptor& bo, const OpDescriptor& ro);
   // FC-layer neighbours on device (reference session.cpp:547-609,
   // kernels.cpp:435-815): SetConst, EwUnary, EwBinary, AddRowColSum.

@@ -126,8 +126,10 @@ def test_recording_errors_like_reference():
 
 
 def test_replay_fuses_bias_relu_into_the_gemm():
-    # The bf16 step's replay launches two kernels fewer than the eager step
-    # (biasAdd and relu ride in the forward GEMM's epilogue); Single does not fuse.
+    # The bf16 step's replay launches four kernels fewer than the eager step:
+    # biasAdd and relu ride in the forward GEMM's epilogue, and the two
+    # setConst(0) before addRowColSum become the sums' zero start. Single only
+    # takes the second peephole.
     counts = {}
     for prec in (G.Precision.BF16, G.Precision.Single):
         with G.Session(workers=1) as s:
@@ -144,9 +146,9 @@ def test_replay_fuses_bias_relu_into_the_gemm():
             n2 = G.kernel_launches()
             counts[prec] = (n1 - n0, n2 - n1)
     eager, replayed = counts[G.Precision.BF16]
-    assert replayed == eager - 2, counts
+    assert replayed == eager - 4, counts
     eager, replayed = counts[G.Precision.Single]
-    assert replayed == eager, counts
+    assert replayed == eager - 2, counts
 
 
 def test_fused_epilogue_not_used_when_bias_needs_a_transfer():
@@ -290,7 +292,39 @@ def test_op_timeline_marks_every_replayed_op():
         s.setOpTimeline(True)
         s.replay(pid)
         tl = s.opTimeline()
-        assert tl[0][0] == "start" and len(tl) == 1 + 13, tl  # 13 recorded ops (Single: nothing fused)
+        # 13 recorded ops; setConst x2 + addRowColSum replay as one mark (zero-sums peephole)
+        assert tl[0][0] == "start" and len(tl) == 1 + 11, tl
+        assert any(lab == "setConst+setConst+addRowColSum" for lab, _, _ in tl), tl
         comp = [c for _, c, _ in tl]
         assert comp == sorted(comp) and comp[-1] > 0, tl
         assert [lab for lab, _, _ in tl[1:4]] == ["gemm", "binary", "unary"], tl
+
+
+def test_zero_sums_peephole_matches_setconst_then_sums():
+    # setConst(R, 0), setConst(C, 0), addRowColSum(X, R, C) replayed with the
+    # peephole (sums start from zero, no setConst kernels) == the three ops
+    # run one by one, bit-for-bit and version-for-version, also when R and C
+    # held other values before and alpha is negative (a -0 product stays +0).
+    def run(fuse, p, prec):
+        with G.Session(workers=p) as s:
+            m = build(s, p, prec)
+            G.setConst(s, m["R"], 3.5)
+            G.setConst(s, m["DB"], -2.0)
+            pid = s.beginRecord()
+            G.setConst(s, m["R"], 0.0)
+            G.setConst(s, m["DB"], 0.0)
+            G.addRowColSum(s, m["D"], m["R"], m["DB"], -0.75, True)
+            s.endRecord()
+            G.setConst(s, m["R"], 7.0)
+            if not fuse:
+                G.setConst(s, m["R"], 0.0)
+                G.setConst(s, m["DB"], 0.0)
+                G.addRowColSum(s, m["D"], m["R"], m["DB"], -0.75, True)
+            else:
+                s.replay(pid)
+            return {k: (s.getDataRaw(m[k]), m[k].version()) for k in ("R", "DB")}
+    for p, prec in ((1, G.Precision.BF16), (2, G.Precision.Single), (3, G.Precision.BF16)):
+        got, want = run(True, p, prec), run(False, p, prec)
+        for k in got:
+            assert got[k][1] == want[k][1], (k, p, prec)
+            assert np.array_equal(got[k][0], want[k][0]), (k, p, prec)
